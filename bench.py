@@ -1,0 +1,451 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 chunk step: reduce-scatter -> fused Adam -> all-gather
+over the ZeRO-3 chunk shards of a planner layout (BASELINE.json metric
+"chunk step GB/s (gather+RS+fused Adam) vs HBM/NVLink roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|flat512 ...]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference ...     # CPU reference arm (oracle port)
+
+One step = one pass of the data plane over every chunk of the workload with
+inputs resident in HBM: per chunk RS (w>1), fused Adam on the owned shard
+(with grad-norm/overflow statistics), AG (w>1). `value` = algorithmic bytes
+of all ranks / max-over-ranks device time; `e2e` = the same
+metric through the C-ABI with pinned HOST gradient / parameter buffers, the
+H2D of the step's gradients and D2H of its parameters (and the grad-norm
+readback) inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+GOLDEN = os.path.join(REPO, "tests", "golden")
+PEAKS_FILE = os.path.join(REPO, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0      # B200_PROFILING.md fallback
+NVLINK_GBS = 770.0             # measured peer copy per direction (B200_PROFILING.md)
+
+WORKLOADS = {
+    # name: (description, layout source)
+    "cfg2": ("GPT-2 1.5B (h1600 L48 25 heads) b8, 3x1GiB chunks, all persistent, ZeRO-3 sharded",
+             "layout:gpt2-1.5b_b8"),
+    "cfg1": ("gpt2-1b b2 (reference test model), 4x512MiB chunks, all persistent",
+             "layout:gpt2-1b_b2"),
+    "flat32": ("flat 32 MiB chunk sweep point", "flat:33554432"),
+    "flat64": ("flat 64 MiB chunk", "flat:67108864"),
+    "flat128": ("flat 128 MiB chunk", "flat:134217728"),
+    "flat256": ("flat 256 MiB chunk", "flat:268435456"),
+    "flat512": ("flat 512 MiB chunk", "flat:536870912"),
+}
+
+
+def chunk_numels(workload: str) -> tuple[list[int], str]:
+    desc, src = WORKLOADS[workload]
+    kind, arg = src.split(":", 1)
+    if kind == "flat":
+        return [int(arg) // 2], desc
+    # The chunk table comes from the planner (pack_chunks / chunk_size_search);
+    # the clean-room planner's output is byte-identical to the committed
+    # reference golden (tests/test_planner_golden.py), which is read here.
+    from paper_2406_08334_b200 import planner
+    layout = planner.layout_for(arg)
+    return [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]], desc
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for k, name in enumerate(names):
+                if r[5 + k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def make_comm(world, rank):
+    """NCCL communicator of libptk; the unique id travels over the gloo group."""
+    from paper_2406_08334_b200 import _native as nat
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return None
+    uid = (ctypes.c_uint8 * nat.PTK_UNIQUE_ID_BYTES)()
+    if rank == 0:
+        nat.lib.ptk_comm_unique_id(uid)
+    t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+    dist.broadcast(t, 0)
+    uid = (ctypes.c_uint8 * nat.PTK_UNIQUE_ID_BYTES)(*t.tolist())
+    comm = ctypes.c_void_p()
+    nat.lib.ptk_comm_init(ctypes.byref(comm), world, rank, uid)
+    return comm
+
+
+def traffic_from_profiles(workload):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ GPU arm --
+
+def run_gpu(args):
+    import torch
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet, stream_handle, vp
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    numels, desc = chunk_numels(args.workload)
+    comm = make_comm(world, rank)
+    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    stream = torch.cuda.current_stream()
+    cs.init_synthetic()
+    cs.fill_grads(0)
+    hyper = AdamHyper(lr=1e-3, weight_decay=0.0)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        cs.step(hyper)
+    torch.cuda.synchronize()
+    barrier(world)
+
+    launches0 = nat.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier(world)
+        start.record(stream)
+        for _ in range(args.steps):
+            cs.step(hyper)
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    launches = nat.launch_count() - launches0
+    ms = start.elapsed_time(end) / args.steps
+    ms_max = max_over_ranks(ms, world)
+    bytes_rank = cs.algorithmic_hbm_bytes()
+    total_bytes = bytes_rank * world  # every rank moves the same algorithmic bytes
+    value = total_bytes / (ms_max * 1e-3) / 1e9
+
+    # Dominant kernel, timed per launch with events on its own stream.
+    sh = stream_handle(stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in cs.chunks]
+    cfg = hyper.config(cs.step_count + 1, world)
+    kern_ms, kern_bytes = 0.0, 0
+    reps = max(1, min(args.steps, 5))
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        for c, (e0, e1) in zip(cs.chunks, ev):
+            e0.record(stream)
+            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                                   vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                                   c.shard, vp(cs.stats), vp(cs.workspace), None, None, sh)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        for c, (e0, e1) in zip(cs.chunks, ev):
+            kern_ms += e0.elapsed_time(e1)
+            kern_bytes += 28 * (c.numel // world)
+    hbm_peak, peak_kind = load_peaks()
+    achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
+    n_launch = reps * len(cs.chunks)
+
+    e2e = run_e2e(cs, hyper, args, world) if not args.no_e2e else None
+    sumsq, nonfinite = cs.grad_stats()
+
+    result = None
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(numels, args)
+        traffic = traffic_from_profiles(args.workload)
+        result = {
+            "metric": "chunk step GB/s (gather+RS+fused Adam) vs HBM/NVLink roofline",
+            "value": round(value, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_max, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32 (Adam state) / bf16 (grads, params)",
+            "data": "synthetic (counter-based uniform; SURVEY §8(d) seeds)",
+            "config": {
+                "workload": f"{args.workload}: {desc}",
+                "params": sum(numels),
+                "chunks": len(numels),
+                "chunk_params": numels,
+                "exchange": "nccl RS/AG (in place)" if world > 1 else "none (w=1)",
+                "parallelism": f"zero3-dp{world}",
+                "l2": "inputs larger than L2 (%.1f GB touched per step)" % (bytes_rank / 1e9),
+                "algorithmic_bytes_per_step_per_rank": bytes_rank,
+                "nvlink_bytes_per_step_per_rank": cs.algorithmic_nvlink_bytes(),
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "chunk_adam_kernel<GradBf16,2,true>",
+                "achieved": round(achieved, 1),
+                "peak": hbm_peak,
+                "peak_kind": peak_kind,
+                "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4),
+                "traffic": traffic,
+                "bytes_per_launch": kern_bytes // n_launch,
+                "ms_per_launch": round(kern_ms / n_launch, 4),
+                "frac_of_8tbs_spec": round(achieved / 8000.0, 4),
+            },
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "grad_stats": {"sumsq": sumsq, "nonfinite": nonfinite},
+            "cpu_baseline": cpu,
+        }
+    if comm is not None:
+        nat.lib.ptk_comm_destroy(comm)
+    return result
+
+
+def run_e2e(cs, hyper, args, world):
+    """Same step through the C-ABI with HOST buffers: per chunk piece, pinned
+    H2D of the gradients (h2d stream) -> fused Adam (compute stream) -> pinned
+    D2H of the updated bf16 parameters (d2h stream); events chain the three
+    streams so the copies of piece i+1 / i-1 overlap the update of piece i."""
+    import torch
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import stream_handle, vp
+
+    if world > 1:
+        return None  # the multi-rank e2e path also needs the AG/RS; single-rank only for now
+    piece = args.e2e_piece
+    comp = torch.cuda.current_stream()
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    host_g = [torch.empty(c.shard, dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
+    host_p = [torch.empty(c.shard, dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
+    host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    for hg, c in zip(host_g, cs.chunks):
+        hg.copy_(c.grad_shard().cpu())
+    sc, sh, sd = stream_handle(comp), stream_handle(h2d), stream_handle(d2h)
+
+    def one_step():
+        cs.step_count += 1
+        cfg = hyper.config(cs.step_count, world)
+        nat.lib.ptk_stats_reset(vp(cs.stats), sc)
+        for c, hg, hp in zip(cs.chunks, host_g, host_p):
+            for lo in range(0, c.shard, piece):
+                n = min(piece, c.shard - lo)
+                g_dev = c.grad_shard()[lo:lo + n]
+                p_dev = c.param_shard()[lo:lo + n]
+                e_in, e_up = torch.cuda.Event(), torch.cuda.Event()
+                h2d.wait_stream(comp) if lo == 0 and c.chunk_id == 0 else None
+                nat.lib.ptk_memcpy_h2d_async(vp(g_dev), ctypes.c_void_p(hg.data_ptr() + 2 * lo),
+                                             2 * n, sh)
+                e_in.record(h2d)
+                comp.wait_event(e_in)
+                nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master[lo:lo + n]),
+                                       vp(c.exp_avg[lo:lo + n]), vp(c.exp_avg_sq[lo:lo + n]),
+                                       vp(g_dev), vp(p_dev), n, vp(cs.stats), vp(cs.workspace),
+                                       None, None, sc)
+                e_up.record(comp)
+                d2h.wait_event(e_up)
+                nat.lib.ptk_memcpy_d2h_async(ctypes.c_void_p(hp.data_ptr() + 2 * lo), vp(p_dev),
+                                             2 * n, sd)
+        comp.wait_stream(d2h)
+        nat.lib.ptk_memcpy_d2h_async(vp(host_stats), vp(cs.stats), 16, sc)
+
+    for _ in range(max(1, args.warmup)):
+        one_step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(comp)
+    for _ in range(args.steps):
+        one_step()
+    t1.record(comp)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    h2d_bytes = sum(2 * c.shard for c in cs.chunks)
+    d2h_bytes = sum(2 * c.shard for c in cs.chunks) + 16
+    value = cs.algorithmic_hbm_bytes() * world / (ms * 1e-3) / 1e9
+    return {"value": round(value, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+            "path": "C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
+                    f"pinned host buffers, {piece}-element pieces on 3 streams"}
+
+
+# ------------------------------------------------------------------ CPU arm --
+
+def cpu_sample_step(n: int, threads: int):
+    """One bounded sample of the chunk step on the host: oracle fp32 Adam over
+    n parameters (28 B/param algorithmic bytes, w = 1)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(REPO, "tests"))
+    import oracle_lib as ol
+    master = ol.fill_f32(n, 0, 0.05)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    g = ol.fill_bf16(n, 1, 1e-3)
+    out = np.empty(n, np.uint16)
+    return ol, master, m, v, g, out
+
+
+def cpu_baseline(numels, args):
+    import numpy as np
+    n = min(args.cpu_sample, sum(numels))
+    ol, master, m, v, g, out = cpu_sample_step(n, 0)
+    times = []
+    for step in range(1, 4):
+        s = ol.scalars(step=step)
+        t0 = time.perf_counter()
+        ol.adam_step(s, master, m, v, g, out)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": round(28 * n / best / 1e9, 3), "unit": "GB/s", "cores": ol.num_threads(),
+            "kind": "port",
+            "sample": f"oracle fp32 Adam step over {n} params of the workload (28 B/param), "
+                      "best of 3, OpenMP over all host threads"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    numels, desc = chunk_numels(args.workload)
+    n = min(args.cpu_sample, sum(numels))
+    ol, master, m, v, g, out = cpu_sample_step(n, 0)
+    for step in range(1, args.warmup + 1):
+        ol.adam_step(ol.scalars(step=step), master, m, v, g, out)
+    t0 = time.perf_counter()
+    for step in range(args.warmup + 1, args.warmup + args.steps + 1):
+        ol.adam_step(ol.scalars(step=step), master, m, v, g, out)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 28 * n / dt / 1e9
+    sample = (f"oracle port (oracle/chunk_step.c) fp32 Adam over a {n}-param sample of the "
+              f"workload per step, w=1 data plane (the reference memplan never executes the "
+              f"data plane, SPEC.md:514), OpenMP over all host threads")
+    return {"impl": "reference", "metric":
+            "chunk step GB/s (gather+RS+fused Adam) vs HBM/NVLink roofline",
+            "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (Adam state) / bf16",
+            "data": "synthetic", "config": {"workload": f"{args.workload}: {desc}",
+                                            "sample_params": n},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s",
+                             "cores": ol.num_threads(), "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ptk", choices=["ptk", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
+    ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        res = run_reference(args)
+    else:
+        res = run_gpu(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+/* ptk.h — C-ABI of the B200 chunk data plane (libptk.so, sm_100a).
+ *
+ * This is the drop-in boundary BELOW the reference's planner API. The
+ * reference (memplan, /root/reference/proj) only MODELS these operations; each
+ * entry point replaces one modeled quantity with the real byte movement:
+ *
+ *   ptk_chunk_adam            <- GPU optimizer time `persist_params / gpu_optim_rate`
+ *                                (proj/src/cost.cpp:206-219) and the Sim `GpuOptim`
+ *                                task per persistent chunk (proj/src/sim.cpp:245-250)
+ *   ptk_grad_stats            <- "gradient-chunk cast/scale" of north_star (not modeled)
+ *   ptk_chunk_allgather       <- `gather_time(used_bytes)` (proj/src/hardware.cpp:29-34),
+ *                                Sim Gather (proj/src/sim.cpp:335-338)
+ *   ptk_chunk_reduce_scatter  <- `reduce_time(used_bytes)` (proj/src/hardware.cpp:36-38),
+ *                                Sim Reduce (proj/src/sim.cpp:428-436)
+ *   ptk_fused_rs_adam_ag      <- reduce_time + GpuOptim + next gather, as ONE kernel
+ *                                over NVLink peer memory (P2P loads / stores)
+ *   ptk_cpu_adam              <- CPU optimizer `nonpersist_params / cpu_optim_rate`
+ *                                (proj/src/cost.cpp:213-218, proj/src/sim.cpp:446-451)
+ *   ptk_memcpy_h2d/d2h_async  <- `transfer_time(shard_bytes, h2d/d2h)` upload/offload
+ *                                (proj/src/cost.cpp:126-127,186-187; sim.cpp:352-368)
+ *
+ * Conventions: plain pointers and sizes only; the caller owns
+ * all memory; every call is asynchronous and stream-ordered on the given
+ * cudaStream_t (passed as void*; NULL = legacy default stream) and performs no
+ * host synchronisation unless its name says so. Every function returns 0 on
+ * success or a negative PTK_E* code; ptk_last_error() returns the message of
+ * the last failure on the calling thread. Element buffers must be 16-byte
+ * aligned; chunk shards are padded to a multiple of world*8 elements
+ * (ptk_shard_elems) so every shard is 16-byte aligned. bf16 values are
+ * passed as uint16_t bit patterns.
+ */
+#ifndef PTK_H
+#define PTK_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTK_OK 0
+#define PTK_EINVAL -1
+#define PTK_ECUDA -2
+#define PTK_ENCCL -3
+#define PTK_EUNSUPPORTED -4
+
+#define PTK_MAX_PEERS 8
+
+/* Adam / AdamW hyper-parameters of one step (host doubles; the library
+ * derives fp32 scalars exactly once, see ptk_adam_scalars). */
+typedef struct ptk_adam_config {
+  double lr;
+  double beta1;
+  double beta2;
+  double eps;
+  double weight_decay;
+  int32_t adamw;     /* 1: decoupled decay p *= 1-lr*wd; 0: L2 g += wd*p */
+  int32_t step;      /* 1-based step count used for bias correction */
+  double grad_scale; /* multiplies every gradient: 1/(world*loss_scale)*clip */
+} ptk_adam_config;
+
+/* fp32 scalars actually used by the kernels (exposed for the tests). */
+typedef struct ptk_adam_scalars {
+  float gscale, wd, decay, w1, b2, w2, eps, neg_step_size, bc2_sqrt;
+  int32_t adamw;
+} ptk_adam_scalars;
+
+/* Gradient statistics accumulated on the device: sum of squares of the
+ * scaled gradient (fp64) and the count of non-finite elements. */
+typedef struct ptk_grad_stats_t {
+  double sumsq;
+  unsigned long long nonfinite;
+} ptk_grad_stats_t;
+
+/* ---- library ---------------------------------------------------------- */
+const char* ptk_last_error(void);
+const char* ptk_version(void);
+int ptk_adam_derive(const ptk_adam_config* cfg, ptk_adam_scalars* out);
+/* elements per rank shard for a chunk of n elements: roundup(n, 8w)/w */
+int64_t ptk_shard_elems(int64_t n, int32_t world);
+/* scratch: CTA partial buffer the reducing kernels need (bytes) */
+int64_t ptk_stats_workspace_bytes(void);
+
+/* ---- K1 + K2: fused chunk Adam ----------------------------------------
+ * master/exp_avg/exp_avg_sq: fp32[n]; grad: bf16[n] (or fp32[n] for the
+ * _f32grad variant); param_out: bf16[n] (nullable). If stats != NULL the
+ * statistics of this launch are ADDED to *stats (device memory; zero it
+ * with ptk_stats_reset); workspace = device scratch of
+ * ptk_stats_workspace_bytes() (required when stats != NULL).
+ * gscale_dev (nullable, device float): extra multiplier read on device
+ * (e.g. a clip coefficient from ptk_clip_coef). skip_dev (nullable, device
+ * int): when nonzero the launch is a no-op (overflow skip). */
+int ptk_chunk_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                   float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
+                   int64_t n, ptk_grad_stats_t* stats, void* workspace,
+                   const float* gscale_dev, const int32_t* skip_dev, void* stream);
+int ptk_chunk_adam_f32grad(const ptk_adam_config* cfg, float* master,
+                           float* exp_avg, float* exp_avg_sq, const float* grad,
+                           uint16_t* param_out, int64_t n,
+                           ptk_grad_stats_t* stats, void* workspace,
+                           const float* gscale_dev, const int32_t* skip_dev,
+                           void* stream);
+
+/* ---- K2 standalone: gradient statistics (+ optional fp32 scaled copy) --- */
+int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale,
+                   float* out_f32 /* nullable */, ptk_grad_stats_t* stats,
+                   void* workspace, void* stream);
+int ptk_stats_reset(ptk_grad_stats_t* stats, void* stream);
+/* coef_out = max_norm > 0 ? min(1, max_norm / (sqrt(sumsq) + 1e-6)) : 1;
+ * skip_out (nullable) = nonfinite != 0 */
+int ptk_clip_coef(const ptk_grad_stats_t* stats, double max_norm,
+                  float* coef_out, int32_t* skip_out, void* stream);
+
+/* ---- fused reduce-scatter -> Adam -> all-gather over peer memory -------
+ * grad_peers[r]: rank r's full bf16 gradient chunk (n_pad elements);
+ * param_peers[r]: rank r's full bf16 parameter chunk buffer. This rank
+ * owns elements [rank*shard, (rank+1)*shard). Reduction is an fp32 sum in
+ * rank order 0..world-1 (deterministic), then Adam on the local fp32
+ * master/m/v shard, then the bf16 result is stored into every peer's
+ * parameter buffer. Pointers may be NVLink peer mappings (ptk_ipc_*) or,
+ * for single-GPU validation, local buffers standing in for virtual ranks.
+ * The caller brackets the launch with ptk_peer_barrier. */
+int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad_peers,
+                         uint16_t* const* param_peers, int32_t world, int32_t rank,
+                         int64_t shard, float* master, float* exp_avg,
+                         float* exp_avg_sq, ptk_grad_stats_t* stats,
+                         void* workspace, void* stream);
+
+/* ---- synthetic inputs (SURVEY §8(d) counter-based generator) ----------- */
+/* out[i] = scale * u(seed, index0 + i), u in [-1, 1) exact in fp32 */
+int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, float scale,
+                         void* stream);
+int ptk_fill_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, int64_t index0, float scale,
+                          void* stream);
+
+/* ---- K3 / K4: NCCL chunk collectives --------------------------------- */
+typedef struct ptk_comm ptk_comm;
+#define PTK_UNIQUE_ID_BYTES 128
+int ptk_comm_unique_id(uint8_t out[PTK_UNIQUE_ID_BYTES]);
+int ptk_comm_init(ptk_comm** out, int32_t world, int32_t rank,
+                  const uint8_t id[PTK_UNIQUE_ID_BYTES]);
+int ptk_comm_destroy(ptk_comm* comm);
+/* dtype: 0 = bf16, 1 = fp32. In place: this rank's shard lives at
+ * buf + rank*shard_elems; after the call buf holds all world shards. */
+int ptk_chunk_allgather(ptk_comm* comm, void* buf, int64_t shard_elems,
+                        int32_t dtype, void* stream);
+/* In place: buf holds world*shard_elems local gradients; afterwards
+ * buf + rank*shard_elems holds the sum over ranks of that shard. */
+int ptk_chunk_reduce_scatter(ptk_comm* comm, void* buf, int64_t shard_elems,
+                             int32_t dtype, void* stream);
+/* Device-side barrier over the communicator (an 1-element all-reduce). */
+int ptk_comm_barrier(ptk_comm* comm, void* stream);
+
+/* ---- NVLink peer memory for the fused path ---------------------------- */
+#define PTK_IPC_HANDLE_BYTES 64
+int ptk_ipc_get_handle(void* dev_ptr, uint8_t out[PTK_IPC_HANDLE_BYTES]);
+int ptk_ipc_open_handle(const uint8_t handle[PTK_IPC_HANDLE_BYTES], void** dev_ptr);
+int ptk_ipc_close_handle(void* dev_ptr);
+/* signal_peers[r]: rank r's int32[PTK_MAX_PEERS] signal slots (zeroed once).
+ * Each call bumps `epoch` (monotone, identical on all ranks), stores it into
+ * slot [rank] of every peer and spins until all slots of its own array
+ * reached epoch. Orders all prior stream work before later stream work
+ * across the world. */
+int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank,
+                     int32_t epoch, void* stream);
+
+/* ---- K5: pinned host <-> device chunk copies on side streams ---------- */
+int ptk_host_alloc_pinned(void** out, size_t bytes);
+int ptk_host_free_pinned(void* ptr);
+int ptk_memcpy_h2d_async(void* dst, const void* src, size_t bytes, void* stream);
+int ptk_memcpy_d2h_async(void* dst, const void* src, size_t bytes, void* stream);
+
+/* ---- K6: host Adam over an offloaded shard (OpenMP, all cores) -------- */
+int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                 float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
+                 int64_t n, int32_t n_threads, double* sumsq_out,
+                 int64_t* nonfinite_out);
+
+/* ---- streams / events / timing helpers used by the host runtime ------- */
+int ptk_stream_create(void** out, int32_t high_priority);
+int ptk_stream_destroy(void* stream);
+int ptk_event_create(void** out);
+int ptk_event_destroy(void* ev);
+int ptk_event_record(void* ev, void* stream);
+int ptk_stream_wait_event(void* stream, void* ev);
+int ptk_event_elapsed_ms(void* start, void* end, float* ms);
+int ptk_stream_synchronize(void* stream);
+int ptk_device_synchronize(void);
+/* number of ptk kernels launched by this process so far */
+int64_t ptk_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTK_H */

@@ -1,0 +1,157 @@
+"""ctypes binding of libptk.so (include/ptk.h) — the only way Python reaches the
+B200 data plane. There is deliberately NO fallback: if the shared library is
+missing or fails to load, importing this module raises, so a GPU run can never
+silently route through a CPU or eager-PyTorch path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_char_p, c_double, c_float, c_int32, c_int64, c_size_t
+from ctypes import c_uint8, c_uint64, c_ulonglong, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libptk.so")
+
+PTK_OK = 0
+PTK_MAX_PEERS = 8
+PTK_UNIQUE_ID_BYTES = 128
+PTK_IPC_HANDLE_BYTES = 64
+
+
+class PtkError(RuntimeError):
+    """A libptk call returned a nonzero status (message from ptk_last_error)."""
+
+
+class AdamConfig(Structure):
+    _fields_ = [
+        ("lr", c_double),
+        ("beta1", c_double),
+        ("beta2", c_double),
+        ("eps", c_double),
+        ("weight_decay", c_double),
+        ("adamw", c_int32),
+        ("step", c_int32),
+        ("grad_scale", c_double),
+    ]
+
+
+class AdamScalars(Structure):
+    _fields_ = [(n, c_float) for n in ("gscale", "wd", "decay", "w1", "b2", "w2", "eps",
+                                       "neg_step_size", "bc2_sqrt")] + [("adamw", c_int32)]
+
+
+class GradStats(Structure):
+    _fields_ = [("sumsq", c_double), ("nonfinite", c_ulonglong)]
+
+
+# name -> (restype, argtypes); int-returning functions are status-checked.
+_SIGNATURES = {
+    "ptk_last_error": (c_char_p, []),
+    "ptk_version": (c_char_p, []),
+    "ptk_adam_derive": (c_int32, [POINTER(AdamConfig), POINTER(AdamScalars)]),
+    "ptk_shard_elems": (c_int64, [c_int64, c_int32]),
+    "ptk_stats_workspace_bytes": (c_int64, []),
+    "ptk_chunk_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
+    "ptk_chunk_adam_f32grad": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p]),
+    "ptk_grad_stats": (c_int32, [c_void_p, c_int64, c_float, c_void_p, c_void_p, c_void_p,
+                                 c_void_p]),
+    "ptk_stats_reset": (c_int32, [c_void_p, c_void_p]),
+    "ptk_clip_coef": (c_int32, [c_void_p, c_double, c_void_p, c_void_p, c_void_p]),
+    "ptk_fused_rs_adam_ag": (c_int32, [POINTER(AdamConfig), POINTER(c_void_p), POINTER(c_void_p),
+                                       c_int32, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p]),
+    "ptk_fill_uniform_f32": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
+    "ptk_fill_uniform_bf16": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
+    "ptk_comm_unique_id": (c_int32, [POINTER(c_uint8)]),
+    "ptk_comm_init": (c_int32, [POINTER(c_void_p), c_int32, c_int32, POINTER(c_uint8)]),
+    "ptk_comm_destroy": (c_int32, [c_void_p]),
+    "ptk_chunk_allgather": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "ptk_chunk_reduce_scatter": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "ptk_comm_barrier": (c_int32, [c_void_p, c_void_p]),
+    "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8)]),
+    "ptk_ipc_open_handle": (c_int32, [POINTER(c_uint8), POINTER(c_void_p)]),
+    "ptk_ipc_close_handle": (c_int32, [c_void_p]),
+    "ptk_peer_barrier": (c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int32, c_void_p]),
+    "ptk_host_alloc_pinned": (c_int32, [POINTER(c_void_p), c_size_t]),
+    "ptk_host_free_pinned": (c_int32, [c_void_p]),
+    "ptk_memcpy_h2d_async": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ptk_memcpy_d2h_async": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ptk_cpu_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p, c_int64, c_int32, POINTER(c_double), POINTER(c_int64)]),
+    "ptk_stream_create": (c_int32, [POINTER(c_void_p), c_int32]),
+    "ptk_stream_destroy": (c_int32, [c_void_p]),
+    "ptk_event_create": (c_int32, [POINTER(c_void_p)]),
+    "ptk_event_destroy": (c_int32, [c_void_p]),
+    "ptk_event_record": (c_int32, [c_void_p, c_void_p]),
+    "ptk_stream_wait_event": (c_int32, [c_void_p, c_void_p]),
+    "ptk_event_elapsed_ms": (c_int32, [c_void_p, c_void_p, POINTER(c_float)]),
+    "ptk_stream_synchronize": (c_int32, [c_void_p]),
+    "ptk_device_synchronize": (c_int32, []),
+    "ptk_kernel_launch_count": (c_int64, []),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libptk.so not found at {LIB_PATH}: build it with `make ptk` (or "
+        "`python -c 'import __graft_entry__ as g; g.build()'`). There is no fallback path.")
+
+_lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+for _name, (_res, _args) in _SIGNATURES.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def last_error() -> str:
+    msg = _lib.ptk_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str) -> None:
+    if rc != PTK_OK:
+        raise PtkError(f"{what} failed ({rc}): {last_error()}")
+
+
+class _Lib:
+    """Status-checked attribute access: lib.ptk_chunk_adam(...) raises on error."""
+
+    def __getattr__(self, name):
+        fn = getattr(_lib, name)
+        if _SIGNATURES[name][0] is c_int32:
+            def call(*args, _fn=fn, _name=name):
+                rc = _fn(*args)
+                check(rc, _name)
+                return rc
+            return call
+        return fn
+
+
+lib = _Lib()
+raw = _lib
+
+
+def adam_config(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, adamw=False,
+                step=1, grad_scale=1.0) -> AdamConfig:
+    return AdamConfig(lr, beta1, beta2, eps, weight_decay, int(bool(adamw)), int(step),
+                      float(grad_scale))
+
+
+def derive_scalars(cfg: AdamConfig) -> AdamScalars:
+    out = AdamScalars()
+    lib.ptk_adam_derive(ctypes.byref(cfg), ctypes.byref(out))
+    return out
+
+
+def shard_elems(n: int, world: int) -> int:
+    return int(_lib.ptk_shard_elems(n, world))
+
+
+def launch_count() -> int:
+    return int(_lib.ptk_kernel_launch_count())

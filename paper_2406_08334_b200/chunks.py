@@ -1,0 +1,260 @@
+"""Host-side chunk data plane: ZeRO-3 sharded chunk buffers and the per-step
+reduce-scatter -> fused Adam -> all-gather over them, driven through the
+C-ABI of libptk.so (include/ptk.h). PyTorch is used only to own device memory
+and streams.
+
+What this executes is what the reference only models:
+
+* chunk layout: one flat bf16 buffer per chunk of the reference's
+  `ChunkLayout` (proj/include/memplan/layout.hpp:27-49); chunk c holds
+  `used_bytes / bytes_per_param` parameters in execution order;
+* shard mapping: the reference models a rank's shard as
+  `floor(used_bytes / w)` bytes (proj/src/cost.cpp:20-22, `shard_bytes`);
+  physically the chunk is padded to a multiple of 8*w elements so the shards
+  are equal and 16-byte aligned — rank r owns [r*shard, (r+1)*shard);
+* persistent chunks hold fp32 master/m/v for the rank's shard on the device
+  (the reference's `persistent_chunk_bytes = 8*s_chunk` accounting,
+  proj/src/cost.cpp:10, counts the unsharded replica — quirk Q2);
+* per step and chunk: reduce-scatter of the bf16 gradient chunk
+  (`reduce_time`, proj/src/hardware.cpp:36-38), fused Adam on the owned
+  shard with grad scale 1/w (`GpuOptim`, proj/src/sim.cpp:245-250), and
+  all-gather of the updated bf16 parameters (`gather_time`,
+  proj/src/hardware.cpp:29-34).
+
+Two exchange modes:
+  "nccl"  — ptk_chunk_reduce_scatter / ptk_chunk_adam / ptk_chunk_allgather
+  "fused" — ptk_fused_rs_adam_ag, one kernel doing RS -> Adam -> AG over
+            peer pointers (NVLink P2P on a multi-GPU box), bracketed by
+            ptk_peer_barrier.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+# Seeds of the synthetic state: master = 0.05*u(seed), grads
+# = 1e-3*u(seed'), generated over the GLOBAL element index of each chunk so a
+# sharded run sees exactly the values of the unsharded run.
+MASTER_SCALE = 0.05
+GRAD_SCALE = 1e-3
+
+
+def master_seed(chunk: int) -> int:
+    return 1000 * chunk
+
+
+def grad_seed(chunk: int, rank: int, step: int = 0) -> int:
+    return 1000 * chunk + 1 + rank + 100_000 * step
+
+
+def vp(t: torch.Tensor | None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr() if t is not None else None)
+
+
+def stream_handle(stream: torch.cuda.Stream | None = None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class ChunkShard:
+    """One chunk as seen by one rank."""
+
+    chunk_id: int
+    numel: int        # parameters in the chunk (used_bytes / bytes_per_param)
+    world: int
+    rank: int
+    shard: int        # padded per-rank shard (elements)
+    param: torch.Tensor      # bf16[n_pad]  gathered working copy
+    grad: torch.Tensor       # bf16[n_pad]  local gradients (RS in place)
+    master: torch.Tensor     # fp32[shard]
+    exp_avg: torch.Tensor    # fp32[shard]
+    exp_avg_sq: torch.Tensor  # fp32[shard]
+
+    @property
+    def n_pad(self) -> int:
+        return self.shard * self.world
+
+    @property
+    def offset(self) -> int:
+        return self.rank * self.shard
+
+    def param_shard(self) -> torch.Tensor:
+        return self.param[self.offset:self.offset + self.shard]
+
+    def grad_shard(self) -> torch.Tensor:
+        return self.grad[self.offset:self.offset + self.shard]
+
+    def owned_numel(self) -> int:
+        """Real (unpadded) parameters in this rank's shard."""
+        return max(0, min(self.shard, self.numel - self.offset))
+
+
+@dataclass
+class AdamHyper:
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    adamw: bool = False
+    loss_scale: float = 1.0
+
+    def config(self, step: int, world: int) -> nat.AdamConfig:
+        return nat.adam_config(self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
+                               self.adamw, step, 1.0 / (world * self.loss_scale))
+
+
+class ChunkSet:
+    """All persistent chunks of one rank plus the step driver.
+
+    `chunk_numels` comes from a `ChunkLayout` (used_bytes // bytes_per_param
+    per chunk). `comm` is a ptk_comm handle (mode "nccl", world > 1);
+    `peers` is a list of per-rank ChunkSets (mode "fused" with virtual ranks
+    on one device) or a PeerMap of NVLink-mapped pointers.
+    """
+
+    def __init__(self, chunk_numels, world: int = 1, rank: int = 0, device=None,
+                 mode: str = "nccl", comm=None):
+        if mode not in ("nccl", "fused"):
+            raise ValueError(f"unknown exchange mode {mode!r}")
+        self.world, self.rank, self.mode, self.comm = world, rank, mode, comm
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.chunks: list[ChunkShard] = []
+        for c, n in enumerate(chunk_numels):
+            shard = nat.shard_elems(int(n), world)
+            n_pad = shard * world
+            self.chunks.append(ChunkShard(
+                c, int(n), world, rank, shard,
+                param=torch.zeros(n_pad, dtype=BF16, device=self.device),
+                grad=torch.zeros(n_pad, dtype=BF16, device=self.device),
+                master=torch.zeros(shard, dtype=F32, device=self.device),
+                exp_avg=torch.zeros(shard, dtype=F32, device=self.device),
+                exp_avg_sq=torch.zeros(shard, dtype=F32, device=self.device)))
+        ws_bytes = int(nat.raw.ptk_stats_workspace_bytes())
+        self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)
+        self.stats = torch.zeros(2, dtype=torch.float64, device=self.device)  # ptk_grad_stats_t
+        self.step_count = 0
+        self.peer_grad_ptrs = None   # fused mode: per chunk (c_void_p * world)
+        self.peer_param_ptrs = None
+        self.signal_ptrs = None      # fused mode: (c_void_p * world) signal slots
+        self.epoch = 0
+
+    # ------------------------------------------------------------ sizes --
+    @property
+    def numel(self) -> int:
+        return sum(c.numel for c in self.chunks)
+
+    def algorithmic_hbm_bytes(self) -> int:
+        """Per-step HBM bytes of this rank: 28*P/w (Adam) +
+        2P(w-1)/w (AG receive) + 2P + 2P/w (RS read local grads, write shard);
+        w = 1 -> 28*P. P = real parameters of the chunk."""
+        w, tot = self.world, 0
+        for c in self.chunks:
+            p = c.numel
+            tot += 28 * p // w
+            if w > 1:
+                tot += 2 * p * (w - 1) // w + 2 * p + 2 * p // w
+        return tot
+
+    def algorithmic_nvlink_bytes(self) -> int:
+        """Per-step NVLink bytes per direction of this rank: 4P(w-1)/w."""
+        w = self.world
+        return sum(4 * c.numel * (w - 1) // w for c in self.chunks)
+
+    # ---------------------------------------------------- synthetic state --
+    def init_synthetic(self, stream=None) -> None:
+        """master = 0.05*u(seed_c) over the global index; m = v = 0; the bf16
+        working copy of the full chunk is RNE(master) (what an all-gather of
+        every rank's shard produces)."""
+        s = stream_handle(stream)
+        for c in self.chunks:
+            nat.lib.ptk_fill_uniform_f32(vp(c.master), c.shard, master_seed(c.chunk_id),
+                                         c.offset, MASTER_SCALE, s)
+            nat.lib.ptk_fill_uniform_bf16(vp(c.param), c.n_pad, master_seed(c.chunk_id), 0,
+                                          MASTER_SCALE, s)
+            c.exp_avg.zero_()
+            c.exp_avg_sq.zero_()
+            self._zero_padding(c)
+
+    def fill_grads(self, step: int = 0, stream=None) -> None:
+        """This rank's local gradients of the full chunk: 1e-3*u(seed_{c,rank,step})."""
+        s = stream_handle(stream)
+        for c in self.chunks:
+            nat.lib.ptk_fill_uniform_bf16(vp(c.grad), c.n_pad, grad_seed(c.chunk_id, self.rank, step),
+                                          0, GRAD_SCALE, s)
+            if c.n_pad > c.numel:
+                c.grad[c.numel:].zero_()
+
+    def _zero_padding(self, c: ChunkShard) -> None:
+        if c.n_pad > c.numel:
+            c.param[c.numel:].zero_()
+            lo = max(0, c.numel - c.offset)
+            if lo < c.shard:
+                c.master[lo:].zero_()
+
+    # --------------------------------------------------------------- step --
+    def reset_stats(self, stream=None) -> None:
+        nat.lib.ptk_stats_reset(vp(self.stats), stream_handle(stream))
+
+    def step(self, hyper: AdamHyper, stream=None, with_stats: bool = True) -> None:
+        """One optimizer step over every chunk: RS -> Adam -> AG."""
+        self.step_count += 1
+        cfg = hyper.config(self.step_count, self.world)
+        s = stream_handle(stream)
+        stats = vp(self.stats) if with_stats else ctypes.c_void_p(None)
+        if with_stats:
+            nat.lib.ptk_stats_reset(vp(self.stats), s)
+        if self.mode == "fused":
+            self._step_fused(cfg, s, stats)
+            return
+        for c in self.chunks:
+            if self.world > 1:
+                nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
+            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                                   vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                                   c.shard, stats, vp(self.workspace), None, None, s)
+            if self.world > 1:
+                nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
+
+    def _step_fused(self, cfg, s, stats) -> None:
+        if self.peer_grad_ptrs is None:
+            raise RuntimeError("fused mode needs peer pointers (attach_virtual_peers / attach_ipc_peers)")
+        if self.signal_ptrs is not None:
+            self.epoch += 1
+            nat.lib.ptk_peer_barrier(self.signal_ptrs, self.world, self.rank, self.epoch, s)
+        for c, gp, pp in zip(self.chunks, self.peer_grad_ptrs, self.peer_param_ptrs):
+            nat.lib.ptk_fused_rs_adam_ag(ctypes.byref(cfg), gp, pp, self.world, self.rank, c.shard,
+                                         vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq), stats,
+                                         vp(self.workspace), s)
+        if self.signal_ptrs is not None:
+            self.epoch += 1
+            nat.lib.ptk_peer_barrier(self.signal_ptrs, self.world, self.rank, self.epoch, s)
+
+    def attach_virtual_peers(self, sets: list["ChunkSet"]) -> None:
+        """Single-GPU validation of the fused path: `sets[r]` plays rank r.
+        The kernel then reads every virtual rank's gradient buffer and writes
+        every virtual rank's parameter buffer exactly as it would over NVLink."""
+        arr = ctypes.c_void_p * PTK_MAX
+        self.peer_grad_ptrs, self.peer_param_ptrs = [], []
+        for ci in range(len(self.chunks)):
+            g = arr(*[sets[r].chunks[ci].grad.data_ptr() for r in range(self.world)])
+            p = arr(*[sets[r].chunks[ci].param.data_ptr() for r in range(self.world)])
+            self.peer_grad_ptrs.append(g)
+            self.peer_param_ptrs.append(p)
+
+    def grad_stats(self) -> tuple[float, int]:
+        v = self.stats.cpu()
+        sumsq = float(v[0])
+        nonfinite = int(v.view(torch.int64)[1])
+        return sumsq, nonfinite
+
+
+PTK_MAX = nat.PTK_MAX_PEERS

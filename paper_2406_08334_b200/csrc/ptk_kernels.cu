@@ -1,0 +1,587 @@
+// libptk device kernels for sm_100a: the chunk data plane of ProTrain.
+//
+//   K1+K2  chunk_adam_kernel     fused grad cast/scale + grad-norm/overflow
+//                                statistics + Adam/AdamW over a flat chunk
+//                                shard (28 B/param of HBM traffic, bf16 grad)
+//   K2     grad_stats_kernel     standalone statistics (+ fp32 scaled copy)
+//   K1+K3+K4 fused_peer_kernel   reduce-scatter (fp32 sum over NVLink peer
+//                                loads) -> Adam -> all-gather (peer stores)
+//   aux    fill kernels (counter-based synthetic inputs), clip coefficient,
+//          peer barrier (system-scope release/acquire flags)
+//
+// The modeled counterparts in the reference are listed in include/ptk.h.
+// Design notes: every kernel is HBM-streaming integer/fp32
+// element work — no data reuse, so no tensor cores and no shared-memory
+// tiling; the levers are 128-bit coalesced accesses, enough bytes in flight
+// per SM (UNROLL independent 8-element units per thread, all loads issued
+// before any math), a persistent grid sized to the SM count × occupancy,
+// streaming cache hints (.cs) so the once-touched chunk bytes do not thrash
+// L2, and deterministic warp-shuffle → CTA → last-CTA reductions for the
+// statistics. The update arithmetic uses explicit round-to-nearest
+// intrinsics (no FMA contraction) so it matches oracle/chunk_step.c bit for
+// bit.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptk_common.h"
+
+namespace ptk {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxGrid = 4096;
+
+struct StatsWorkspace {
+  double sq[kMaxGrid];
+  unsigned long long bad[kMaxGrid];
+  unsigned int arrived;
+  unsigned int pad[3];
+};
+
+// ---------------------------------------------------------------- helpers --
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  f[0] = bf_lo(u.x); f[1] = bf_hi(u.x);
+  f[2] = bf_lo(u.y); f[3] = bf_hi(u.y);
+  f[4] = bf_lo(u.z); f[5] = bf_hi(u.z);
+  f[6] = bf_lo(u.w); f[7] = bf_hi(u.w);
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                    pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+}
+
+__device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+__device__ __forceinline__ void st8f(float* p, const float (&f)[8]) {
+  __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
+  __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(f[4], f[5], f[6], f[7]));
+}
+
+// Gradient loaders: 8 consecutive elements as fp32.
+struct GradBf16 {
+  using T = uint16_t;
+  __device__ __forceinline__ static void load8(const uint16_t* g, float (&f)[8]) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4*>(g));
+    unpack8(u, f);
+  }
+  __device__ __forceinline__ static float load1(const uint16_t* g) {
+    return __uint_as_float(static_cast<uint32_t>(*g) << 16);
+  }
+};
+struct GradF32 {
+  using T = float;
+  __device__ __forceinline__ static void load8(const float* g, float (&f)[8]) { ld8f(g, f); }
+  __device__ __forceinline__ static float load1(const float* g) { return *g; }
+};
+
+// The per-element update rule (see oracle/chunk_step.h for the statement).
+__device__ __forceinline__ float adam_elem(const ptk_adam_scalars& s, float g, float& p,
+                                           float& m, float& v) {
+  if (s.wd != 0.0f) g = __fadd_rn(g, __fmul_rn(s.wd, p));
+  if (s.adamw) p = __fmul_rn(p, s.decay);
+  m = __fadd_rn(m, __fmul_rn(s.w1, __fsub_rn(g, m)));
+  v = __fadd_rn(__fmul_rn(v, s.b2), __fmul_rn(s.w2, __fmul_rn(g, g)));
+  const float d = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), s.bc2_sqrt), s.eps);
+  p = __fadd_rn(p, __fmul_rn(s.neg_step_size, __fdiv_rn(m, d)));
+  return p;
+}
+
+__device__ __forceinline__ void accum_stats(float g, float& sq, unsigned& bad) {
+  sq = __fmaf_rn(g, g, sq);
+  bad += isfinite(g) ? 0u : 1u;
+}
+
+// Deterministic grid reduction: warp shuffle -> CTA (fixed order) -> the last
+// CTA to arrive sums the per-CTA partials in index order and ADDS the result
+// to *stats. Safe across back-to-back launches on one stream (the arrival
+// counter is re-armed by the last CTA).
+__device__ __forceinline__ void reduce_stats(float sq, unsigned bad, StatsWorkspace* ws,
+                                             ptk_grad_stats_t* stats) {
+  __shared__ double s_sq[kThreads / 32];
+  __shared__ unsigned long long s_bad[kThreads / 32];
+  __shared__ bool s_last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_sq[warp] = static_cast<double>(sq);
+    s_bad[warp] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bsq = 0.0;
+    unsigned long long bbad = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      bsq += s_sq[w];
+      bbad += s_bad[w];
+    }
+    ws->sq[blockIdx.x] = bsq;
+    ws->bad[blockIdx.x] = bbad;
+    __threadfence();
+    const unsigned prev = atomicAdd(&ws->arrived, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double tsq = 0.0;
+    unsigned long long tbad = 0;
+    const volatile double* vsq = ws->sq;
+    const volatile unsigned long long* vbad = ws->bad;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      tsq += vsq[b];
+      tbad += vbad[b];
+    }
+    stats->sumsq += tsq;
+    stats->nonfinite += tbad;
+    ws->arrived = 0;
+  }
+}
+
+// ------------------------------------------------------------ K1 + K2 ----
+
+template <class G, int U, bool kStats>
+__global__ void __launch_bounds__(kThreads)
+chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                  float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
+                  uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
+                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+  if (skip_dev != nullptr && *skip_dev != 0) return;  // grid-uniform
+  float gs = s.gscale;
+  if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
+  float sq = 0.0f;
+  unsigned bad = 0;
+
+  const int64_t nvec = n >> 3;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+
+  // Main loop: U independent 8-element units per thread, loads first.
+  for (; i + (U - 1) * stride < nvec; i += U * stride) {
+    float p[U][8], m[U][8], v[U][8], g[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = (i + u * stride) << 3;
+      G::load8(grad + e, g[u]);
+      ld8f(master + e, p[u]);
+      ld8f(exp_avg + e, m[u]);
+      ld8f(exp_avg_sq + e, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = (i + u * stride) << 3;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float gk = __fmul_rn(g[u][k], gs);
+        if (kStats) accum_stats(gk, sq, bad);
+        adam_elem(s, gk, p[u][k], m[u][k], v[u][k]);
+      }
+      st8f(master + e, p[u]);
+      st8f(exp_avg + e, m[u]);
+      st8f(exp_avg_sq + e, v[u]);
+      if (param_out != nullptr) __stcs(reinterpret_cast<uint4*>(param_out + e), pack8(p[u]));
+    }
+  }
+  // Remainder units.
+  for (; i < nvec; i += stride) {
+    const int64_t e = i << 3;
+    float p[8], m[8], v[8], g[8];
+    G::load8(grad + e, g);
+    ld8f(master + e, p);
+    ld8f(exp_avg + e, m);
+    ld8f(exp_avg_sq + e, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float gk = __fmul_rn(g[k], gs);
+      if (kStats) accum_stats(gk, sq, bad);
+      adam_elem(s, gk, p[k], m[k], v[k]);
+    }
+    st8f(master + e, p);
+    st8f(exp_avg + e, m);
+    st8f(exp_avg_sq + e, v);
+    if (param_out != nullptr) __stcs(reinterpret_cast<uint4*>(param_out + e), pack8(p));
+  }
+  // Scalar tail (< 8 elements) on CTA 0.
+  const int64_t t0 = nvec << 3;
+  if (blockIdx.x == 0 && threadIdx.x < n - t0) {
+    const int64_t e = t0 + threadIdx.x;
+    const float gk = __fmul_rn(G::load1(grad + e), gs);
+    if (kStats) accum_stats(gk, sq, bad);
+    float p = master[e], m = exp_avg[e], v = exp_avg_sq[e];
+    adam_elem(s, gk, p, m, v);
+    master[e] = p;
+    exp_avg[e] = m;
+    exp_avg_sq[e] = v;
+    if (param_out != nullptr) param_out[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
+  }
+  if (kStats) reduce_stats(sq, bad, ws, stats);
+}
+
+// -------------------------------------------------------------- K2 -------
+
+template <bool kWrite>
+__global__ void __launch_bounds__(kThreads)
+grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
+                  float* __restrict__ out, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
+  float sq = 0.0f;
+  unsigned bad = 0;
+  const int64_t nvec = n >> 3;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < nvec;
+       i += stride) {
+    float g[8];
+    GradBf16::load8(grad + (i << 3), g);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      g[k] = __fmul_rn(g[k], scale);
+      accum_stats(g[k], sq, bad);
+    }
+    if (kWrite) st8f(out + (i << 3), g);
+  }
+  const int64_t t0 = nvec << 3;
+  if (blockIdx.x == 0 && threadIdx.x < n - t0) {
+    const int64_t e = t0 + threadIdx.x;
+    const float gk = __fmul_rn(GradBf16::load1(grad + e), scale);
+    accum_stats(gk, sq, bad);
+    if (kWrite) out[e] = gk;
+  }
+  reduce_stats(sq, bad, ws, stats);
+}
+
+__global__ void stats_reset_kernel(ptk_grad_stats_t* stats) {
+  stats->sumsq = 0.0;
+  stats->nonfinite = 0;
+}
+
+__global__ void clip_coef_kernel(const ptk_grad_stats_t* stats, double max_norm, float* coef,
+                                 int32_t* skip) {
+  const double norm = sqrt(stats->sumsq);
+  double c = 1.0;
+  if (max_norm > 0.0) {
+    c = max_norm / (norm + 1e-6);
+    if (c > 1.0) c = 1.0;
+  }
+  *coef = static_cast<float>(c);
+  if (skip != nullptr) *skip = stats->nonfinite != 0 ? 1 : 0;
+}
+
+// ------------------------------------------------ K1+K3+K4 over NVLink ----
+
+struct PeerTable {
+  const uint16_t* grad[PTK_MAX_PEERS];
+  uint16_t* param[PTK_MAX_PEERS];
+};
+
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t shard,
+                  float* __restrict__ master, float* __restrict__ exp_avg,
+                  float* __restrict__ exp_avg_sq, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
+  float sq = 0.0f;
+  unsigned bad = 0;
+  const int64_t nvec = shard >> 3;  // shards are multiples of 8 elements
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < nvec;
+       i += stride) {
+    const int64_t e = i << 3;
+    uint4 raw[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r)
+      raw[r] = __ldcs(reinterpret_cast<const uint4*>(peers.grad[r] + offset + e));
+    float p[8], m[8], v[8], g[8], t[8];
+    ld8f(master + e, p);
+    ld8f(exp_avg + e, m);
+    ld8f(exp_avg_sq + e, v);
+    unpack8(raw[0], g);
+#pragma unroll
+    for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
+      unpack8(raw[r], t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) g[k] = __fadd_rn(g[k], t[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float gk = __fmul_rn(g[k], s.gscale);
+      accum_stats(gk, sq, bad);
+      adam_elem(s, gk, p[k], m[k], v[k]);
+    }
+    st8f(master + e, p);
+    st8f(exp_avg + e, m);
+    st8f(exp_avg_sq + e, v);
+    const uint4 out = pack8(p);
+#pragma unroll
+    for (int r = 0; r < W; ++r)  // all-gather by push
+      __stcs(reinterpret_cast<uint4*>(peers.param[r] + offset + e), out);
+  }
+  if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
+}
+
+struct SignalTable {
+  int32_t* slot[PTK_MAX_PEERS];
+};
+
+__global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int epoch) {
+  const int t = threadIdx.x;
+  if (t >= world) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(sig.slot[t] + rank), "r"(epoch)
+               : "memory");
+  const int32_t* mine = sig.slot[rank] + t;
+  int32_t seen;
+  do {
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
+  } while (seen < epoch);
+}
+
+// ----------------------------------------------------------- synthetic ----
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float uniform_pm1(uint64_t seed, uint64_t i) {
+  const uint32_t top = static_cast<uint32_t>(splitmix64(seed ^ i) >> 40);
+  return __fsub_rn(__fmul_rn(__fmul_rn(static_cast<float>(top), 0x1p-24f), 2.0f), 1.0f);
+}
+
+__global__ void fill_f32_kernel(float* out, int64_t n, uint64_t seed, int64_t index0, float scale) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __fmul_rn(scale, uniform_pm1(seed, static_cast<uint64_t>(index0 + i)));
+}
+
+__global__ void fill_bf16_kernel(uint16_t* out, int64_t n, uint64_t seed, int64_t index0, float scale) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float f = __fmul_rn(scale, uniform_pm1(seed, static_cast<uint64_t>(index0 + i)));
+    out[i] = static_cast<uint16_t>(pack_bf16x2(f, 0.0f) & 0xffffu);
+  }
+}
+
+// --------------------------------------------------------- launch sizing --
+
+int sm_count() {
+  static int count = [] {
+    int dev = 0, c = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }();
+  return count;
+}
+
+template <typename K>
+int grid_for(K kernel, int64_t work_items) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  int64_t g = static_cast<int64_t>(sm_count()) * per_sm;
+  const int64_t need = (work_items + kThreads - 1) / kThreads;
+  if (g > need) g = need;
+  if (g > kMaxGrid) g = kMaxGrid;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+constexpr int kUnroll = 2;
+
+template <class G>
+int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
+                const typename G::T* grad, uint16_t* param_out, int64_t n,
+                ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                const int32_t* skip_dev, void* stream) {
+  if (!cfg || !master || !m || !v || !grad) return fail(PTK_EINVAL, "ptk_chunk_adam: null buffer");
+  if (n < 0) return fail(PTK_EINVAL, "ptk_chunk_adam: negative n");
+  if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_chunk_adam: step must be >= 1");
+  if (!aligned16(master) || !aligned16(m) || !aligned16(v) || !aligned16(grad) ||
+      (param_out && !aligned16(param_out)))
+    return fail(PTK_EINVAL, "ptk_chunk_adam: buffers must be 16-byte aligned");
+  if (stats && !workspace) return fail(PTK_EINVAL, "ptk_chunk_adam: stats requires workspace");
+  if (n == 0) return PTK_OK;
+  const ptk_adam_scalars s = derive_scalars(*cfg);
+  const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
+  auto* ws = static_cast<StatsWorkspace*>(workspace);
+  if (stats) {
+    auto k = chunk_adam_kernel<G, kUnroll, true>;
+    const int grid = grid_for(k, units);
+    k<<<grid, kThreads, 0, as_stream(stream)>>>(s, master, m, v, grad, param_out, n, ws, stats,
+                                                gscale_dev, skip_dev);
+  } else {
+    auto k = chunk_adam_kernel<G, kUnroll, false>;
+    const int grid = grid_for(k, units);
+    k<<<grid, kThreads, 0, as_stream(stream)>>>(s, master, m, v, grad, param_out, n, ws, stats,
+                                                gscale_dev, skip_dev);
+  }
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "chunk_adam_kernel launch");
+}
+
+template <int W>
+void launch_fused(const ptk_adam_scalars& s, const PeerTable& t, int64_t off, int64_t shard,
+                  float* p, float* m, float* v, StatsWorkspace* ws, ptk_grad_stats_t* stats,
+                  cudaStream_t st) {
+  auto k = fused_peer_kernel<W>;
+  const int grid = grid_for(k, (shard >> 3) > 0 ? (shard >> 3) : 1);
+  k<<<grid, kThreads, 0, st>>>(s, t, off, shard, p, m, v, ws, stats);
+}
+
+}  // namespace
+}  // namespace ptk
+
+using namespace ptk;
+
+extern "C" {
+
+int64_t ptk_stats_workspace_bytes(void) { return static_cast<int64_t>(sizeof(StatsWorkspace)); }
+
+int ptk_chunk_adam(const ptk_adam_config* cfg, float* master, float* exp_avg, float* exp_avg_sq,
+                   const uint16_t* grad, uint16_t* param_out, int64_t n, ptk_grad_stats_t* stats,
+                   void* workspace, const float* gscale_dev, const int32_t* skip_dev,
+                   void* stream) {
+  return launch_adam<GradBf16>(cfg, master, exp_avg, exp_avg_sq, grad, param_out, n, stats,
+                               workspace, gscale_dev, skip_dev, stream);
+}
+
+int ptk_chunk_adam_f32grad(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                           float* exp_avg_sq, const float* grad, uint16_t* param_out, int64_t n,
+                           ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                           const int32_t* skip_dev, void* stream) {
+  return launch_adam<GradF32>(cfg, master, exp_avg, exp_avg_sq, grad, param_out, n, stats,
+                              workspace, gscale_dev, skip_dev, stream);
+}
+
+int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale, float* out_f32,
+                   ptk_grad_stats_t* stats, void* workspace, void* stream) {
+  if (!grad || !stats || !workspace) return fail(PTK_EINVAL, "ptk_grad_stats: null argument");
+  if (!aligned16(grad) || (out_f32 && !aligned16(out_f32)))
+    return fail(PTK_EINVAL, "ptk_grad_stats: buffers must be 16-byte aligned");
+  if (n <= 0) return n == 0 ? PTK_OK : fail(PTK_EINVAL, "ptk_grad_stats: negative n");
+  auto* ws = static_cast<StatsWorkspace*>(workspace);
+  const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
+  if (out_f32) {
+    auto k = grad_stats_kernel<true>;
+    k<<<grid_for(k, units), kThreads, 0, as_stream(stream)>>>(grad, n, scale, out_f32, ws, stats);
+  } else {
+    auto k = grad_stats_kernel<false>;
+    k<<<grid_for(k, units), kThreads, 0, as_stream(stream)>>>(grad, n, scale, out_f32, ws, stats);
+  }
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "grad_stats_kernel launch");
+}
+
+int ptk_stats_reset(ptk_grad_stats_t* stats, void* stream) {
+  if (!stats) return fail(PTK_EINVAL, "ptk_stats_reset: null stats");
+  stats_reset_kernel<<<1, 1, 0, as_stream(stream)>>>(stats);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "stats_reset_kernel launch");
+}
+
+int ptk_clip_coef(const ptk_grad_stats_t* stats, double max_norm, float* coef_out,
+                  int32_t* skip_out, void* stream) {
+  if (!stats || !coef_out) return fail(PTK_EINVAL, "ptk_clip_coef: null argument");
+  clip_coef_kernel<<<1, 1, 0, as_stream(stream)>>>(stats, max_norm, coef_out, skip_out);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "clip_coef_kernel launch");
+}
+
+int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad_peers,
+                         uint16_t* const* param_peers, int32_t world, int32_t rank, int64_t shard,
+                         float* master, float* exp_avg, float* exp_avg_sq,
+                         ptk_grad_stats_t* stats, void* workspace, void* stream) {
+  if (!cfg || !grad_peers || !param_peers || !master || !exp_avg || !exp_avg_sq)
+    return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: null argument");
+  if (world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: bad world/rank");
+  if (shard < 0 || (shard & 7) != 0)
+    return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: shard must be a multiple of 8 elements");
+  if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: step must be >= 1");
+  if (stats && !workspace) return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: stats requires workspace");
+  PeerTable t{};
+  for (int r = 0; r < world; ++r) {
+    if (!grad_peers[r] || !param_peers[r] || !aligned16(grad_peers[r]) || !aligned16(param_peers[r]))
+      return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: peer buffers must be non-null and 16-byte aligned");
+    t.grad[r] = grad_peers[r];
+    t.param[r] = param_peers[r];
+  }
+  if (!aligned16(master) || !aligned16(exp_avg) || !aligned16(exp_avg_sq))
+    return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: state buffers must be 16-byte aligned");
+  if (shard == 0) return PTK_OK;
+  const ptk_adam_scalars s = derive_scalars(*cfg);
+  const int64_t off = static_cast<int64_t>(rank) * shard;
+  auto* ws = static_cast<StatsWorkspace*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  switch (world) {
+    case 1: launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 2: launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 3: launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 4: launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 5: launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 6: launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 7: launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    default: launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+  }
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "fused_peer_kernel launch");
+}
+
+int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank, int32_t epoch,
+                     void* stream) {
+  if (!signal_peers || world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(PTK_EINVAL, "ptk_peer_barrier: bad arguments");
+  SignalTable t{};
+  for (int r = 0; r < world; ++r) {
+    if (!signal_peers[r]) return fail(PTK_EINVAL, "ptk_peer_barrier: null signal slot");
+    t.slot[r] = signal_peers[r];
+  }
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "peer_barrier_kernel launch");
+}
+
+int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, float scale,
+                         void* stream) {
+  if (!out || n < 0) return fail(PTK_EINVAL, "ptk_fill_uniform_f32: bad arguments");
+  if (n == 0) return PTK_OK;
+  const int64_t blocks = (n + 255) / 256;
+  const int grid = static_cast<int>(blocks < 8 * 148 * 4 ? blocks : 8 * 148 * 4);
+  fill_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(out, n, seed, index0, scale);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "fill_f32_kernel launch");
+}
+
+int ptk_fill_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, int64_t index0, float scale,
+                          void* stream) {
+  if (!out || n < 0) return fail(PTK_EINVAL, "ptk_fill_uniform_bf16: bad arguments");
+  if (n == 0) return PTK_OK;
+  const int64_t blocks = (n + 255) / 256;
+  const int grid = static_cast<int>(blocks < 8 * 148 * 4 ? blocks : 8 * 148 * 4);
+  fill_bf16_kernel<<<grid, 256, 0, as_stream(stream)>>>(out, n, seed, index0, scale);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "fill_bf16_kernel launch");
+}
+
+}  // extern "C"

