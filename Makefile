@@ -22,7 +22,7 @@ PTK_CU   := $(PKG)/csrc/ptk_kernels.cu
 PTK_CPP  := $(PKG)/csrc/ptk_host.cpp $(PKG)/csrc/ptk_comm.cpp $(PKG)/csrc/ptk_cpu_adam.cpp
 PTK_OBJS := $(OBJ)/ptk_kernels.o $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(PTK_CPP))
 
-.PHONY: all ptk planner oracle clean
+.PHONY: all ptk planner oracle reftests clean
 all: ptk planner oracle
 
 ptk: $(PKG)/libptk.so
@@ -38,8 +38,42 @@ $(OBJ)/%.o: $(PKG)/csrc/%.cpp $(PKG)/csrc/ptk_common.h include/ptk.h
 $(PKG)/libptk.so: $(PTK_OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lnccl -Xcompiler -fopenmp -lgomp
 
-planner:
-	@true
+# ---- planner (drop-in memplan API) -----------------------------------------
+PLAN_SRC  := model serialize packing costmodel search simulator cli
+PLAN_OBJS := $(addprefix $(OBJ)/planner_,$(addsuffix .o,$(PLAN_SRC)))
+PLANFLAGS := -std=c++20 -O2 -fPIC -pthread -ffp-contract=off -Wall -Wextra -Iinclude -I$(JSON_DIR)
+
+planner: build/libmemplan.a $(PKG)/libmemplan.so build/memplan
+
+$(OBJ)/planner_%.o: $(PKG)/csrc/planner/%.cpp $(wildcard include/memplan/*.hpp) $(PKG)/csrc/planner/digest.hpp
+	@mkdir -p $(OBJ)
+	$(CXX) $(PLANFLAGS) -c $< -o $@
+
+build/libmemplan.a: $(PLAN_OBJS)
+	ar rcs $@ $^
+
+$(PKG)/libmemplan.so: $(PLAN_OBJS)
+	$(CXX) -shared -pthread -o $@ $^
+
+build/memplan: $(PKG)/csrc/planner/memplan_main.cpp build/libmemplan.a
+	$(CXX) $(PLANFLAGS) $< build/libmemplan.a -o $@
+
+# The reference's own unit suites + acceptance binary, compiled UNMODIFIED
+# from /root/reference against this planner (drop-in proof; build container only).
+REF_TESTS_DIR ?= /root/reference/proj/tests
+REF_SUITES := test_trace test_hardware test_layout test_presets test_cost test_sim test_search test_cli acceptance
+reftests: $(addprefix build/reftests/,$(REF_SUITES))
+
+build/reftests/test_main.o: $(REF_TESTS_DIR)/test_main.cpp
+	@mkdir -p build/reftests
+	$(CXX) $(PLANFLAGS) -Ioracle/shim -c $< -o $@
+
+build/reftests/test_%: $(REF_TESTS_DIR)/test_%.cpp build/reftests/test_main.o build/libmemplan.a
+	$(CXX) $(PLANFLAGS) -Ioracle/shim $< build/reftests/test_main.o build/libmemplan.a -o $@
+
+build/reftests/acceptance: $(REF_TESTS_DIR)/acceptance.cpp build/libmemplan.a
+	@mkdir -p build/reftests
+	$(CXX) $(PLANFLAGS) $< build/libmemplan.a -o $@
 
 oracle:
 	$(MAKE) -C oracle all

@@ -1,0 +1,262 @@
+// Cost-model configuration search over {n_persist, n_buffer, n_swap,
+// n_checkpoint}.
+//
+// Behavioural sources (clean-room restatement; same winner, counters and
+// frontier as the reference):
+//   swap caps                    proj/src/search.cpp:13-37
+//   candidate stream + ordering  proj/src/search.cpp:45-121
+//   feasibility / preference     proj/src/search.cpp:135-155
+//   memory-ordered walk          proj/src/search.cpp:157-226
+//
+// What is different (B200 build): the reference
+// re-derives every per-trace quantity inside each of ~10^6 estimate calls.
+// Here the trace / layout / link terms are digested once (digest.hpp), the
+// schedule terms once per (n_swap, n_checkpoint), and the surviving prefix of
+// the memory-ordered stream is evaluated by a pool of threads. Each
+// candidate's t_iter is computed with the reference's exact operation order,
+// the argmin under config_preferred (a total order) is unique, and the
+// frontier is built by the same std::sort over the same sequence, so the
+// result is bit-identical and independent of the thread count.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <thread>
+
+#include "digest.hpp"
+#include "memplan/errors.hpp"
+#include "memplan/search.hpp"
+
+namespace memplan {
+
+namespace {
+
+std::atomic<int> g_threads{0};
+
+struct Candidate {
+  PlanConfig config;
+  std::int64_t m_peak = 0;
+  std::int64_t m_peak_before_alpha = 0;
+};
+
+// Largest swap count whose swap positions j*(k+1) stay inside the model.
+int swap_cap_layout(int n_block, int n_interval) {
+  return n_block <= 0 ? 0 : (n_block - 1) / (n_interval + 1) + 1;
+}
+
+// Largest swap count whose block swap-outs all fit inside the forward pass at
+// half (contended) D2H bandwidth.
+int swap_cap_bandwidth(const ModelTrace& trace, const HardwareProfile& hw) {
+  const std::int64_t act = mean_block_act_bytes(trace);
+  if (act <= 0) return trace.n_blocks;
+  double fwd = 0;
+  for (const OperatorRecord& op : trace.ops)
+    if (op.block_id) fwd += op.t_fwd;
+  const double one_swap = static_cast<double>(act) / contended_bandwidth(hw.d2h_bw, 2);
+  if (one_swap <= 0) return trace.n_blocks;
+  return static_cast<int>(std::floor(fwd / one_swap));
+}
+
+std::int64_t largest_block_act(const ModelTrace& trace) {
+  std::vector<std::int64_t> act(static_cast<std::size_t>(std::max(1, trace.n_blocks)), 0);
+  for (const OperatorRecord& op : trace.ops)
+    if (op.block_id) act[*op.block_id] += op.act_bytes;
+  return *std::max_element(act.begin(), act.end());
+}
+
+bool candidate_before(const Candidate& a, const Candidate& b) {
+  if (a.m_peak != b.m_peak) return a.m_peak < b.m_peak;
+  const PlanConfig& x = a.config;
+  const PlanConfig& y = b.config;
+  if (x.n_persist != y.n_persist) return x.n_persist < y.n_persist;
+  if (x.n_buffer != y.n_buffer) return x.n_buffer < y.n_buffer;
+  if (x.n_swap != y.n_swap) return x.n_swap < y.n_swap;
+  return x.n_checkpoint < y.n_checkpoint;
+}
+
+// The memory-ordered candidate stream. Peaks come from one activation replay
+// per (n_swap, n_checkpoint) plus the model-state bytes of (n_persist,
+// n_buffer).
+std::vector<Candidate> candidate_stream(const ChunkLayout& layout, const ModelTrace& trace,
+                                        const HardwareProfile& hw, const CostOptions& opts) {
+  const int n_chunk = layout.n_chunk();
+  const int n_block = trace.n_blocks;
+  const int n_interval = compute_interval(trace, hw);
+  const int max_swaps = std::min(swap_cap_layout(n_block, n_interval), swap_cap_bandwidth(trace, hw));
+  const int ns_hi = std::min(max_swaps, n_block);
+
+  std::map<std::pair<int, int>, std::int64_t> replay;
+  for (int ns = 0; ns <= ns_hi; ++ns) {
+    const int nc_lo = ns > 1 ? (ns - 1) * n_interval : 0;
+    for (int nc = nc_lo; nc <= n_block - ns; ++nc) {
+      const BlockSchedule sched = build_block_schedule(n_block, ns, nc, n_interval);
+      replay[{ns, nc}] = detail::replay_peak(trace, sched, ns, nc);
+    }
+  }
+
+  std::vector<Candidate> out;
+  for (int np = 0; np <= n_chunk; ++np) {
+    const int nb_lo = np == n_chunk ? 0 : std::min(3, n_chunk - np);
+    const int nb_hi = np == n_chunk ? 0 : n_chunk - np;
+    for (int nb = nb_lo; nb <= nb_hi; ++nb) {
+      const std::int64_t states = persistent_chunk_bytes(layout.s_chunk) * np +
+                                  buffer_chunk_bytes(layout.s_chunk) * nb;
+      for (int ns = 0; ns <= ns_hi; ++ns) {
+        const int nc_lo = ns > 1 ? (ns - 1) * n_interval : 0;
+        for (int nc = nc_lo; nc <= n_block - ns; ++nc) {
+          Candidate c;
+          c.config = PlanConfig{layout.s_chunk, n_chunk, np, nb, n_block, n_interval, ns, nc};
+          c.m_peak_before_alpha = replay.at({ns, nc}) + states;
+          c.m_peak = static_cast<std::int64_t>(
+              std::llround(opts.alpha * static_cast<double>(c.m_peak_before_alpha)));
+          out.push_back(c);
+        }
+      }
+    }
+  }
+  // All five keys together identify a candidate, so any correct sort yields
+  // the reference's stable order.
+  std::sort(out.begin(), out.end(), candidate_before);
+  return out;
+}
+
+int worker_count(std::size_t work) {
+  int n = g_threads.load();
+  if (n <= 0) n = static_cast<int>(std::thread::hardware_concurrency());
+  if (n <= 0) n = 1;
+  const int by_work = static_cast<int>(work / 4096) + 1;  // tiny searches stay serial
+  return std::max(1, std::min(n, by_work));
+}
+
+}  // namespace
+
+void set_search_threads(int n) { g_threads.store(n); }
+
+std::vector<PlanConfig> enumerate_candidates(const ChunkLayout& layout, const ModelTrace& trace,
+                                             const HardwareProfile& hw, const CostOptions& opts) {
+  std::vector<PlanConfig> out;
+  for (const Candidate& c : candidate_stream(layout, trace, hw, opts)) out.push_back(c.config);
+  return out;
+}
+
+bool config_feasible(const ModelTrace& trace, const PlanConfig& config, std::int64_t m_peak,
+                     const HardwareProfile& hw) {
+  if (m_peak >= hw.gpu_mem) return false;
+  // swap-ins need one block of activation headroom on the device
+  if (config.n_swap > 0 && hw.gpu_mem - m_peak < largest_block_act(trace)) return false;
+  const std::int64_t offloaded =
+      persistent_chunk_bytes(config.s_chunk) * (config.n_chunk - config.n_persist);
+  return offloaded <= hw.cpu_mem;
+}
+
+bool config_preferred(double t_iter_a, const PlanConfig& a, std::int64_t peak_a, double t_iter_b,
+                      const PlanConfig& b, std::int64_t peak_b) {
+  if (t_iter_a != t_iter_b) return t_iter_a < t_iter_b;
+  if (a.n_swap != b.n_swap) return a.n_swap < b.n_swap;
+  if (a.n_checkpoint != b.n_checkpoint) return a.n_checkpoint < b.n_checkpoint;
+  if (a.n_persist != b.n_persist) return a.n_persist > b.n_persist;
+  if (a.n_buffer != b.n_buffer) return a.n_buffer > b.n_buffer;
+  return peak_a < peak_b;
+}
+
+SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
+                           const HardwareProfile& hw, const CostOptions& opts) {
+  hw.validate();
+  const std::vector<Candidate> stream = candidate_stream(layout, trace, hw, opts);
+
+  // Memory-ordered: the first candidate past capacity ends the walk.
+  const auto past = std::partition_point(stream.begin(), stream.end(), [&](const Candidate& c) {
+    return c.m_peak < hw.gpu_mem;
+  });
+  const std::size_t walk = static_cast<std::size_t>(past - stream.begin());
+
+  // Shared digests; one schedule digest per (n_swap, n_checkpoint).
+  const detail::TraceDigest digest(trace, layout);
+  const detail::LinkDigest links(digest, hw);
+  std::map<std::pair<int, int>, std::unique_ptr<detail::ScheduleDigest>> sched_digest;
+  std::map<std::pair<int, int>, BlockSchedule> schedules;
+  const std::int64_t biggest_block = largest_block_act(trace);
+  std::vector<char> feasible(walk, 0);
+  for (std::size_t i = 0; i < walk; ++i) {
+    const PlanConfig& c = stream[i].config;
+    // config_feasible with the per-trace maximum hoisted out of the loop
+    bool ok = stream[i].m_peak < hw.gpu_mem;
+    if (ok && c.n_swap > 0 && hw.gpu_mem - stream[i].m_peak < biggest_block) ok = false;
+    if (ok && persistent_chunk_bytes(c.s_chunk) * (c.n_chunk - c.n_persist) > hw.cpu_mem) ok = false;
+    feasible[i] = ok;
+    if (!ok) continue;
+    const auto key = std::make_pair(c.n_swap, c.n_checkpoint);
+    if (!sched_digest.count(key)) {
+      auto it = schedules.emplace(key, build_block_schedule(c.n_block, c.n_swap, c.n_checkpoint,
+                                                            c.n_interval)).first;
+      sched_digest.emplace(key, std::make_unique<detail::ScheduleDigest>(digest, it->second, hw));
+    }
+  }
+
+  // Evaluate the feasible prefix in parallel (each t_iter in reference order).
+  std::vector<double> t_iter(walk, 0.0);
+  const auto optim = [&](const PlanConfig& c) { return estimate_optim(layout, c, hw); };
+  const auto eval_range = [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      if (!feasible[i]) continue;
+      const PlanConfig& c = stream[i].config;
+      const detail::ScheduleDigest& sd = *sched_digest.at({c.n_swap, c.n_checkpoint});
+      const double f = detail::fwd_time(digest, sd, links, c.n_persist, nullptr);
+      const double b = detail::bwd_time(digest, sd, links, c.n_persist, c.n_buffer, nullptr);
+      const auto [gpu, cpu] = optim(c);
+      t_iter[i] = f + std::max(b + gpu, cpu);
+    }
+  };
+  const int workers = worker_count(walk);
+  if (workers == 1) {
+    eval_range(0, walk);
+  } else {
+    std::vector<std::thread> pool;
+    const std::size_t per = (walk + workers - 1) / workers;
+    for (int w = 0; w < workers; ++w) {
+      const std::size_t lo = std::min(walk, w * per), hi = std::min(walk, lo + per);
+      pool.emplace_back(eval_range, lo, hi);
+    }
+    for (auto& t : pool) t.join();
+  }
+
+  // Deterministic merge in stream order.
+  SearchOutcome outcome;
+  bool have = false;
+  double best_t = 0;
+  std::int64_t best_peak = 0;
+  std::vector<std::pair<PlanConfig, double>> ranked;
+  for (std::size_t i = 0; i < walk; ++i) {
+    if (!feasible[i]) {
+      ++outcome.n_pruned;
+      continue;
+    }
+    ++outcome.n_evaluated;
+    const Candidate& cand = stream[i];
+    ranked.emplace_back(cand.config, t_iter[i]);
+    if (!have || config_preferred(t_iter[i], cand.config, cand.m_peak, best_t, outcome.best,
+                                  best_peak)) {
+      have = true;
+      best_t = t_iter[i];
+      best_peak = cand.m_peak;
+      outcome.best = cand.config;
+    }
+  }
+  outcome.n_pruned += static_cast<std::int64_t>(stream.size() - walk);
+  if (!have) throw NoFeasibleConfig("even the maximum-savings configuration exceeds device memory");
+
+  // Frontier: the same (unstable) introsort over the same sequence as the
+  // reference, then the 16 fastest.
+  std::sort(ranked.begin(), ranked.end(),
+            [](const auto& a, const auto& b) { return a.second < b.second; });
+  if (ranked.size() > 16) ranked.resize(16);
+  outcome.frontier = std::move(ranked);
+
+  const BlockSchedule best_sched = build_block_schedule(
+      outcome.best.n_block, outcome.best.n_swap, outcome.best.n_checkpoint, outcome.best.n_interval);
+  outcome.estimate = estimate_iteration(trace, layout, best_sched, outcome.best, hw, opts);
+  return outcome;
+}
+
+}  // namespace memplan

@@ -23,6 +23,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "ptk_common.h"
 
@@ -103,6 +106,8 @@ __device__ __forceinline__ float adam_elem(const ptk_adam_scalars& s, float g, f
   return p;
 }
 
+// Statistics: squares are summed in fp32 over one 8-element unit, the unit
+// sums in fp64 per thread (keeps the full-chunk sum within ~1e-7 relative).
 __device__ __forceinline__ void accum_stats(float g, float& sq, unsigned& bad) {
   sq = __fmaf_rn(g, g, sq);
   bad += isfinite(g) ? 0u : 1u;
@@ -112,10 +117,10 @@ __device__ __forceinline__ void accum_stats(float g, float& sq, unsigned& bad) {
 // CTA to arrive sums the per-CTA partials in index order and ADDS the result
 // to *stats. Safe across back-to-back launches on one stream (the arrival
 // counter is re-armed by the last CTA).
-__device__ __forceinline__ void reduce_stats(float sq, unsigned bad, StatsWorkspace* ws,
+__device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorkspace* ws,
                                              ptk_grad_stats_t* stats) {
-  __shared__ double s_sq[kThreads / 32];
-  __shared__ unsigned long long s_bad[kThreads / 32];
+  __shared__ double s_sq[32];
+  __shared__ unsigned long long s_bad[32];
   __shared__ bool s_last;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -124,14 +129,14 @@ __device__ __forceinline__ void reduce_stats(float sq, unsigned bad, StatsWorksp
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
-    s_sq[warp] = static_cast<double>(sq);
+    s_sq[warp] = sq;
     s_bad[warp] = bad;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double bsq = 0.0;
     unsigned long long bbad = 0;
-    for (int w = 0; w < kThreads / 32; ++w) {
+    for (unsigned w = 0; w < blockDim.x / 32; ++w) {
       bsq += s_sq[w];
       bbad += s_bad[w];
     }
@@ -162,15 +167,17 @@ __device__ __forceinline__ void reduce_stats(float sq, unsigned bad, StatsWorksp
 // ------------------------------------------------------------ K1 + K2 ----
 
 template <class G, int U, bool kStats>
-__global__ void __launch_bounds__(kThreads)
-chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
-                  float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
-                  uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
-                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+__device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict__ master,
+                                          float* __restrict__ exp_avg,
+                                          float* __restrict__ exp_avg_sq,
+                                          const typename G::T* __restrict__ grad,
+                                          uint16_t* __restrict__ param_out, int64_t n,
+                                          StatsWorkspace* ws, ptk_grad_stats_t* stats,
+                                          const float* gscale_dev, const int32_t* skip_dev) {
   if (skip_dev != nullptr && *skip_dev != 0) return;  // grid-uniform
   float gs = s.gscale;
   if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
-  float sq = 0.0f;
+  double sq = 0.0;
   unsigned bad = 0;
 
   const int64_t nvec = n >> 3;
@@ -191,12 +198,14 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e = (i + u * stride) << 3;
+      float usq = 0.0f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float gk = __fmul_rn(g[u][k], gs);
-        if (kStats) accum_stats(gk, sq, bad);
+        if (kStats) accum_stats(gk, usq, bad);
         adam_elem(s, gk, p[u][k], m[u][k], v[u][k]);
       }
+      if (kStats) sq += usq;
       st8f(master + e, p[u]);
       st8f(exp_avg + e, m[u]);
       st8f(exp_avg_sq + e, v[u]);
@@ -211,12 +220,14 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
     ld8f(master + e, p);
     ld8f(exp_avg + e, m);
     ld8f(exp_avg_sq + e, v);
+    float usq = 0.0f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float gk = __fmul_rn(g[k], gs);
-      if (kStats) accum_stats(gk, sq, bad);
+      if (kStats) accum_stats(gk, usq, bad);
       adam_elem(s, gk, p[k], m[k], v[k]);
     }
+    if (kStats) sq += usq;
     st8f(master + e, p);
     st8f(exp_avg + e, m);
     st8f(exp_avg_sq + e, v);
@@ -227,7 +238,9 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
   if (blockIdx.x == 0 && threadIdx.x < n - t0) {
     const int64_t e = t0 + threadIdx.x;
     const float gk = __fmul_rn(G::load1(grad + e), gs);
-    if (kStats) accum_stats(gk, sq, bad);
+    float usq = 0.0f;
+    if (kStats) accum_stats(gk, usq, bad);
+    sq += usq;
     float p = master[e], m = exp_avg[e], v = exp_avg_sq[e];
     adam_elem(s, gk, p, m, v);
     master[e] = p;
@@ -238,13 +251,201 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
 
+template <class G, int U, bool kStats>
+__global__ void __launch_bounds__(kThreads)
+chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                  float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
+                  uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
+                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+  adam_body<G, U, kStats>(s, master, exp_avg, exp_avg_sq, grad, param_out, n, ws, stats,
+                          gscale_dev, skip_dev);
+}
+
+// Same body, higher occupancy (launch bounds force <= 64 registers).
+template <class G, int U, bool kStats, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+chunk_adam_occ_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                      float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
+                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
+                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+  adam_body<G, U, kStats>(s, master, exp_avg, exp_avg_sq, grad, param_out, n, ws, stats,
+                          gscale_dev, skip_dev);
+}
+
+// ------------------------------------------- K1 + K2, TMA bulk pipeline --
+//
+// Persistent CTAs walk whole tiles of kTile elements. One elected thread
+// moves every tile with 1-D bulk copies (cp.async.bulk, the TMA engine):
+// master/m/v/grad global -> shared, completion counted on an mbarrier
+// (complete_tx), and after the update master/m/v/param shared -> global as a
+// bulk_group. kStages tiles of shared memory form a ring; the producer runs
+// kStages-2 tiles ahead of the consumers, and a stage is refilled only after
+// the bulk store that last read it has finished reading shared memory
+// (cp.async.bulk.wait_group.read 1). Register pressure no longer limits the
+// bytes in flight: they live in shared memory.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int kTile>
+struct TmaStage {
+  float master[kTile];
+  float m[kTile];
+  float v[kTile];
+  uint16_t grad[kTile];
+  uint16_t param[kTile];
+};
+
+template <int kTile, int kStages, int kThr, bool kStats>
+__global__ void __launch_bounds__(kThr, 1)
+chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                      float* __restrict__ exp_avg_sq, const uint16_t* __restrict__ grad,
+                      uint16_t* __restrict__ param_out, int64_t n_tiles, StatsWorkspace* ws,
+                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+  static_assert(kTile % (kThr * 4) == 0, "tile must be a multiple of 4 elements per thread");
+  static_assert(kStages >= 3, "ring needs >= 3 stages");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto* stage = reinterpret_cast<TmaStage<kTile>*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages];
+
+  if (skip_dev != nullptr && *skip_dev != 0) return;
+  float gs = s.gscale;
+  if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
+
+  const int tid = threadIdx.x;
+  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int64_t my_tiles =
+      n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kLoadBytes = kTile * (3 * sizeof(float) + sizeof(uint16_t));
+  const bool has_param = param_out != nullptr;
+
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    fence_async_smem();
+  }
+  __syncthreads();
+
+  auto issue_load = [&](int64_t k) {  // k-th tile of this CTA
+    const int st = static_cast<int>(k % kStages);
+    const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
+    TmaStage<kTile>& S = stage[st];
+    mbar_expect_tx(&full[st], kLoadBytes);
+    bulk_load(S.master, master + e, kTile * 4, &full[st]);
+    bulk_load(S.m, exp_avg + e, kTile * 4, &full[st]);
+    bulk_load(S.v, exp_avg_sq + e, kTile * 4, &full[st]);
+    bulk_load(S.grad, grad + e, kTile * 2, &full[st]);
+  };
+
+  constexpr int kAhead = kStages - 2;
+  if (tid == 0)
+    for (int64_t k = 0; k < kAhead && k < my_tiles; ++k) issue_load(k);
+
+  double sq = 0.0;
+  unsigned bad = 0;
+  for (int64_t k = 0; k < my_tiles; ++k) {
+    if (tid == 0 && k + kAhead < my_tiles) {
+      bulk_wait_read<1>();  // the store of tile k-2 (same stage) has read its smem
+      issue_load(k + kAhead);
+    }
+    const int st = static_cast<int>(k % kStages);
+    mbar_wait(&full[st], static_cast<uint32_t>((k / kStages) & 1));
+    TmaStage<kTile>& S = stage[st];
+    float usq = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kTile / (kThr * 4); ++j) {
+      const int e = (j * kThr + tid) * 4;
+      float4 p = *reinterpret_cast<float4*>(&S.master[e]);
+      float4 m = *reinterpret_cast<float4*>(&S.m[e]);
+      float4 v = *reinterpret_cast<float4*>(&S.v[e]);
+      const uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[e]);
+      float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
+      float* pp = &p.x;
+      float* mm = &m.x;
+      float* vv = &v.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float gk = __fmul_rn(g[q], gs);
+        if (kStats) accum_stats(gk, usq, bad);
+        adam_elem(s, gk, pp[q], mm[q], vv[q]);
+      }
+      *reinterpret_cast<float4*>(&S.master[e]) = p;
+      *reinterpret_cast<float4*>(&S.m[e]) = m;
+      *reinterpret_cast<float4*>(&S.v[e]) = v;
+      *reinterpret_cast<uint2*>(&S.param[e]) =
+          make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
+    }
+    if (kStats) sq += usq;
+    fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
+      bulk_store(master + e, S.master, kTile * 4);
+      bulk_store(exp_avg + e, S.m, kTile * 4);
+      bulk_store(exp_avg_sq + e, S.v, kTile * 4);
+      if (has_param) bulk_store(param_out + e, S.param, kTile * 2);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  if (kStats) reduce_stats(sq, bad, ws, stats);
+}
+
 // -------------------------------------------------------------- K2 -------
 
 template <bool kWrite>
 __global__ void __launch_bounds__(kThreads)
 grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
                   float* __restrict__ out, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
-  float sq = 0.0f;
+  double sq = 0.0;
   unsigned bad = 0;
   const int64_t nvec = n >> 3;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
@@ -252,18 +453,22 @@ grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
        i += stride) {
     float g[8];
     GradBf16::load8(grad + (i << 3), g);
+    float usq = 0.0f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       g[k] = __fmul_rn(g[k], scale);
-      accum_stats(g[k], sq, bad);
+      accum_stats(g[k], usq, bad);
     }
+    sq += usq;
     if (kWrite) st8f(out + (i << 3), g);
   }
   const int64_t t0 = nvec << 3;
   if (blockIdx.x == 0 && threadIdx.x < n - t0) {
     const int64_t e = t0 + threadIdx.x;
     const float gk = __fmul_rn(GradBf16::load1(grad + e), scale);
-    accum_stats(gk, sq, bad);
+    float usq = 0.0f;
+    accum_stats(gk, usq, bad);
+    sq += usq;
     if (kWrite) out[e] = gk;
   }
   reduce_stats(sq, bad, ws, stats);
@@ -298,7 +503,7 @@ __global__ void __launch_bounds__(kThreads)
 fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t shard,
                   float* __restrict__ master, float* __restrict__ exp_avg,
                   float* __restrict__ exp_avg_sq, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
-  float sq = 0.0f;
+  double sq = 0.0;
   unsigned bad = 0;
   const int64_t nvec = shard >> 3;  // shards are multiples of 8 elements
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
@@ -320,12 +525,14 @@ fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t s
 #pragma unroll
       for (int k = 0; k < 8; ++k) g[k] = __fadd_rn(g[k], t[k]);
     }
+    float usq = 0.0f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float gk = __fmul_rn(g[k], s.gscale);
-      accum_stats(gk, sq, bad);
+      accum_stats(gk, usq, bad);
       adam_elem(s, gk, p[k], m[k], v[k]);
     }
+    sq += usq;
     st8f(master + e, p);
     st8f(exp_avg + e, m);
     st8f(exp_avg_sq + e, v);
@@ -409,6 +616,98 @@ int grid_for(K kernel, int64_t work_items) {
 
 constexpr int kUnroll = 2;
 
+// Kernel variant of the bf16-gradient chunk Adam. Selected once per process
+// from PTK_ADAM_VARIANT (benchmarking aid); the default is the measured best.
+enum class AdamVariant { Ldg, LdgOcc, Tma1024x8, Tma2048x6, Tma1024x6x2, Tma2048x6t512,
+                         Tma2048x7t512, Tma1024x12, Tma1024x12t512, Tma2048x5t512 };
+
+AdamVariant adam_variant() {
+  static AdamVariant v = [] {
+    const char* e = std::getenv("PTK_ADAM_VARIANT");
+    const std::string name = e ? e : "";
+    if (name == "ldg") return AdamVariant::Ldg;
+    if (name == "ldg_occ") return AdamVariant::LdgOcc;
+    if (name == "tma2048x6") return AdamVariant::Tma2048x6;
+    if (name == "tma1024x6x2") return AdamVariant::Tma1024x6x2;
+    if (name == "tma1024x8") return AdamVariant::Tma1024x8;
+    if (name == "tma2048x6t512") return AdamVariant::Tma2048x6t512;
+    if (name == "tma2048x7t512") return AdamVariant::Tma2048x7t512;
+    if (name == "tma2048x5t512") return AdamVariant::Tma2048x5t512;
+    if (name == "tma1024x12") return AdamVariant::Tma1024x12;
+    if (name == "tma1536x8t384") return AdamVariant::Tma1024x12t512;
+    if (name == "tma2048x6") return AdamVariant::Tma2048x6;
+    return AdamVariant::Tma2048x6;
+  }();
+  return v;
+}
+
+template <class G, int U, bool kStats, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+chunk_adam_occ_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                      float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
+                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
+                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev);
+
+template <class G, bool kStats>
+void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
+                const typename G::T* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
+                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+                cudaStream_t st) {
+  const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
+  auto k = chunk_adam_kernel<G, kUnroll, kStats>;
+  k<<<grid_for(k, units), kThreads, 0, st>>>(s, master, m, v, grad, param_out, n, ws, stats,
+                                             gscale_dev, skip_dev);
+  launch_counter()++;
+}
+
+template <int kTile, int kStages, int kPerSm, int kThr, bool kStats>
+int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
+               const uint16_t* grad, uint16_t* param_out, int64_t n_tiles, StatsWorkspace* ws,
+               ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+               cudaStream_t st) {
+  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats>;
+  constexpr int kSmem = kStages * static_cast<int>(sizeof(TmaStage<kTile>));
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return check_cuda(e, "chunk_adam_tma_kernel smem attribute");
+    configured = true;
+  }
+  int64_t grid = static_cast<int64_t>(sm_count()) * kPerSm;
+  if (grid > n_tiles) grid = n_tiles;
+  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, master, m, v, grad, param_out, n_tiles, ws,
+                                                     stats, gscale_dev, skip_dev);
+  launch_counter()++;
+  return PTK_OK;
+}
+
+template <int kTile, int kStages, int kPerSm, int kThr>
+int adam_tma_then_tail(const ptk_adam_scalars& s, float* master, float* m, float* v,
+                       const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
+                       ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+                       cudaStream_t st) {
+  const int64_t tiles = n / kTile;
+  const int64_t done = tiles * kTile;
+  int rc = PTK_OK;
+  if (tiles > 0) {
+    rc = stats ? launch_tma<kTile, kStages, kPerSm, kThr, true>(
+                     s, master, m, v, grad, param_out, tiles, ws, stats, gscale_dev, skip_dev, st)
+               : launch_tma<kTile, kStages, kPerSm, kThr, false>(
+                     s, master, m, v, grad, param_out, tiles, ws, stats, gscale_dev, skip_dev, st);
+    if (rc != PTK_OK) return rc;
+  }
+  if (done < n) {
+    uint16_t* po = param_out ? param_out + done : nullptr;
+    if (stats)
+      launch_ldg<GradBf16, true>(s, master + done, m + done, v + done, grad + done, po, n - done,
+                                 ws, stats, gscale_dev, skip_dev, st);
+    else
+      launch_ldg<GradBf16, false>(s, master + done, m + done, v + done, grad + done, po, n - done,
+                                  ws, stats, gscale_dev, skip_dev, st);
+  }
+  return rc;
+}
+
 template <class G>
 int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
                 const typename G::T* grad, uint16_t* param_out, int64_t n,
@@ -423,20 +722,56 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
   if (stats && !workspace) return fail(PTK_EINVAL, "ptk_chunk_adam: stats requires workspace");
   if (n == 0) return PTK_OK;
   const ptk_adam_scalars s = derive_scalars(*cfg);
-  const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
   auto* ws = static_cast<StatsWorkspace*>(workspace);
-  if (stats) {
-    auto k = chunk_adam_kernel<G, kUnroll, true>;
-    const int grid = grid_for(k, units);
-    k<<<grid, kThreads, 0, as_stream(stream)>>>(s, master, m, v, grad, param_out, n, ws, stats,
-                                                gscale_dev, skip_dev);
-  } else {
-    auto k = chunk_adam_kernel<G, kUnroll, false>;
-    const int grid = grid_for(k, units);
-    k<<<grid, kThreads, 0, as_stream(stream)>>>(s, master, m, v, grad, param_out, n, ws, stats,
-                                                gscale_dev, skip_dev);
+  cudaStream_t st = as_stream(stream);
+  int rc = PTK_OK;
+  if constexpr (std::is_same_v<G, GradBf16>) {
+    switch (adam_variant()) {
+#define PTK_TMA_CASE(V, T, S, P, THR)                                                       \
+  case AdamVariant::V:                                                                       \
+    rc = adam_tma_then_tail<T, S, P, THR>(s, master, m, v, grad, param_out, n, ws, stats,    \
+                                          gscale_dev, skip_dev, st);                         \
+    return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
+      PTK_TMA_CASE(Tma2048x6t512, 2048, 6, 1, 512)
+      PTK_TMA_CASE(Tma2048x7t512, 2048, 7, 1, 512)
+      PTK_TMA_CASE(Tma2048x5t512, 2048, 5, 1, 512)
+      PTK_TMA_CASE(Tma1024x12, 1024, 12, 1, 256)
+      PTK_TMA_CASE(Tma1024x12t512, 1536, 8, 1, 384)
+#undef PTK_TMA_CASE
+      case AdamVariant::Tma1024x8:
+        rc = adam_tma_then_tail<1024, 8, 1, 256>(s, master, m, v, grad, param_out, n, ws, stats,
+                                            gscale_dev, skip_dev, st);
+        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
+      case AdamVariant::Tma2048x6:
+        rc = adam_tma_then_tail<2048, 6, 1, 256>(s, master, m, v, grad, param_out, n, ws, stats,
+                                            gscale_dev, skip_dev, st);
+        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
+      case AdamVariant::Tma1024x6x2:
+        rc = adam_tma_then_tail<1024, 6, 2, 256>(s, master, m, v, grad, param_out, n, ws, stats,
+                                            gscale_dev, skip_dev, st);
+        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
+      case AdamVariant::LdgOcc: {
+        const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
+        if (stats) {
+          auto k = chunk_adam_occ_kernel<G, 1, true, 4>;
+          k<<<grid_for(k, units), kThreads, 0, st>>>(s, master, m, v, grad, param_out, n, ws,
+                                                     stats, gscale_dev, skip_dev);
+        } else {
+          auto k = chunk_adam_occ_kernel<G, 1, false, 4>;
+          k<<<grid_for(k, units), kThreads, 0, st>>>(s, master, m, v, grad, param_out, n, ws,
+                                                     stats, gscale_dev, skip_dev);
+        }
+        launch_counter()++;
+        return check_cuda(cudaGetLastError(), "chunk_adam_occ_kernel launch");
+      }
+      default:
+        break;
+    }
   }
-  launch_counter()++;
+  if (stats)
+    launch_ldg<G, true>(s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st);
+  else
+    launch_ldg<G, false>(s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st);
   return check_cuda(cudaGetLastError(), "chunk_adam_kernel launch");
 }
 

@@ -55,6 +55,10 @@ CASES = [
      ["--hw", "a100x1"] + B200_LIKE + ["--gpu-optim-rate", "2e11", "--world-size", "1"]),
     ("plan_gpt2-1.5b_b8_b200x8", "plan", "gpt2-1.5b_b8",
      ["--hw", "a100x1"] + B200_LIKE + ["--gpu-optim-rate", "2e11", "--world-size", "8"]),
+    ("plan_gpt2-10b_b8_b200x8", "plan", "gpt2-10b_b8",
+     ["--hw", "a100x4"] + B200_LIKE + ["--world-size", "8"]),
+    ("plan_gpt2-10b_b8_b200x2_gpu2e11", "plan", "gpt2-10b_b8",
+     ["--hw", "a100x4"] + B200_LIKE + ["--gpu-optim-rate", "2e11", "--world-size", "2"]),
     ("plan_llama-13b_b8_b200x8", "plan", "llama-13b_b8",
      ["--hw", "a100x4"] + B200_LIKE + ["--gpu-optim-rate", "2e11", "--world-size", "8"]),
     ("estimate_gpt2-1.5b_b8_allpersist_w1", "estimate", "gpt2-1.5b_b8",
