@@ -22,6 +22,7 @@
 // bit.
 #include <cuda_runtime.h>
 
+#include <cctype>
 #include <cstdint>
 #include <cstdlib>
 #include <string>
@@ -618,25 +619,37 @@ constexpr int kUnroll = 2;
 
 // Kernel variant of the bf16-gradient chunk Adam. Selected once per process
 // from PTK_ADAM_VARIANT (benchmarking aid); the default is the measured best.
-enum class AdamVariant { Ldg, LdgOcc, Tma1024x8, Tma2048x6, Tma1024x6x2, Tma2048x6t512,
-                         Tma2048x7t512, Tma1024x12, Tma1024x12t512, Tma2048x5t512 };
+// TMA pipeline shapes: (name, tile elements, ring stages, CTAs per SM, threads).
+#define PTK_TMA_VARIANTS(X)               \
+  X(Tma1536x8t384, 1536, 8, 1, 384)       \
+  X(Tma2048x6, 2048, 6, 1, 256)           \
+  X(Tma1536x8t192, 1536, 8, 1, 192)       \
+  X(Tma3072x4t384, 3072, 4, 1, 384)       \
+  X(Tma1792x7t448, 1792, 7, 1, 448)       \
+  X(Tma1536x9t384, 1536, 9, 1, 384)       \
+  X(Tma1280x10t320, 1280, 10, 1, 320)
 
+#define PTK_ENUM_ENTRY(V, T, S, P, THR) V,
+enum class AdamVariant { Ldg, LdgOcc, PTK_TMA_VARIANTS(PTK_ENUM_ENTRY) };
+#undef PTK_ENUM_ENTRY
+
+// Default: the fastest shape measured on B200 (profiles/README.md).
 AdamVariant adam_variant() {
   static AdamVariant v = [] {
     const char* e = std::getenv("PTK_ADAM_VARIANT");
-    const std::string name = e ? e : "";
+    std::string name = e ? e : "";
+    for (auto& ch : name) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
     if (name == "ldg") return AdamVariant::Ldg;
     if (name == "ldg_occ") return AdamVariant::LdgOcc;
-    if (name == "tma2048x6") return AdamVariant::Tma2048x6;
-    if (name == "tma1024x6x2") return AdamVariant::Tma1024x6x2;
-    if (name == "tma1024x8") return AdamVariant::Tma1024x8;
-    if (name == "tma2048x6t512") return AdamVariant::Tma2048x6t512;
-    if (name == "tma2048x7t512") return AdamVariant::Tma2048x7t512;
-    if (name == "tma2048x5t512") return AdamVariant::Tma2048x5t512;
-    if (name == "tma1024x12") return AdamVariant::Tma1024x12;
-    if (name == "tma1536x8t384") return AdamVariant::Tma1024x12t512;
-    if (name == "tma2048x6") return AdamVariant::Tma2048x6;
-    return AdamVariant::Tma2048x6;
+#define PTK_NAME_ENTRY(V, T, S, P, THR)                                   \
+    {                                                                     \
+      std::string tag = #V;                                               \
+      for (auto& ch : tag) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch))); \
+      if (name == tag) return AdamVariant::V;                             \
+    }
+    PTK_TMA_VARIANTS(PTK_NAME_ENTRY)
+#undef PTK_NAME_ENTRY
+    return AdamVariant::Tma1536x8t384;
   }();
   return v;
 }
@@ -732,24 +745,8 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
     rc = adam_tma_then_tail<T, S, P, THR>(s, master, m, v, grad, param_out, n, ws, stats,    \
                                           gscale_dev, skip_dev, st);                         \
     return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
-      PTK_TMA_CASE(Tma2048x6t512, 2048, 6, 1, 512)
-      PTK_TMA_CASE(Tma2048x7t512, 2048, 7, 1, 512)
-      PTK_TMA_CASE(Tma2048x5t512, 2048, 5, 1, 512)
-      PTK_TMA_CASE(Tma1024x12, 1024, 12, 1, 256)
-      PTK_TMA_CASE(Tma1024x12t512, 1536, 8, 1, 384)
+      PTK_TMA_VARIANTS(PTK_TMA_CASE)
 #undef PTK_TMA_CASE
-      case AdamVariant::Tma1024x8:
-        rc = adam_tma_then_tail<1024, 8, 1, 256>(s, master, m, v, grad, param_out, n, ws, stats,
-                                            gscale_dev, skip_dev, st);
-        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
-      case AdamVariant::Tma2048x6:
-        rc = adam_tma_then_tail<2048, 6, 1, 256>(s, master, m, v, grad, param_out, n, ws, stats,
-                                            gscale_dev, skip_dev, st);
-        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
-      case AdamVariant::Tma1024x6x2:
-        rc = adam_tma_then_tail<1024, 6, 2, 256>(s, master, m, v, grad, param_out, n, ws, stats,
-                                            gscale_dev, skip_dev, st);
-        return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
       case AdamVariant::LdgOcc: {
         const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
         if (stats) {

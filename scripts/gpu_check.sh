@@ -14,7 +14,7 @@ echo "== ncu launch list"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_bench.log 2>&1; echo "ncu-list rc=$?"
 echo "== ncu full"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:chunk_adam -s 3 -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:chunk_adam_tma -s 2 -c 1 \
   -o $OUT/prof_adam -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1; echo "ncu-full rc=$?"
 fi
 echo done
