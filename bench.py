@@ -194,10 +194,16 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     numels, desc = chunk_numels(args.workload)
     comm = make_comm(world, rank)
-    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    mode = args.exchange
+    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode=mode, comm=comm)
     stream = torch.cuda.current_stream()
     cs.init_synthetic()
     cs.fill_grads(0)
+    if mode == "fused":
+        if world > 1:
+            cs.attach_ipc_peers()
+        else:
+            cs.attach_virtual_peers([cs])
     hyper = AdamHyper(lr=1e-3, weight_decay=0.0)
     torch.cuda.synchronize()
 
@@ -225,27 +231,8 @@ def run_gpu(args):
     value = total_bytes / (ms_max * 1e-3) / 1e9
 
     # Dominant kernel, timed per launch with events on its own stream.
-    sh = stream_handle(stream)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in cs.chunks]
-    cfg = hyper.config(cs.step_count + 1, world)
-    kern_ms, kern_bytes = 0.0, 0
-    reps = max(1, min(args.steps, 5))
-    torch.cuda.synchronize()
-    for _ in range(reps):
-        for c, (e0, e1) in zip(cs.chunks, ev):
-            e0.record(stream)
-            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
-                                   vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
-                                   c.shard, vp(cs.stats), vp(cs.workspace), None, None, sh)
-            e1.record(stream)
-        torch.cuda.synchronize()
-        for c, (e0, e1) in zip(cs.chunks, ev):
-            kern_ms += e0.elapsed_time(e1)
-            kern_bytes += 28 * (c.numel // world)
+    kern = time_dominant_kernel(cs, hyper, stream, world, reps=max(1, min(args.steps, 5)))
     hbm_peak, peak_kind = load_peaks()
-    achieved = kern_bytes / (kern_ms * 1e-3) / 1e9
-    n_launch = reps * len(cs.chunks)
 
     e2e = run_e2e(cs, hyper, args, world) if not args.no_e2e else None
     sumsq, nonfinite = cs.grad_stats()
@@ -253,7 +240,6 @@ def run_gpu(args):
     result = None
     if rank == 0:
         cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(numels, args)
-        traffic = traffic_from_profiles(args.workload)
         result = {
             "metric": "chunk step GB/s (gather+RS+fused Adam) vs HBM/NVLink roofline",
             "value": round(value, 2),
@@ -272,25 +258,15 @@ def run_gpu(args):
                 "params": sum(numels),
                 "chunks": len(numels),
                 "chunk_params": numels,
-                "exchange": "nccl RS/AG (in place)" if world > 1 else "none (w=1)",
+                "exchange": ({"nccl": "nccl RS/AG (in place)",
+                              "fused": "fused RS->Adam->AG kernel over NVLink peer memory"}[mode]
+                             if world > 1 else f"none (w=1, {mode} path)"),
                 "parallelism": f"zero3-dp{world}",
                 "l2": "inputs larger than L2 (%.1f GB touched per step)" % (bytes_rank / 1e9),
                 "algorithmic_bytes_per_step_per_rank": bytes_rank,
                 "nvlink_bytes_per_step_per_rank": cs.algorithmic_nvlink_bytes(),
             },
-            "roofline": {
-                "bound": "hbm",
-                "kernel": "chunk_adam_kernel<GradBf16,2,true>",
-                "achieved": round(achieved, 1),
-                "peak": hbm_peak,
-                "peak_kind": peak_kind,
-                "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4),
-                "traffic": traffic,
-                "bytes_per_launch": kern_bytes // n_launch,
-                "ms_per_launch": round(kern_ms / n_launch, 4),
-                "frac_of_8tbs_spec": round(achieved / 8000.0, 4),
-            },
+            "roofline": roofline(kern, hbm_peak, peak_kind, args.workload),
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -300,6 +276,66 @@ def run_gpu(args):
     if comm is not None:
         nat.lib.ptk_comm_destroy(comm)
     return result
+
+
+def time_dominant_kernel(cs, hyper, stream, world, reps):
+    """Average launch duration of the step's dominant kernel (CUDA events on
+    the stream it is launched on) and its algorithmic bytes per launch."""
+    import torch
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import stream_handle, vp
+    sh = stream_handle(stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in cs.chunks]
+    cfg = hyper.config(cs.step_count + 1, world)
+    ms, hbm, nvl = 0.0, 0, 0
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        for i, (c, (e0, e1)) in enumerate(zip(cs.chunks, ev)):
+            e0.record(stream)
+            if cs.mode == "fused":
+                nat.lib.ptk_fused_rs_adam_ag(ctypes.byref(cfg), cs.peer_grad_ptrs[i],
+                                             cs.peer_param_ptrs[i], world, cs.rank, c.shard,
+                                             vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq),
+                                             vp(cs.stats), vp(cs.workspace), sh)
+            else:
+                nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                                       vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                                       c.shard, vp(cs.stats), vp(cs.workspace), None, None, sh)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        for c, (e0, e1) in zip(cs.chunks, ev):
+            ms += e0.elapsed_time(e1)
+            p, w = c.numel, world
+            if cs.mode == "fused":
+                # local state 28P/w + grad shard reads 2P/w from each of w ranks
+                # + param shard writes to w ranks (counted once per byte moved)
+                hbm += 28 * p // w + 2 * p * (w - 1) // w * 2
+                nvl += 2 * p * (w - 1) // w
+            else:
+                hbm += 28 * p // w
+    n = reps * len(cs.chunks)
+    name = ("fused_peer_kernel<W>" if cs.mode == "fused"
+            else "chunk_adam_tma_kernel (" + nat.raw.ptk_adam_kernel_name().decode() + ")")
+    return {"kernel": name, "ms": ms, "hbm_bytes": hbm, "nvl_bytes": nvl, "launches": n,
+            "world": world}
+
+
+def roofline(k, hbm_peak, peak_kind, workload):
+    t_hbm = k["hbm_bytes"] / (hbm_peak * 1e9)
+    t_nvl = k["nvl_bytes"] / (NVLINK_GBS * 1e9)
+    nvl_bound = t_nvl > t_hbm
+    sec = k["ms"] * 1e-3
+    achieved = (k["nvl_bytes"] if nvl_bound else k["hbm_bytes"]) / sec / 1e9
+    peak = NVLINK_GBS if nvl_bound else hbm_peak
+    return {"bound": "nvlink" if nvl_bound else "hbm", "kernel": k["kernel"],
+            "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": "measured peer copy per direction (B200_PROFILING.md)" if nvl_bound
+            else peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": traffic_from_profiles(workload),
+            "bytes_per_launch": (k["nvl_bytes"] if nvl_bound else k["hbm_bytes"]) // k["launches"],
+            "ms_per_launch": round(k["ms"] / k["launches"], 4),
+            "frac_of_8tbs_spec": None if nvl_bound else round(achieved / 8000.0, 4)}
 
 
 def run_e2e(cs, hyper, args, world):
@@ -439,6 +475,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ptk", choices=["ptk", "reference"])
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="N>1 chunk exchange: NCCL RS/AG + fused Adam, or the single fused "
+                         "RS->Adam->AG kernel over NVLink peer memory")
     ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
     ap.add_argument("--no-e2e", action="store_true")

@@ -77,6 +77,8 @@ const char* ptk_version(void);
 int ptk_adam_derive(const ptk_adam_config* cfg, ptk_adam_scalars* out);
 /* elements per rank shard for a chunk of n elements: roundup(n, 8w)/w */
 int64_t ptk_shard_elems(int64_t n, int32_t world);
+/* name of the chunk-Adam kernel shape in use (PTK_ADAM_VARIANT or default) */
+const char* ptk_adam_kernel_name(void);
 /* scratch: CTA partial buffer the reducing kernels need (bytes) */
 int64_t ptk_stats_workspace_bytes(void);
 
@@ -152,7 +154,10 @@ int ptk_comm_barrier(ptk_comm* comm, void* stream);
 
 /* ---- NVLink peer memory for the fused path ---------------------------- */
 #define PTK_IPC_HANDLE_BYTES 64
-int ptk_ipc_get_handle(void* dev_ptr, uint8_t out[PTK_IPC_HANDLE_BYTES]);
+/* Handle of the allocation containing dev_ptr; *offset_out = dev_ptr - base
+ * (buffers carved from a caching allocator are sub-ranges of an allocation). */
+int ptk_ipc_get_handle(void* dev_ptr, uint8_t out[PTK_IPC_HANDLE_BYTES], int64_t* offset_out);
+/* Maps a peer allocation; *dev_ptr = its base (add the peer's offset). */
 int ptk_ipc_open_handle(const uint8_t handle[PTK_IPC_HANDLE_BYTES], void** dev_ptr);
 int ptk_ipc_close_handle(void* dev_ptr);
 /* signal_peers[r]: rank r's int32[PTK_MAX_PEERS] signal slots (zeroed once).

@@ -52,6 +52,7 @@ _SIGNATURES = {
     "ptk_adam_derive": (c_int32, [POINTER(AdamConfig), POINTER(AdamScalars)]),
     "ptk_shard_elems": (c_int64, [c_int64, c_int32]),
     "ptk_stats_workspace_bytes": (c_int64, []),
+    "ptk_adam_kernel_name": (c_char_p, []),
     "ptk_chunk_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),
@@ -73,7 +74,7 @@ _SIGNATURES = {
     "ptk_chunk_allgather": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "ptk_chunk_reduce_scatter": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "ptk_comm_barrier": (c_int32, [c_void_p, c_void_p]),
-    "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8)]),
+    "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8), POINTER(c_int64)]),
     "ptk_ipc_open_handle": (c_int32, [POINTER(c_uint8), POINTER(c_void_p)]),
     "ptk_ipc_close_handle": (c_int32, [c_void_p]),
     "ptk_peer_barrier": (c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int32, c_void_p]),

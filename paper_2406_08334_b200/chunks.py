@@ -250,6 +250,52 @@ class ChunkSet:
             self.peer_grad_ptrs.append(g)
             self.peer_param_ptrs.append(p)
 
+    def attach_ipc_peers(self, group=None) -> None:
+        """Multi-GPU fused mode: map every peer's gradient / parameter chunk
+        buffers and signal slots into this process over NVLink (cudaIpc
+        handles exchanged through torch.distributed, which is only plumbing
+        here). Must be called collectively by all ranks."""
+        import torch.distributed as dist
+        arr = ctypes.c_void_p * PTK_MAX
+        self.signal = torch.zeros(PTK_MAX, dtype=torch.int32, device=self.device)
+        mine = []
+        for t in [c.grad for c in self.chunks] + [c.param for c in self.chunks] + [self.signal]:
+            h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
+            off = ctypes.c_int64()
+            nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
+            mine.append((bytes(h), off.value))
+        torch.cuda.synchronize(self.device)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []
+        ptrs = []  # ptrs[r][k]: rank r's k-th buffer as mapped here
+        for r in range(self.world):
+            row = []
+            for k, (hb, off) in enumerate(everyone[r]):
+                if r == self.rank:
+                    own = ([c.grad for c in self.chunks] + [c.param for c in self.chunks] +
+                           [self.signal])[k]
+                    row.append(own.data_ptr())
+                    continue
+                base = ctypes.c_void_p()
+                nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
+                                            ctypes.byref(base))
+                self._opened.append(base)
+                row.append(base.value + off)
+            ptrs.append(row)
+        n = len(self.chunks)
+        self.peer_grad_ptrs = [arr(*[ptrs[r][ci] for r in range(self.world)]) for ci in range(n)]
+        self.peer_param_ptrs = [arr(*[ptrs[r][n + ci] for r in range(self.world)])
+                                for ci in range(n)]
+        self.signal_ptrs = arr(*[ptrs[r][2 * n] for r in range(self.world)])
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def close_ipc_peers(self) -> None:
+        for base in getattr(self, "_opened", []):
+            nat.lib.ptk_ipc_close_handle(base)
+        self._opened = []
+
     def grad_stats(self) -> tuple[float, int]:
         v = self.stats.cpu()
         sumsq = float(v[0])

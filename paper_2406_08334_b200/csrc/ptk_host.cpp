@@ -140,13 +140,31 @@ int ptk_device_synchronize(void) {
 
 int64_t ptk_kernel_launch_count(void) { return ptk::launch_counter().load(); }
 
-int ptk_ipc_get_handle(void* dev_ptr, uint8_t out[PTK_IPC_HANDLE_BYTES]) {
+int ptk_ipc_get_handle(void* dev_ptr, uint8_t out[PTK_IPC_HANDLE_BYTES], int64_t* offset_out) {
   static_assert(sizeof(cudaIpcMemHandle_t) <= PTK_IPC_HANDLE_BYTES, "ipc handle size");
-  if (!dev_ptr || !out) return fail(PTK_EINVAL, "ptk_ipc_get_handle: null argument");
+  if (!dev_ptr || !out || !offset_out) return fail(PTK_EINVAL, "ptk_ipc_get_handle: null argument");
+  // Allocation base through the driver entry point (no link-time libcuda
+  // dependency, so the library still loads on a machine without a driver).
+  using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<GetRange>(nullptr);
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range) return fail(PTK_ECUDA, "ptk_ipc_get_handle: cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+    return fail(PTK_ECUDA, "ptk_ipc_get_handle: cuMemGetAddressRange failed");
   cudaIpcMemHandle_t h;
-  PTK_TRY_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+  PTK_TRY_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
   std::memset(out, 0, PTK_IPC_HANDLE_BYTES);
   std::memcpy(out, &h, sizeof(h));
+  *offset_out = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
   return PTK_OK;
 }
 

@@ -790,6 +790,19 @@ extern "C" {
 
 int64_t ptk_stats_workspace_bytes(void) { return static_cast<int64_t>(sizeof(StatsWorkspace)); }
 
+const char* ptk_adam_kernel_name(void) {
+  switch (adam_variant()) {
+    case AdamVariant::Ldg: return "ldg";
+    case AdamVariant::LdgOcc: return "ldg_occ";
+#define PTK_NAME_CASE(V, T, S, P, THR) \
+  case AdamVariant::V:                 \
+    return "tma tile=" #T " stages=" #S " ctas/sm=" #P " threads=" #THR;
+    PTK_TMA_VARIANTS(PTK_NAME_CASE)
+#undef PTK_NAME_CASE
+  }
+  return "?";
+}
+
 int ptk_chunk_adam(const ptk_adam_config* cfg, float* master, float* exp_avg, float* exp_avg_sq,
                    const uint16_t* grad, uint16_t* param_out, int64_t n, ptk_grad_stats_t* stats,
                    void* workspace, const float* gscale_dev, const int32_t* skip_dev,
