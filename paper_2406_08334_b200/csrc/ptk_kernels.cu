@@ -350,7 +350,7 @@ template <int kTile, int kStages, int kThr, bool kStats>
 __global__ void __launch_bounds__(kThr, 1)
 chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
                       float* __restrict__ exp_avg_sq, const uint16_t* __restrict__ grad,
-                      uint16_t* __restrict__ param_out, int64_t n_tiles, StatsWorkspace* ws,
+                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
                       ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
   static_assert(kTile % (kThr * 4) == 0, "tile must be a multiple of 4 elements per thread");
   static_assert(kStages >= 3, "ring needs >= 3 stages");
@@ -365,7 +365,7 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
   const int tid = threadIdx.x;
   // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
   const int64_t my_tiles =
-      n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      n / kTile > blockIdx.x ? (n / kTile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   constexpr uint32_t kLoadBytes = kTile * (3 * sizeof(float) + sizeof(uint16_t));
   const bool has_param = param_out != nullptr;
 
@@ -437,6 +437,22 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     }
   }
   if (tid == 0) bulk_wait_all();
+  // The last CTA also updates the partial tile (< kTile elements) with plain
+  // loads, so a chunk is one launch whatever its size.
+  if (blockIdx.x == gridDim.x - 1) {
+    float usq = 0.0f;
+    for (int64_t e = n / kTile * kTile + tid; e < n; e += kThr) {
+      const float gk = __fmul_rn(GradBf16::load1(grad + e), gs);
+      if (kStats) accum_stats(gk, usq, bad);
+      float p = master[e], mm = exp_avg[e], vv = exp_avg_sq[e];
+      adam_elem(s, gk, p, mm, vv);
+      master[e] = p;
+      exp_avg[e] = mm;
+      exp_avg_sq[e] = vv;
+      if (has_param) param_out[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
+    }
+    if (kStats) sq += usq;
+  }
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
 
@@ -675,7 +691,7 @@ void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
 
 template <int kTile, int kStages, int kPerSm, int kThr, bool kStats>
 int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
-               const uint16_t* grad, uint16_t* param_out, int64_t n_tiles, StatsWorkspace* ws,
+               const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                cudaStream_t st) {
   auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats>;
@@ -687,38 +703,25 @@ int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
     configured = true;
   }
   int64_t grid = static_cast<int64_t>(sm_count()) * kPerSm;
-  if (grid > n_tiles) grid = n_tiles;
-  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, master, m, v, grad, param_out, n_tiles, ws,
-                                                     stats, gscale_dev, skip_dev);
+  if (grid > n / kTile) grid = n / kTile;
+  if (grid < 1) grid = 1;  // partial tile only
+  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, master, m, v, grad, param_out, n, ws, stats,
+                                                 gscale_dev, skip_dev);
   launch_counter()++;
   return PTK_OK;
 }
 
+// One launch per chunk: full tiles through the TMA ring, the partial tile by
+// the last CTA.
 template <int kTile, int kStages, int kPerSm, int kThr>
 int adam_tma_then_tail(const ptk_adam_scalars& s, float* master, float* m, float* v,
                        const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
                        ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                        cudaStream_t st) {
-  const int64_t tiles = n / kTile;
-  const int64_t done = tiles * kTile;
-  int rc = PTK_OK;
-  if (tiles > 0) {
-    rc = stats ? launch_tma<kTile, kStages, kPerSm, kThr, true>(
-                     s, master, m, v, grad, param_out, tiles, ws, stats, gscale_dev, skip_dev, st)
+  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true>(
+                     s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st)
                : launch_tma<kTile, kStages, kPerSm, kThr, false>(
-                     s, master, m, v, grad, param_out, tiles, ws, stats, gscale_dev, skip_dev, st);
-    if (rc != PTK_OK) return rc;
-  }
-  if (done < n) {
-    uint16_t* po = param_out ? param_out + done : nullptr;
-    if (stats)
-      launch_ldg<GradBf16, true>(s, master + done, m + done, v + done, grad + done, po, n - done,
-                                 ws, stats, gscale_dev, skip_dev, st);
-    else
-      launch_ldg<GradBf16, false>(s, master + done, m + done, v + done, grad + done, po, n - done,
-                                  ws, stats, gscale_dev, skip_dev, st);
-  }
-  return rc;
+                     s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st);
 }
 
 template <class G>
