@@ -236,6 +236,15 @@ def run_gpu(args):
 
     e2e = run_e2e(cs, hyper, args, world) if not args.no_e2e else None
     sumsq, nonfinite = cs.grad_stats()
+    nvl_bytes_rank = cs.algorithmic_nvlink_bytes()
+    if mode == "fused" and world > 1:
+        cs.close_ipc_peers()
+    del cs
+    torch.cuda.empty_cache()
+    train = None
+    if args.train_steps > 0 and args.workload == "cfg2":
+        train = run_train(args, world, rank, dev, comm)
+    copy_peak = live_copy_peak()
 
     result = None
     if rank == 0:
@@ -264,10 +273,14 @@ def run_gpu(args):
                 "parallelism": f"zero3-dp{world}",
                 "l2": "inputs larger than L2 (%.1f GB touched per step)" % (bytes_rank / 1e9),
                 "algorithmic_bytes_per_step_per_rank": bytes_rank,
-                "nvlink_bytes_per_step_per_rank": cs.algorithmic_nvlink_bytes(),
+                "nvlink_bytes_per_step_per_rank": nvl_bytes_rank,
             },
-            "roofline": roofline(kern, hbm_peak, peak_kind, args.workload),
+            "roofline": dict(roofline(kern, hbm_peak, peak_kind, args.workload),
+                             live_copy_gbs_this_box=copy_peak,
+                             frac_of_live_copy=round(kern["hbm_bytes"] / (kern["ms"] * 1e-3) /
+                                                     1e9 / copy_peak, 4)),
             "e2e": e2e,
+            "train": train,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "grad_stats": {"sumsq": sumsq, "nonfinite": nonfinite},
@@ -336,6 +349,74 @@ def roofline(k, hbm_peak, peak_kind, workload):
             "bytes_per_launch": (k["nvl_bytes"] if nvl_bound else k["hbm_bytes"]) // k["launches"],
             "ms_per_launch": round(k["ms"] / k["launches"], 4),
             "frac_of_8tbs_spec": None if nvl_bound else round(achieved / 8000.0, 4)}
+
+
+def live_copy_peak():
+    """This box's HBM copy bandwidth, measured like MEASURED_PEAKS.json
+    ('b.copy_(a) over 1 Gi bf16 elements, read+write bytes, best of 10'), to
+    separate box-to-box HBM variance from kernel quality."""
+    import torch
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return round(2 * 2 * (1 << 30) / (best * 1e-3) / 1e9, 1)
+
+
+def run_train(args, world, rank, dev, comm):
+    """tokens/s of a full training iteration of the cfg2 model (GPT-2 1.5B,
+    b8, seq 1024) whose parameters live in the planner's chunk buffers:
+    forward + backward in PyTorch (bf16 GEMMs / SDPA), then the chunk step
+    (RS -> fused Adam -> AG) through the C-ABI. Random-init weights, synthetic
+    uniform tokens; CUDA-event time over the timed iterations, max over ranks."""
+    import torch
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    trace = planner.trace_for("gpt2-1.5b_b8")
+    layout = planner.layout_for("gpt2-1.5b_b8")
+    numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
+    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
+    model = ChunkedGPT2(shape, layout, cs, trace["ops"])
+    model.init_weights(seed=0)
+    batch = int(trace["meta"]["batch_size"])
+    n_iter = args.warmup + args.train_steps
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    tokens = torch.randint(0, shape.vocab, (n_iter, batch, shape.seq + 1), device=dev,
+                           generator=gen)
+    hyper = AdamHyper(lr=1e-4, weight_decay=0.01, adamw=True)
+    stream = torch.cuda.current_stream()
+    losses = []
+    for i in range(args.warmup):
+        losses.append(train_step(model, tokens[i, :, :-1], tokens[i, :, 1:], hyper))
+    torch.cuda.synchronize()
+    barrier(world)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.warmup, n_iter):
+        losses.append(train_step(model, tokens[i, :, :-1], tokens[i, :, 1:], hyper))
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.train_steps, world)
+    loss_vals = [float(x) for x in losses]
+    del model, cs
+    torch.cuda.empty_cache()
+    return {"tokens_per_s": round(batch * shape.seq * world / (ms * 1e-3), 1),
+            "ms_per_iter": round(ms, 3), "iters": args.train_steps,
+            "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, no final LN as in the trace), "
+                     f"b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
+            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
+            "data": "synthetic uniform tokens, random init"}
 
 
 def run_e2e(cs, hyper, args, world):
@@ -481,6 +562,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=10,
+                    help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -32,6 +32,24 @@ def run_memplan(args: list[str]) -> str:
                           text=True).stdout
 
 
+def trace_file(args: list[str], path: str) -> str:
+    """Synthesize a trace with the planner (`memplan gen-trace`)."""
+    run_memplan(["gen-trace"] + args + ["-o", path])
+    return path
+
+
+def trace_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
+    os.makedirs(scratch, exist_ok=True)
+    with open(trace_file(TRACE_ARGS[name], os.path.join(scratch, f"trace_{name}.json"))) as f:
+        return json.load(f)
+
+
+def pack(trace_path: str, grid: str | None = None) -> dict:
+    out = json.loads(run_memplan(["pack", "--trace", trace_path] + (["--grid", grid] if grid else [])))
+    out.setdefault("bytes_per_param", 2)
+    return out
+
+
 def layout_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
     """Chunk layout of a named trace, produced by the clean-room planner."""
     if not os.path.exists(MEMPLAN_BIN):

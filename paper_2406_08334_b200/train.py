@@ -1,0 +1,164 @@
+"""End-to-end chunked training step: a GPT-2 shaped decoder whose parameters
+live in the planner's chunk buffers, trained with the B200 chunk data plane.
+
+The model is exactly the operator sequence the reference synthesizes for the
+trace (proj/src/trace.cpp:213-242,316-340): embedding (token + learned
+position), per block {attn_norm, attn_qkv, attn_core, attn_out, mlp_norm,
+mlp_up, mlp_act, mlp_down}, tied lm_head, cross-entropy. (Like the trace it
+has no final LayerNorm.) Parameters are views into the chunk buffers of the
+`ChunkLayout` computed by the planner, in execution order — parameter bytes of
+op i start at the prefix sum of param_bytes within its chunk (SURVEY §8(a)
+a9) — so the chunk the data plane updates is byte-for-byte the chunk the
+planner packed.
+
+One iteration (ZeRO-3 chunk semantics):
+  1. parameters are the gathered bf16 chunk buffers (all-gathered at the end
+     of the previous step);
+  2. forward + backward in PyTorch (cuBLAS GEMMs / SDPA attention: the only
+     tensor-core work of the step); each parameter's gradient is
+     copied into its slot of the chunk's flat bf16 gradient buffer by a
+     post-accumulate hook;
+  3. the chunk step — reduce-scatter -> fused Adam -> all-gather — through the
+     C-ABI (ChunkSet.step).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from .chunks import AdamHyper, ChunkSet
+
+BF16 = torch.bfloat16
+
+
+@dataclass
+class GPT2Shape:
+    hidden: int = 1600
+    blocks: int = 48
+    heads: int = 25
+    vocab: int = 50257
+    seq: int = 1024
+
+    @staticmethod
+    def from_trace_meta(meta: dict, n_blocks: int) -> "GPT2Shape":
+        return GPT2Shape(int(meta["hidden_size"]), n_blocks, int(meta["n_heads"]),
+                         int(meta["vocab_size"]), int(meta["seq_len"]))
+
+
+def op_param_shapes(shape: GPT2Shape) -> list[tuple[str, list[tuple[str, tuple[int, ...]]]]]:
+    """(op name, [(param name, shape)...]) in trace order, GPT-2 with biases and
+    tied embeddings (proj/src/trace.cpp:213-242)."""
+    h, v, s = shape.hidden, shape.vocab, shape.seq
+    ops = [("embedding", [("wte", (v, h)), ("wpe", (s, h))])]
+    for b in range(shape.blocks):
+        ops += [
+            (f"attn_norm.{b}", [("ln1_w", (h,)), ("ln1_b", (h,))]),
+            (f"attn_qkv.{b}", [("qkv_w", (3 * h, h)), ("qkv_b", (3 * h,))]),
+            (f"attn_core.{b}", []),
+            (f"attn_out.{b}", [("out_w", (h, h)), ("out_b", (h,))]),
+            (f"mlp_norm.{b}", [("ln2_w", (h,)), ("ln2_b", (h,))]),
+            (f"mlp_up.{b}", [("up_w", (4 * h, h)), ("up_b", (4 * h,))]),
+            (f"mlp_act.{b}", []),
+            (f"mlp_down.{b}", [("down_w", (h, 4 * h)), ("down_b", (h,))]),
+        ]
+    ops += [("lm_head", []), ("cross_entropy", [])]
+    return ops
+
+
+class ChunkedGPT2:
+    """GPT-2 whose parameters are views into a ChunkSet's gathered buffers."""
+
+    def __init__(self, shape: GPT2Shape, layout: dict, chunks: ChunkSet, trace_ops: list[dict]):
+        self.shape = shape
+        self.chunks = chunks
+        specs = op_param_shapes(shape)
+        if len(specs) != len(trace_ops):
+            raise ValueError(f"model has {len(specs)} ops, trace has {len(trace_ops)}")
+        # op index -> chunk (the layout's spans), then prefix offsets in op order
+        chunk_of = {}
+        for c in layout["chunks"]:
+            for i in range(c["first_op"], c["last_op"] + 1):
+                chunk_of[i] = c["chunk_id"]
+        offset = [0] * len(layout["chunks"])
+        self.params: dict[str, torch.Tensor] = {}
+        self.blocks: list[dict[str, torch.Tensor]] = [dict() for _ in range(shape.blocks)]
+        self._hooks = []
+        for i, ((name, plist), top) in enumerate(zip(specs, trace_ops)):
+            assert top["name"] == name, (top["name"], name)
+            n_el = sum(math.prod(s) for _, s in plist)
+            assert 2 * n_el == top["param_bytes"], (name, 2 * n_el, top["param_bytes"])
+            ci = chunk_of[i]
+            cs = chunks.chunks[ci]
+            for pname, pshape in plist:
+                numel = math.prod(pshape)
+                lo = offset[ci]
+                p = cs.param[lo:lo + numel].view(pshape)
+                p.requires_grad_(True)
+                g = cs.grad[lo:lo + numel].view(pshape)
+                self._hooks.append(p.register_post_accumulate_grad_hook(_stash_into(g)))
+                offset[ci] += numel
+                if "." in name:
+                    self.blocks[int(name.split(".")[1])][pname] = p
+                else:
+                    self.params[pname] = p
+        for ci, c in enumerate(layout["chunks"]):
+            assert 2 * offset[ci] == c["used_bytes"], "chunk payload mismatch"
+
+    def init_weights(self, seed: int = 0) -> None:
+        """GPT-2 style init, written straight into the chunk buffers; the
+        fp32 master copies are refreshed from them."""
+        g = torch.Generator(device=self.chunks.device).manual_seed(seed)
+        std = 0.02
+        with torch.no_grad():
+            for p in [self.params["wte"], self.params["wpe"]]:
+                p.normal_(0.0, std, generator=g)
+            for blk in self.blocks:
+                for k, p in blk.items():
+                    if k.endswith("_w") and p.dim() == 2:
+                        s = std / math.sqrt(2 * self.shape.blocks) if k in ("out_w", "down_w") else std
+                        p.normal_(0.0, s, generator=g)
+                    elif k in ("ln1_w", "ln2_w"):
+                        p.fill_(1.0)
+                    else:
+                        p.zero_()
+            for c in self.chunks.chunks:
+                c.master.copy_(c.param_shard().float())
+                c.exp_avg.zero_()
+                c.exp_avg_sq.zero_()
+
+    def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        sh = self.shape
+        b, s = tokens.shape
+        x = F.embedding(tokens, self.params["wte"]) + self.params["wpe"][:s]
+        for blk in self.blocks:
+            y = F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"])
+            qkv = F.linear(y, blk["qkv_w"], blk["qkv_b"])
+            q, k, v = qkv.view(b, s, 3, sh.heads, sh.hidden // sh.heads).unbind(2)
+            a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                               v.transpose(1, 2), is_causal=True)
+            x = x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"], blk["out_b"])
+            y = F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"])
+            y = F.gelu(F.linear(y, blk["up_w"], blk["up_b"]), approximate="tanh")
+            x = x + F.linear(y, blk["down_w"], blk["down_b"])
+        logits = F.linear(x, self.params["wte"])  # tied lm_head
+        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.view(-1))
+
+
+def _stash_into(slot: torch.Tensor):
+    def hook(p: torch.Tensor) -> None:
+        slot.copy_(p.grad)
+        p.grad = None
+    return hook
+
+
+def train_step(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
+               hyper: AdamHyper) -> torch.Tensor:
+    """One iteration; returns the (device) loss. Gradient slots of the chunk
+    buffers are fully overwritten by the hooks each step (padding stays 0)."""
+    loss = model.loss(tokens, targets)
+    loss.backward()
+    model.chunks.step(hyper)
+    return loss.detach()
