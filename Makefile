@@ -35,8 +35,16 @@ $(OBJ)/%.o: $(PKG)/csrc/%.cpp $(PKG)/csrc/ptk_common.h include/ptk.h
 	@mkdir -p $(OBJ)
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 
-$(PKG)/libptk.so: $(PTK_OBJS)
-	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lnccl -Xcompiler -fopenmp -lgomp
+# libptk.so = data-plane kernels + C-ABI + the planner + the chunk runtime
+RT_SRC  := executor profile
+RT_OBJS := $(addprefix $(OBJ)/rt_,$(addsuffix .o,$(RT_SRC)))
+
+$(OBJ)/rt_%.o: $(PKG)/csrc/runtime/%.cpp include/ptk.h include/memplan/execute.hpp $(PKG)/csrc/ptk_common.h
+	@mkdir -p $(OBJ)
+	$(CXX) -std=c++20 -O2 -fPIC -pthread -Wall -Wextra -Iinclude -I$(JSON_DIR) -I/usr/local/cuda/include -c $< -o $@
+
+$(PKG)/libptk.so: $(PTK_OBJS) $(PLAN_OBJS) $(RT_OBJS)
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lnccl -Xcompiler -fopenmp -lgomp -Xcompiler -pthread
 
 # ---- planner (drop-in memplan API) -----------------------------------------
 PLAN_SRC  := model serialize packing costmodel search simulator cli

@@ -134,6 +134,10 @@ int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, f
 int ptk_fill_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, int64_t index0, float scale,
                           void* stream);
 
+/* Occupies `stream` for ns nanoseconds of device time: the stand-in for an
+ * operator's compute when a trace is executed without its model. */
+int ptk_busy_wait(int64_t ns, void* stream);
+
 /* ---- K3 / K4: NCCL chunk collectives --------------------------------- */
 typedef struct ptk_comm ptk_comm;
 #define PTK_UNIQUE_ID_BYTES 128
@@ -179,6 +183,23 @@ int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
                  float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
                  int64_t n, int32_t n_threads, double* sumsq_out,
                  int64_t* nonfinite_out);
+
+/* ---- the chunk runtime (memplan::execute) and the profiler re-feed ----- */
+/* Executes `iterations` iterations of a plan (plan JSON as written by
+ * `memplan plan`, or a bare PlanConfig) for a trace (trace JSON) on this
+ * device with the hardware profile (profile JSON): real chunk storage,
+ * uploads/offloads, collectives and optimizer updates; stand-in compute of
+ * compute_scale x the trace's op times. Writes the measured result (the
+ * simulator's summary schema + estimate_t_iter + byte counters) as JSON and
+ * the measured event timeline as CSV (either path may be NULL). */
+int ptk_execute_plan(const char* trace_path, const char* plan_path, const char* profile_path,
+                     void* comm, int32_t rank, double compute_scale, int32_t iterations,
+                     const char* result_json_path, const char* timeline_csv_path);
+/* Measures this machine's HardwareProfile (H2D/D2H, NCCL alpha/beta when
+ * comm != NULL, device/host Adam rates, memory) starting from a base profile
+ * JSON and writes the measured profile JSON to out_path. */
+int ptk_measure_profile(const char* base_profile_path, void* comm, int32_t world,
+                        const char* out_path);
 
 /* ---- streams / events / timing helpers used by the host runtime ------- */
 int ptk_stream_create(void** out, int32_t high_priority);

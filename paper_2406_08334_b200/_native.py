@@ -68,6 +68,7 @@ _SIGNATURES = {
                                        c_void_p, c_void_p, c_void_p]),
     "ptk_fill_uniform_f32": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
     "ptk_fill_uniform_bf16": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
+    "ptk_busy_wait": (c_int32, [c_int64, c_void_p]),
     "ptk_comm_unique_id": (c_int32, [POINTER(c_uint8)]),
     "ptk_comm_init": (c_int32, [POINTER(c_void_p), c_int32, c_int32, POINTER(c_uint8)]),
     "ptk_comm_destroy": (c_int32, [c_void_p]),
@@ -84,6 +85,9 @@ _SIGNATURES = {
     "ptk_memcpy_d2h_async": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "ptk_cpu_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_int64, c_int32, POINTER(c_double), POINTER(c_int64)]),
+    "ptk_execute_plan": (c_int32, [c_char_p, c_char_p, c_char_p, c_void_p, c_int32, c_double,
+                                   c_int32, c_char_p, c_char_p]),
+    "ptk_measure_profile": (c_int32, [c_char_p, c_void_p, c_int32, c_char_p]),
     "ptk_stream_create": (c_int32, [POINTER(c_void_p), c_int32]),
     "ptk_stream_destroy": (c_int32, [c_void_p]),
     "ptk_event_create": (c_int32, [POINTER(c_void_p)]),

@@ -578,6 +578,17 @@ __global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int ep
   } while (seen < epoch);
 }
 
+// Occupies the stream for `ns` nanoseconds of device time (global timer).
+// Stand-in for an operator's compute when the executor replays a trace
+// without the model (the real model's kernels replace it in training).
+__global__ void busy_wait_kernel(int64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (static_cast<int64_t>(t - t0) < ns);
+}
+
 // ----------------------------------------------------------- synthetic ----
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -908,6 +919,14 @@ int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank, 
   peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch);
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "peer_barrier_kernel launch");
+}
+
+int ptk_busy_wait(int64_t ns, void* stream) {
+  if (ns < 0) return fail(PTK_EINVAL, "ptk_busy_wait: negative duration");
+  if (ns == 0) return PTK_OK;
+  busy_wait_kernel<<<1, 1, 0, as_stream(stream)>>>(ns);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "busy_wait_kernel launch");
 }
 
 int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, float scale,

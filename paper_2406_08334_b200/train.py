@@ -144,7 +144,7 @@ class ChunkedGPT2:
             y = F.gelu(F.linear(y, blk["up_w"], blk["up_b"]), approximate="tanh")
             x = x + F.linear(y, blk["down_w"], blk["down_b"])
         logits = F.linear(x, self.params["wte"])  # tied lm_head
-        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.view(-1))
+        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
 
 
 def _stash_into(slot: torch.Tensor):
