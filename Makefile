@@ -22,6 +22,10 @@ PTK_CU   := $(PKG)/csrc/ptk_kernels.cu
 PTK_CPP  := $(PKG)/csrc/ptk_host.cpp $(PKG)/csrc/ptk_comm.cpp $(PKG)/csrc/ptk_cpu_adam.cpp
 PTK_OBJS := $(OBJ)/ptk_kernels.o $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(PTK_CPP))
 
+PLAN_SRC  := model serialize packing costmodel search simulator cli
+PLAN_OBJS := $(addprefix $(OBJ)/planner_,$(addsuffix .o,$(PLAN_SRC)))
+PLANFLAGS := -std=c++20 -O2 -fPIC -pthread -ffp-contract=off -Wall -Wextra -Iinclude -I$(JSON_DIR)
+
 .PHONY: all ptk planner oracle reftests clean
 all: ptk planner oracle
 
@@ -47,10 +51,6 @@ $(PKG)/libptk.so: $(PTK_OBJS) $(PLAN_OBJS) $(RT_OBJS)
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $^ -lnccl -Xcompiler -fopenmp -lgomp -Xcompiler -pthread
 
 # ---- planner (drop-in memplan API) -----------------------------------------
-PLAN_SRC  := model serialize packing costmodel search simulator cli
-PLAN_OBJS := $(addprefix $(OBJ)/planner_,$(addsuffix .o,$(PLAN_SRC)))
-PLANFLAGS := -std=c++20 -O2 -fPIC -pthread -ffp-contract=off -Wall -Wextra -Iinclude -I$(JSON_DIR)
-
 planner: build/libmemplan.a $(PKG)/libmemplan.so build/memplan
 
 $(OBJ)/planner_%.o: $(PKG)/csrc/planner/%.cpp $(wildcard include/memplan/*.hpp) $(PKG)/csrc/planner/digest.hpp
