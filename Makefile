@@ -16,7 +16,7 @@ PY_SITE  ?= $(shell python -c "import sysconfig;print(sysconfig.get_paths()['pur
 JSON_DIR ?= $(PY_SITE)/include/cudnn_frontend/thirdparty/nlohmann
 
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -ccbin $(CXX) -Xcompiler -fPIC -Iinclude -Xptxas -v
-HOSTFLAGS := -O3 -std=c++17 -fPIC -fopenmp -Iinclude -I/usr/local/cuda/include -ffp-contract=off
+HOSTFLAGS := -O3 -std=c++17 -fPIC -fopenmp -fno-math-errno -Iinclude -I/usr/local/cuda/include -ffp-contract=off
 
 PTK_CU   := $(PKG)/csrc/ptk_kernels.cu
 PTK_CPP  := $(PKG)/csrc/ptk_host.cpp $(PKG)/csrc/ptk_comm.cpp $(PKG)/csrc/ptk_cpu_adam.cpp

@@ -21,14 +21,20 @@ int oracle_num_threads(void) {
 static inline uint32_t f2u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 static inline float u2f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 
-uint16_t oracle_f32_to_bf16(float f) {
+static inline uint16_t to_bf16(float f) {
   uint32_t u = f2u(f);
   if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fff; /* canonical NaN */
   u += 0x7fffu + ((u >> 16) & 1u);                    /* round to nearest even */
   return (uint16_t)(u >> 16);
 }
 
-float oracle_bf16_to_f32(uint16_t h) { return u2f((uint32_t)h << 16); }
+static inline float from_bf16(uint16_t h) { return u2f((uint32_t)h << 16); }
+
+/* exported wrappers (internal loops use the inline forms so they vectorise) */
+uint16_t oracle_f32_to_bf16(float f) { return to_bf16(f); }
+float oracle_bf16_to_f32(uint16_t h) { return from_bf16(h); }
+#define oracle_f32_to_bf16 to_bf16
+#define oracle_bf16_to_f32 from_bf16
 
 void oracle_adam_scalars(double lr, double beta1, double beta2, double eps,
                          double weight_decay, int adamw, int step,
@@ -65,18 +71,34 @@ static inline float adam_elem(const oracle_adam_scalars_t* s, float g, float* p,
   return pv;
 }
 
+/* Blocks of 64 Ki elements per OpenMP iteration: the fp64 statistics loop
+ * and the (vectorisable, reduction-free) update loop run per block. */
+#define ORACLE_BLOCK ((int64_t)1 << 16)
+
 void oracle_adam_step(const oracle_adam_scalars_t* s, float* master, float* m,
                       float* v, const uint16_t* grad, uint16_t* param_out,
                       int64_t n, double* sumsq, int64_t* nonfinite) {
   double sq = 0.0;
   int64_t bad = 0;
+  const int64_t blocks = (n + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
 #pragma omp parallel for schedule(static) reduction(+ : sq, bad)
-  for (int64_t i = 0; i < n; ++i) {
-    const float g = oracle_bf16_to_f32(grad[i]) * s->gscale;
-    sq += (double)g * (double)g;
-    bad += isfinite(g) ? 0 : 1;
-    const float p = adam_elem(s, g, &master[i], &m[i], &v[i]);
-    if (param_out) param_out[i] = oracle_f32_to_bf16(p);
+  for (int64_t b = 0; b < blocks; ++b) {
+    const int64_t lo = b * ORACLE_BLOCK;
+    const int64_t hi = lo + ORACLE_BLOCK < n ? lo + ORACLE_BLOCK : n;
+    for (int64_t i = lo; i < hi; ++i) {
+      const float g = oracle_bf16_to_f32(grad[i]) * s->gscale;
+      sq += (double)g * (double)g;
+      bad += isfinite(g) ? 0 : 1;
+    }
+    const oracle_adam_scalars_t sc = *s; /* local copy: provably not aliased by the stores */
+    if (param_out) {
+      for (int64_t i = lo; i < hi; ++i)
+        param_out[i] = oracle_f32_to_bf16(
+            adam_elem(&sc, oracle_bf16_to_f32(grad[i]) * sc.gscale, &master[i], &m[i], &v[i]));
+    } else {
+      for (int64_t i = lo; i < hi; ++i)
+        adam_elem(&sc, oracle_bf16_to_f32(grad[i]) * sc.gscale, &master[i], &m[i], &v[i]);
+    }
   }
   if (sumsq) *sumsq = sq;
   if (nonfinite) *nonfinite = bad;

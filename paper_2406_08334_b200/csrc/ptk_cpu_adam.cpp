@@ -30,6 +30,51 @@ inline uint16_t f32_to_bf16(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+// The element loop, branch-free inside so it vectorises (IEEE vdivps /
+// vsqrtps keep it bit-exact with the GPU rule; no FMA contraction).
+template <bool kL2, bool kDecay, bool kOut>
+inline __attribute__((always_inline)) void update_run(const ptk_adam_scalars& s, float* __restrict__ pm,
+                                                       float* __restrict__ mm, float* __restrict__ vm,
+                                                       const uint16_t* __restrict__ gr,
+                                                       uint16_t* __restrict__ out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    float g = bf16_to_f32(gr[i]) * s.gscale;
+    float p = pm[i];
+    if (kL2) g = g + s.wd * p;
+    if (kDecay) p = p * s.decay;
+    float m = mm[i];
+    m = m + s.w1 * (g - m);
+    float v = vm[i];
+    v = v * s.b2 + s.w2 * (g * g);
+    const float d = std::sqrt(v) / s.bc2_sqrt + s.eps;
+    p = p + s.neg_step_size * (m / d);
+    pm[i] = p;
+    mm[i] = m;
+    vm[i] = v;
+    if (kOut) out[i] = f32_to_bf16(p);
+  }
+}
+
+// One block of the shard, compiled for AVX-512, AVX2 and baseline x86-64
+// (resolved once at load time), so the library runs on any host CPU.
+__attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
+    const ptk_adam_scalars& s, float* pm, float* mm, float* vm, const uint16_t* gr, uint16_t* out,
+    int64_t n) {
+  const bool l2 = s.wd != 0.0f, decay = s.adamw != 0, has_out = out != nullptr;
+  if (l2) {
+    if (has_out) update_run<true, false, true>(s, pm, mm, vm, gr, out, n);
+    else update_run<true, false, false>(s, pm, mm, vm, gr, out, n);
+  } else if (decay) {
+    if (has_out) update_run<false, true, true>(s, pm, mm, vm, gr, out, n);
+    else update_run<false, true, false>(s, pm, mm, vm, gr, out, n);
+  } else {
+    if (has_out) update_run<false, false, true>(s, pm, mm, vm, gr, out, n);
+    else update_run<false, false, false>(s, pm, mm, vm, gr, out, n);
+  }
+}
+
+constexpr int64_t kBlock = 1 << 16;
+
 }  // namespace
 
 extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
@@ -41,26 +86,22 @@ extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* ex
   if (cfg->step < 1) return ptk::fail(PTK_EINVAL, "ptk_cpu_adam: step must be >= 1");
   const ptk_adam_scalars s = ptk::derive_scalars(*cfg);
   const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  const bool stats = sumsq_out != nullptr || nonfinite_out != nullptr;
+  const int64_t blocks = (n + kBlock - 1) / kBlock;
   double sq = 0.0;
   int64_t bad = 0;
 #pragma omp parallel for num_threads(threads) schedule(static) reduction(+ : sq, bad)
-  for (int64_t i = 0; i < n; ++i) {
-    float g = bf16_to_f32(grad[i]) * s.gscale;
-    sq += static_cast<double>(g) * static_cast<double>(g);
-    bad += std::isfinite(g) ? 0 : 1;
-    float p = master[i];
-    if (s.wd != 0.0f) g = g + s.wd * p;
-    if (s.adamw) p = p * s.decay;
-    float m = exp_avg[i];
-    m = m + s.w1 * (g - m);
-    float v = exp_avg_sq[i];
-    v = v * s.b2 + s.w2 * (g * g);
-    const float d = std::sqrt(v) / s.bc2_sqrt + s.eps;
-    p = p + s.neg_step_size * (m / d);
-    master[i] = p;
-    exp_avg[i] = m;
-    exp_avg_sq[i] = v;
-    if (param_out) param_out[i] = f32_to_bf16(p);
+  for (int64_t b = 0; b < blocks; ++b) {
+    const int64_t lo = b * kBlock, len = std::min(kBlock, n - lo);
+    if (stats) {  // statistics of this block's scaled gradient (still in cache after)
+      for (int64_t i = lo; i < lo + len; ++i) {
+        const float g = bf16_to_f32(grad[i]) * s.gscale;
+        sq += static_cast<double>(g) * static_cast<double>(g);
+        bad += std::isfinite(g) ? 0 : 1;
+      }
+    }
+    update_block(s, master + lo, exp_avg + lo, exp_avg_sq + lo, grad + lo,
+                 param_out ? param_out + lo : nullptr, len);
   }
   if (sumsq_out) *sumsq_out = sq;
   if (nonfinite_out) *nonfinite_out = bad;
