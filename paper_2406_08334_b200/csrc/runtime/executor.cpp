@@ -397,7 +397,9 @@ class Runtime {
 
   // iteration state (mirrors the simulator)
   std::vector<Job> jobs_;
-  std::size_t next_ = 0;
+  std::size_t next_ = 0;         // oldest unfinished GPU job (the simulator's next_task)
+  std::size_t next_launch_ = 0;  // next GPU job to put on the compute stream
+  static constexpr std::size_t kRunAhead = 4;  // GPU jobs queued ahead (hides launch gaps)
   std::vector<Where> where_;
   std::vector<int> bwd_left_;
   std::vector<char> reduce_done_;
@@ -427,6 +429,7 @@ class Runtime {
 void Runtime::prepare_iteration() {
   jobs_.clear();
   next_ = 0;
+  next_launch_ = 0;
   log_.clear();
   mem_.clear();
   held_ = high_ = 0;
@@ -499,10 +502,15 @@ bool Runtime::issue_prefetch(std::int64_t t) {
     return true;
   }
   if (free_slot_ids_.empty()) {
-    const int pinned = next_ < jobs_.size() ? jobs_[next_].chunk : 0;
+    // never evict a chunk a queued or next-to-queue GPU job uses
+    const auto pinned = [&](int v) {
+      for (std::size_t k = next_; k <= next_launch_ && k < jobs_.size(); ++k)
+        if (jobs_[k].chunk == v) return true;
+      return false;
+    };
     int victim = 0, victim_use = -1;
     for (int v = cfg_.n_persist + 1; v <= nc_; ++v) {
-      if (where_[v] != Where::Here || v == pinned) continue;
+      if (where_[v] != Where::Here || pinned(v)) continue;
       const int use = next_use(v);
       if (use > victim_use) {
         victim_use = use;
@@ -643,10 +651,15 @@ bool Runtime::ready(const Job& j) const {
   return false;
 }
 
+// Queues the next GPU job if it is ready. Up to kRunAhead jobs sit on the
+// compute stream at once (stream order keeps them serial, as the simulator's
+// single GPU queue); readiness can only be lost by eviction, and queued jobs'
+// chunks are pinned against eviction.
 bool Runtime::start_gpu(std::int64_t t) {
-  if (gpu_busy_ || next_ >= jobs_.size()) return false;
-  const Job& j = jobs_[next_];
+  if (next_launch_ >= jobs_.size() || next_launch_ - next_ >= kRunAhead) return false;
+  const Job& j = jobs_[next_launch_];
   if (!ready(j)) return false;
+  ++next_launch_;
   enqueue_until(j.slot + 1);
   if (j.kind == Kind::Bwd || j.kind == Kind::Recompute) {
     in_backward_ = true;
@@ -699,8 +712,8 @@ bool Runtime::start_gpu(std::int64_t t) {
 
 void Runtime::finish_gpu(std::int64_t t) {
   const Job j = jobs_[next_];
-  gpu_busy_ = false;
   ++next_;
+  gpu_busy_ = next_ < next_launch_;
   gpu_end_ = t;
   const auto chunk_done = [&](int c) {
     if (--bwd_left_[c] != 0) return;
@@ -860,7 +873,7 @@ SimulationResult Runtime::iterate() {
         free_events_.push_back(p.end);
         break;
       }
-      std::this_thread::sleep_for(std::chrono::microseconds(5));
+      std::this_thread::yield();  // busy-poll: completions are usually microseconds apart
     }
   }
   free_events_.push_back(base_);

@@ -56,8 +56,9 @@ def test_chunked_training_matches_plain_torch(tmp_path, cuda_device):
     g = torch.Generator(device=cuda_device).manual_seed(0)
     ours, ref = [], []
     for step in range(6):
-        tok = torch.randint(0, shape.vocab, (4, shape.seq + 1), device=cuda_device, generator=g)
-        x, y = tok[:, :-1], tok[:, 1:]
+        # learnable synthetic data: the next token is the current one + 1
+        x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device, generator=g)
+        y = (x + 1) % shape.vocab
         ours.append(float(train_step(model, x, y, hyper)))
         loss = ChunkedGPT2.loss(twin, x, y)
         loss.backward()
