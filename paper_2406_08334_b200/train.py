@@ -28,6 +28,7 @@ from dataclasses import dataclass
 
 import torch
 import torch.nn.functional as F
+import torch.utils.checkpoint
 
 from .chunks import AdamHyper, ChunkSet
 
@@ -129,22 +130,83 @@ class ChunkedGPT2:
                 c.exp_avg.zero_()
                 c.exp_avg_sq.zero_()
 
+    def set_block_schedule(self, strategies: list[str]) -> None:
+        """Per-block activation policy from the planner's BlockSchedule
+        ("swap" | "checkpoint" | "none", proj/src/layout.cpp:218-249):
+        checkpoint = recompute the block in backward; swap = its saved
+        activations go to pinned host memory on a side stream after use in
+        forward and come back before its backward (parameters stay put)."""
+        if len(strategies) != self.shape.blocks:
+            raise ValueError("one strategy per block")
+        self.strategies = list(strategies)
+        self._swap = ActivationSwap({c.param.untyped_storage().data_ptr()
+                                     for c in self.chunks.chunks})
+
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         sh = self.shape
         b, s = tokens.shape
         x = F.embedding(tokens, self.params["wte"]) + self.params["wpe"][:s]
-        for blk in self.blocks:
-            y = F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"])
-            qkv = F.linear(y, blk["qkv_w"], blk["qkv_b"])
-            q, k, v = qkv.view(b, s, 3, sh.heads, sh.hidden // sh.heads).unbind(2)
-            a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
-                                               v.transpose(1, 2), is_causal=True)
-            x = x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"], blk["out_b"])
-            y = F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"])
-            y = F.gelu(F.linear(y, blk["up_w"], blk["up_b"]), approximate="tanh")
-            x = x + F.linear(y, blk["down_w"], blk["down_b"])
+        strategies = getattr(self, "strategies", None) or ["none"] * len(self.blocks)
+        for blk, strategy in zip(self.blocks, strategies):
+            if strategy == "checkpoint":
+                x = torch.utils.checkpoint.checkpoint(block_forward, sh, blk, x, use_reentrant=False)
+            elif strategy == "swap":
+                with torch.autograd.graph.saved_tensors_hooks(self._swap.pack, self._swap.unpack):
+                    x = block_forward(sh, blk, x)
+            else:
+                x = block_forward(sh, blk, x)
         logits = F.linear(x, self.params["wte"])  # tied lm_head
         return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
+
+
+def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor) -> torch.Tensor:
+    """One transformer block: the trace's attn_norm .. mlp_down operators."""
+    b, s, _ = x.shape
+    y = F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"])
+    qkv = F.linear(y, blk["qkv_w"], blk["qkv_b"])
+    q, k, v = qkv.view(b, s, 3, sh.heads, sh.hidden // sh.heads).unbind(2)
+    a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                       v.transpose(1, 2), is_causal=True)
+    x = x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"], blk["out_b"])
+    y = F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"])
+    y = F.gelu(F.linear(y, blk["up_w"], blk["up_b"]), approximate="tanh")
+    return x + F.linear(y, blk["down_w"], blk["down_b"])
+
+
+class ActivationSwap:
+    """saved_tensors_hooks for Swap blocks: each saved activation is copied to
+    pinned host memory on a side stream (swap-out overlapping the forward),
+    its device memory released to the allocator once that copy is done
+    (record_stream), and copied back on the side stream when backward needs
+    it (swap-in), the compute stream waiting only on that copy. Tensors that
+    live in the chunk buffers (parameters) are never swapped."""
+
+    def __init__(self, param_storages: set[int]):
+        self.params = param_storages
+        self.side = torch.cuda.Stream()
+
+    def pack(self, t: torch.Tensor):
+        if not t.is_cuda or t.untyped_storage().data_ptr() in self.params:
+            return ("keep", t)
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            host.copy_(t, non_blocking=True)
+        t.record_stream(self.side)
+        return ("swap", host, t.device)
+
+    def unpack(self, packed):
+        if packed[0] == "keep":
+            return packed[1]
+        _, host, device = packed
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            dev = host.to(device, non_blocking=True)
+        cur.wait_stream(self.side)
+        dev.record_stream(cur)
+        return dev
 
 
 def _stash_into(slot: torch.Tensor):
