@@ -428,19 +428,44 @@ def run_e2e(cs, hyper, args, world):
     from paper_2406_08334_b200 import _native as nat
     from paper_2406_08334_b200.chunks import stream_handle, vp
 
-    if world > 1:
-        return None  # the multi-rank e2e path also needs the AG/RS; single-rank only for now
     piece = args.e2e_piece
     comp = torch.cuda.current_stream()
     h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
-    host_g = [torch.empty(c.shard, dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
-    host_p = [torch.empty(c.shard, dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
+    # w = 1: the rank's shard is the chunk. w > 1: each rank hands in its
+    # full local gradient chunk and gets the full gathered parameter chunk
+    # back (what a ZeRO-3 caller's backward produces / forward consumes).
+    span = (lambda c: c.shard) if world == 1 else (lambda c: c.n_pad)
+    host_g = [torch.empty(span(c), dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
+    host_p = [torch.empty(span(c), dtype=torch.bfloat16, pin_memory=True) for c in cs.chunks]
     host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
     for hg, c in zip(host_g, cs.chunks):
-        hg.copy_(c.grad_shard().cpu())
+        hg.copy_((c.grad_shard() if world == 1 else c.grad).cpu())
     sc, sh, sd = stream_handle(comp), stream_handle(h2d), stream_handle(d2h)
 
+    def one_step_sharded():
+        cs.step_count += 1
+        cfg = hyper.config(cs.step_count, world)
+        nat.lib.ptk_stats_reset(vp(cs.stats), sc)
+        h2d.wait_stream(comp)
+        for c, hg, hp in zip(cs.chunks, host_g, host_p):
+            e_in, e_up = torch.cuda.Event(), torch.cuda.Event()
+            nat.lib.ptk_memcpy_h2d_async(vp(c.grad), ctypes.c_void_p(hg.data_ptr()), 2 * c.n_pad, sh)
+            e_in.record(h2d)
+            comp.wait_event(e_in)
+            nat.lib.ptk_chunk_reduce_scatter(cs.comm, vp(c.grad), c.shard, 0, sc)
+            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                                   vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                                   c.shard, vp(cs.stats), vp(cs.workspace), None, None, sc)
+            nat.lib.ptk_chunk_allgather(cs.comm, vp(c.param), c.shard, 0, sc)
+            e_up.record(comp)
+            d2h.wait_event(e_up)
+            nat.lib.ptk_memcpy_d2h_async(ctypes.c_void_p(hp.data_ptr()), vp(c.param), 2 * c.n_pad, sd)
+        comp.wait_stream(d2h)
+        nat.lib.ptk_memcpy_d2h_async(vp(host_stats), vp(cs.stats), 16, sc)
+
     def one_step():
+        if world > 1:
+            return one_step_sharded()
         cs.step_count += 1
         cfg = hyper.config(cs.step_count, world)
         nat.lib.ptk_stats_reset(vp(cs.stats), sc)
@@ -466,23 +491,29 @@ def run_e2e(cs, hyper, args, world):
         comp.wait_stream(d2h)
         nat.lib.ptk_memcpy_d2h_async(vp(host_stats), vp(cs.stats), 16, sc)
 
+    steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(max(1, args.warmup)):
         one_step()
     torch.cuda.synchronize()
+    barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(comp)
-    for _ in range(args.steps):
+    for _ in range(steps):
         one_step()
     t1.record(comp)
     torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1) / args.steps
-    h2d_bytes = sum(2 * c.shard for c in cs.chunks)
-    d2h_bytes = sum(2 * c.shard for c in cs.chunks) + 16
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1) / steps, world)
+    h2d_bytes = sum(2 * span(c) for c in cs.chunks)
+    d2h_bytes = sum(2 * span(c) for c in cs.chunks) + 16
     value = cs.algorithmic_hbm_bytes() * world / (ms * 1e-3) / 1e9
     return {"value": round(value, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
-            "path": "C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
-                    f"pinned host buffers, {piece}-element pieces on 3 streams"}
+            "steps": steps,
+            "path": ("C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
+                     f"pinned host buffers, {piece}-element pieces on 3 streams") if world == 1 else
+                    ("C-ABI per chunk: H2D local grad chunk -> ptk_chunk_reduce_scatter -> "
+                     "ptk_chunk_adam -> ptk_chunk_allgather -> D2H gathered params, 3 streams")}
 
 
 # ------------------------------------------------------------------ CPU arm --
@@ -561,6 +592,7 @@ def main():
                          "RS->Adam->AG kernel over NVLink peer memory")
     ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")

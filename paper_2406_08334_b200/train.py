@@ -159,18 +159,22 @@ class ChunkedGPT2:
         return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
 
 
-def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor) -> torch.Tensor:
-    """One transformer block: the trace's attn_norm .. mlp_down operators."""
+def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor, mark=None) -> torch.Tensor:
+    """One transformer block: the trace's attn_norm .. mlp_down operators.
+    `mark(k, out)` (profiler only) is called after operator k with its output."""
+    mark = mark or (lambda k, out: out)
     b, s, _ = x.shape
-    y = F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"])
-    qkv = F.linear(y, blk["qkv_w"], blk["qkv_b"])
+    y = mark(0, F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"]))
+    qkv = mark(1, F.linear(y, blk["qkv_w"], blk["qkv_b"]))
     q, k, v = qkv.view(b, s, 3, sh.heads, sh.hidden // sh.heads).unbind(2)
-    a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
-                                       v.transpose(1, 2), is_causal=True)
-    x = x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"], blk["out_b"])
-    y = F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"])
-    y = F.gelu(F.linear(y, blk["up_w"], blk["up_b"]), approximate="tanh")
-    return x + F.linear(y, blk["down_w"], blk["down_b"])
+    a = mark(2, F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                               v.transpose(1, 2), is_causal=True))
+    x = mark(3, x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"],
+                             blk["out_b"]))
+    y = mark(4, F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"]))
+    y = mark(5, F.linear(y, blk["up_w"], blk["up_b"]))
+    y = mark(6, F.gelu(y, approximate="tanh"))
+    return mark(7, x + F.linear(y, blk["down_w"], blk["down_b"]))
 
 
 class ActivationSwap:

@@ -118,6 +118,30 @@ def test_block_schedule_swap_checkpoint_is_exact(tmp_path, cuda_device, schedule
     assert torch.equal(runs[0][1], runs[1][1])
 
 
+def test_profiler_measures_a_loadable_trace(tmp_path, cuda_device):
+    """The profiler's measured trace has the synthesized trace's operators and
+    parameter bytes, positive measured times that add up to the measured
+    iteration, retained activations, and loads into the planner unchanged."""
+    import subprocess
+    from paper_2406_08334_b200.profiler import profile_trace
+    model, shape = _setup(tmp_path, cuda_device)
+    x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device)
+    measured = profile_trace(model, x, (x + 1) % shape.vocab, reps=2)
+    synth = json.load(open(tmp_path / "t.json"))
+    assert [o["name"] for o in measured["ops"]] == [o["name"] for o in synth["ops"]]
+    assert [o["param_bytes"] for o in measured["ops"]] == [o["param_bytes"] for o in synth["ops"]]
+    assert all(o["t_fwd"] > 0 for o in measured["ops"])
+    assert sum(o["t_bwd"] for o in measured["ops"]) > 0
+    assert sum(o["act_bytes"] for o in measured["ops"]) > 0
+    path = tmp_path / "measured.json"
+    path.write_text(json.dumps(measured))
+    memplan = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "build", "memplan")
+    out = subprocess.run([memplan, "pack", "--trace", str(path), "--grid", "2Mi"], check=True,
+                         capture_output=True, text=True).stdout
+    assert json.loads(out)["n_chunk"] == 3
+
+
 def _fresh(tmp_path, name):
     d = tmp_path / name
     d.mkdir(parents=True, exist_ok=True)
