@@ -153,6 +153,9 @@ int ptk_chunk_allgather(ptk_comm* comm, void* buf, int64_t shard_elems,
  * buf + rank*shard_elems holds the sum over ranks of that shard. */
 int ptk_chunk_reduce_scatter(ptk_comm* comm, void* buf, int64_t shard_elems,
                              int32_t dtype, void* stream);
+/* Sums a ptk_grad_stats_t (sumsq fp64, nonfinite u64) over all ranks, in
+ * place on the device (global gradient norm / overflow across the world). */
+int ptk_stats_allreduce(ptk_comm* comm, ptk_grad_stats_t* stats, void* stream);
 /* Device-side barrier over the communicator (an 1-element all-reduce). */
 int ptk_comm_barrier(ptk_comm* comm, void* stream);
 

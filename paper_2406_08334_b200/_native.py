@@ -75,6 +75,7 @@ _SIGNATURES = {
     "ptk_chunk_allgather": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "ptk_chunk_reduce_scatter": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "ptk_comm_barrier": (c_int32, [c_void_p, c_void_p]),
+    "ptk_stats_allreduce": (c_int32, [c_void_p, c_void_p, c_void_p]),
     "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8), POINTER(c_int64)]),
     "ptk_ipc_open_handle": (c_int32, [POINTER(c_uint8), POINTER(c_void_p)]),
     "ptk_ipc_close_handle": (c_int32, [c_void_p]),

@@ -204,14 +204,29 @@ class ChunkSet:
     def reset_stats(self, stream=None) -> None:
         nat.lib.ptk_stats_reset(vp(self.stats), stream_handle(stream))
 
-    def step(self, hyper: AdamHyper, stream=None, with_stats: bool = True) -> None:
-        """One optimizer step over every chunk: RS -> Adam -> AG."""
+    def step(self, hyper: AdamHyper, stream=None, with_stats: bool = True,
+             max_grad_norm: float = 0.0, skip_nonfinite: bool = False) -> None:
+        """One optimizer step over every chunk: RS -> Adam -> AG.
+
+        With `max_grad_norm > 0` or `skip_nonfinite`, the global statistics
+        of the scaled gradient are needed BEFORE any update: all chunks are
+        reduce-scattered, ptk_grad_stats sums squares / counts non-finite
+        elements of every owned shard (warp-shuffle + CTA reductions), the
+        partial statistics are all-reduced over the ranks, ptk_clip_coef
+        turns them into a device-side clip coefficient and skip flag, and
+        every chunk's fused Adam reads both from device memory (no host
+        synchronisation anywhere)."""
         self.step_count += 1
         cfg = hyper.config(self.step_count, self.world)
         s = stream_handle(stream)
         stats = vp(self.stats) if with_stats else ctypes.c_void_p(None)
-        if with_stats:
+        if with_stats or max_grad_norm > 0 or skip_nonfinite:
             nat.lib.ptk_stats_reset(vp(self.stats), s)
+        if max_grad_norm > 0 or skip_nonfinite:
+            if self.mode == "fused":
+                raise ValueError("clipping needs the global norm before the update: use mode='nccl'")
+            self._step_clipped(cfg, s, max_grad_norm, skip_nonfinite)
+            return
         if self.mode == "fused":
             self._step_fused(cfg, s, stats)
             return
@@ -221,6 +236,27 @@ class ChunkSet:
             nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
                                    vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
                                    c.shard, stats, vp(self.workspace), None, None, s)
+            if self.world > 1:
+                nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
+
+    def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
+        if not hasattr(self, "clip_coef"):
+            self.clip_coef = torch.ones(1, dtype=F32, device=self.device)
+            self.skip_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        for c in self.chunks:
+            if self.world > 1:
+                nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
+            nat.lib.ptk_grad_stats(vp(c.grad_shard()), c.shard, ctypes.c_float(cfg.grad_scale),
+                                   None, vp(self.stats), vp(self.workspace), s)
+        if self.world > 1:
+            nat.lib.ptk_stats_allreduce(self.comm, vp(self.stats), s)
+        nat.lib.ptk_clip_coef(vp(self.stats), max_grad_norm, vp(self.clip_coef),
+                              vp(self.skip_flag) if skip_nonfinite else None, s)
+        for c in self.chunks:
+            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq),
+                                   vp(c.grad_shard()), vp(c.param_shard()), c.shard, None, None,
+                                   vp(self.clip_coef), vp(self.skip_flag) if skip_nonfinite else None,
+                                   s)
             if self.world > 1:
                 nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
 

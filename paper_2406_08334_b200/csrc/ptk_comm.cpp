@@ -105,6 +105,18 @@ int ptk_chunk_reduce_scatter(ptk_comm* c, void* buf, int64_t shard_elems, int32_
   return PTK_OK;
 }
 
+int ptk_stats_allreduce(ptk_comm* c, ptk_grad_stats_t* stats, void* stream) {
+  if (!c || !stats) return ptk::fail(PTK_EINVAL, "ptk_stats_allreduce: null argument");
+  if (c->world == 1) return PTK_OK;
+  PTK_TRY_NCCL(ncclGroupStart());
+  PTK_TRY_NCCL(ncclAllReduce(&stats->sumsq, &stats->sumsq, 1, ncclFloat64, ncclSum, c->comm,
+                             ptk::as_stream(stream)));
+  PTK_TRY_NCCL(ncclAllReduce(&stats->nonfinite, &stats->nonfinite, 1, ncclUint64, ncclSum,
+                             c->comm, ptk::as_stream(stream)));
+  PTK_TRY_NCCL(ncclGroupEnd());
+  return PTK_OK;
+}
+
 int ptk_comm_barrier(ptk_comm* c, void* stream) {
   if (!c) return ptk::fail(PTK_EINVAL, "ptk_comm_barrier: null comm");
   if (c->world == 1) return PTK_OK;

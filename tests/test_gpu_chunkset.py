@@ -154,6 +154,56 @@ def test_full_size_layout_sampled_parity(cuda_device, workload):
     assert abs(sumsq - total_sq) <= 1e-6 * total_sq
 
 
+def test_global_norm_clipping_matches_oracle(cuda_device):
+    """max_grad_norm: global norm over all chunks -> device clip coefficient ->
+    every chunk's Adam reads it from device memory. Checked against the
+    oracle with the same coefficient (bit-exact state) and the coefficient
+    against the oracle's fp64 norm."""
+    nat, ch = _modules()
+    numels = [50_001, 70_003]
+    cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device)
+    cs.init_synthetic()
+    cs.fill_grads(0)
+    max_norm = 0.05
+    cs.step(ch.AdamHyper(), max_grad_norm=max_norm)
+    torch.cuda.synchronize()
+    coef = float(cs.clip_coef[0])
+    sq = 0.0
+    for ci, n in enumerate(numels):
+        g = ol.bf16_to_f32(ol.fill_bf16(n, ch.grad_seed(ci, 0, 0), ch.GRAD_SCALE))
+        sq += float(np.dot(g.astype(np.float64), g.astype(np.float64)))
+    want = min(1.0, max_norm / (np.sqrt(sq) + 1e-6))
+    assert want < 1.0 and abs(coef - want) <= 1e-6 * want
+    for ci, n in enumerate(numels):
+        c = cs.chunks[ci]
+        mst = ol.fill_f32(c.shard, ch.master_seed(ci), ch.MASTER_SCALE)
+        mst[n:] = 0
+        g = ol.fill_bf16(c.shard, ch.grad_seed(ci, 0, 0), ch.GRAD_SCALE)
+        g[n:] = 0
+        s = ol.scalars(step=1)
+        s.gscale = float(np.float32(s.gscale) * np.float32(coef))
+        m = np.zeros(c.shard, np.float32)
+        v = np.zeros(c.shard, np.float32)
+        out = np.zeros(c.shard, np.uint16)
+        ol.adam_step(s, mst, m, v, g, out)
+        np.testing.assert_array_equal(_bits(c.master), mst.view(np.uint32))
+        np.testing.assert_array_equal(_bf16_bits(c.param), out)
+
+
+def test_nonfinite_gradient_skips_the_whole_step(cuda_device):
+    nat, ch = _modules()
+    cs = ch.ChunkSet([4096, 8192], world=1, rank=0, device=cuda_device)
+    cs.init_synthetic()
+    cs.fill_grads(0)
+    cs.chunks[1].grad[100] = float("inf")
+    before = [c.master.clone() for c in cs.chunks]
+    cs.step(ch.AdamHyper(), skip_nonfinite=True)
+    torch.cuda.synchronize()
+    assert int(cs.skip_flag[0]) == 1
+    for b, c in zip(before, cs.chunks):
+        assert torch.equal(b, c.master)  # no chunk updated, not even the finite one
+
+
 def test_pinned_copies_round_trip(cuda_device):
     nat, ch = _modules()
     n = 1 << 20
