@@ -1,0 +1,236 @@
+"""Non-persistent chunks inside the training model: host-resident shards, a
+pool of device buffers, fetch-before-use and drain-after-backward — the
+chunk runtime's policy (csrc/runtime/executor.cpp, which restates
+proj/src/sim.cpp:275-451) driven by autograd instead of a trace.
+
+* storage: chunk c >= n_persist keeps its rank shard in pinned host memory
+  (fp32 master/m/v, bf16 params, bf16 grads); `n_buffer` device slots hold
+  gathered bf16 chunks (the reference's buffer = the working copy only);
+* fetch (`acquire`): wait for the chunk's previous host update, H2D of the
+  shard into its slot position on the h2d stream (+ NCCL all-gather, w > 1),
+  the compute stream waits on that event; one prefetch ahead (the next chunk
+  in forward, the previous one in backward);
+* eviction: the resident pool chunk whose next use (forward position c,
+  backward position 2N-c+1) is farthest, never the chunk being acquired or
+  in use; the h2d stream waits for all compute issued so far before it
+  overwrites the slot;
+* autograd: a chunk's parameters are outputs of `ChunkGather` (one node per
+  use in forward); tensors autograd saves that live in a slot are saved as
+  (chunk, offset, shape) and re-acquired on unpack, so a chunk evicted between
+  its forward and backward is fetched again (re-gather in backward);
+* drain: when the gradients of all uses of chunk c have arrived
+  (ChunkGather.backward), they are summed in a padded staging tensor,
+  reduce-scattered (w > 1), the shard goes D2H on the d2h stream and a worker
+  thread runs the host Adam (ptk_cpu_adam — bit-identical to the device rule)
+  producing the bf16 shard the next fetch uploads.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import torch
+
+from . import _native as nat
+from .chunks import AdamHyper, vp
+
+BF16 = torch.bfloat16
+
+
+def _sh(stream: torch.cuda.Stream) -> ctypes.c_void_p:
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class ChunkPool:
+    def __init__(self, numels: list[int], first: int, n_buffer: int, world: int = 1, rank: int = 0,
+                 comm=None, device=None):
+        if n_buffer < 1:
+            raise ValueError("non-persistent chunks need at least one buffer")
+        self.device = torch.device(device or "cuda")
+        self.first, self.world, self.rank, self.comm = first, world, rank, comm
+        self.n_total = len(numels)
+        self.numel = {c: numels[c] for c in range(first, len(numels))}
+        self.shard = {c: nat.shard_elems(n, world) for c, n in self.numel.items()}
+        n_pad_max = max(self.shard[c] * world for c in self.numel)
+        pin = dict(device="cpu", pin_memory=True)
+        self.h_param = {c: torch.zeros(s, dtype=BF16, **pin) for c, s in self.shard.items()}
+        self.h_grad = {c: torch.zeros(s, dtype=BF16, **pin) for c, s in self.shard.items()}
+        self.h_master = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
+        self.h_m = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
+        self.h_v = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
+        self.slots = [torch.zeros(n_pad_max, dtype=BF16, device=self.device)
+                      for _ in range(n_buffer)]
+        self.device_bytes = 2 * n_pad_max * n_buffer
+        self.host_bytes = sum(16 * s for s in self.shard.values())
+        self.slot_of: dict[int, int] = {}
+        self.free = list(range(n_buffer - 1, -1, -1))
+        self.ready: dict[int, torch.cuda.Event] = {}
+        self.h2d, self.d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
+        self.worker = ThreadPoolExecutor(max_workers=1)
+        self.updates: dict[int, object] = {}   # chunk -> Future of its host Adam
+        self.position = 0
+        self.pending_uses: dict[int, int] = {}
+        self.partial: dict[int, torch.Tensor] = {}
+        self.hyper = AdamHyper()
+        self.step = 0
+        self.counters = {"fetch": 0, "evict": 0, "h2d_bytes": 0, "d2h_bytes": 0}
+        self._lock = threading.RLock()
+        self._slot_ptr = {t.untyped_storage().data_ptr(): k for k, t in enumerate(self.slots)}
+
+    # ------------------------------------------------------------ storage --
+    def load_initial(self, c: int, full_chunk: torch.Tensor) -> None:
+        """Initial bf16 parameters of chunk c (the gathered chunk, on device)."""
+        s, lo = self.shard[c], self.rank * self.shard[c]
+        part = torch.zeros(s, dtype=BF16, device=self.device)
+        n = max(0, min(s, full_chunk.numel() - lo))
+        part[:n] = full_chunk[lo:lo + n]
+        self.h_param[c].copy_(part.cpu())
+        self.h_master[c].copy_(part.float().cpu())
+        self.h_m[c].zero_()
+        self.h_v[c].zero_()
+
+    # -------------------------------------------------------------- policy --
+    def _next_use(self, c: int) -> int:
+        fwd, bwd = c + 1, 2 * self.n_total - c
+        if fwd >= self.position:
+            return fwd
+        if bwd >= self.position:
+            return bwd
+        return 1 << 30
+
+    def _fetch(self, c: int, keep: int) -> None:
+        """Issue the fetch of chunk c (host update -> H2D shard -> all-gather)."""
+        if c in self.slot_of:
+            return
+        fut = self.updates.pop(c, None)
+        if fut is not None:
+            fut.result()  # the previous step's host Adam of this chunk
+        if self.free:
+            k = self.free.pop()
+        else:
+            victims = [(self._next_use(v), v) for v in self.slot_of if v not in (c, keep)]
+            if not victims:
+                raise RuntimeError("chunk pool exhausted: every buffer is in use")
+            _, v = max(victims)
+            k = self.slot_of.pop(v)
+            self.ready.pop(v, None)
+            self.counters["evict"] += 1
+        self.slot_of[c] = k
+        # the slot may still be read by compute already issued (evicted chunk)
+        self.h2d.wait_stream(torch.cuda.current_stream(self.device))
+        s = self.shard[c]
+        dst = self.slots[k][self.rank * s:(self.rank + 1) * s]
+        nat.lib.ptk_memcpy_h2d_async(vp(dst), vp(self.h_param[c]), 2 * s, _sh(self.h2d))
+        self.counters["h2d_bytes"] += 2 * s
+        if self.world > 1:
+            nat.lib.ptk_chunk_allgather(self.comm, vp(self.slots[k]), s, 0, _sh(self.h2d))
+        ev = torch.cuda.Event()
+        ev.record(self.h2d)
+        self.ready[c] = ev
+        self.counters["fetch"] += 1
+
+    def acquire(self, c: int, position: int, prefetch: int | None = None) -> torch.Tensor:
+        """Make chunk c resident for the compute stream; returns its gathered
+        bf16 buffer (n_pad elements) and starts the prefetch of `prefetch`."""
+        with self._lock:
+            self.position = position
+            self._fetch(c, c)
+            torch.cuda.current_stream(self.device).wait_event(self.ready[c])
+            view = self.slots[self.slot_of[c]][: self.shard[c] * self.world]
+            if prefetch is not None and prefetch in self.numel and prefetch not in self.slot_of:
+                if self.free or len(self.slot_of) > 1:
+                    self._fetch(prefetch, c)
+            return view
+
+    # --------------------------------------------------------------- drain --
+    def begin_step(self, step: int, hyper: AdamHyper, uses: dict[int, int]) -> None:
+        self.step, self.hyper = step, hyper
+        self.pending_uses = dict(uses)
+        self.partial.clear()
+
+    def add_grad(self, c: int, flat: torch.Tensor) -> None:
+        """Gradient of one use of chunk c (flat bf16, numel[c] elements)."""
+        with self._lock:
+            if c in self.partial:
+                self.partial[c] += flat
+            else:
+                self.partial[c] = flat
+            self.pending_uses[c] -= 1
+            if self.pending_uses[c] == 0:
+                self._drain(c, self.partial.pop(c))
+
+    def _drain(self, c: int, grad: torch.Tensor) -> None:
+        s = self.shard[c]
+        cur = torch.cuda.current_stream(self.device)
+        staged = torch.zeros(s * self.world, dtype=BF16, device=self.device)
+        staged[: grad.numel()] = grad
+        if self.world > 1:
+            nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
+        self.d2h.wait_stream(cur)
+        nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c]), vp(staged[self.rank * s:]), 2 * s,
+                                     _sh(self.d2h))
+        staged.record_stream(self.d2h)
+        self.counters["d2h_bytes"] += 2 * s
+        done = torch.cuda.Event()
+        done.record(self.d2h)
+        cfg = self.hyper.config(self.step, self.world)
+        # the device copy is stale once the host update runs: release the slot
+        if c in self.slot_of:
+            self.free.append(self.slot_of.pop(c))
+            self.ready.pop(c, None)
+        self.updates[c] = self.worker.submit(self._host_adam, c, done, cfg)
+
+    def _host_adam(self, c: int, d2h_done: torch.cuda.Event, cfg) -> None:
+        d2h_done.synchronize()
+        nat.lib.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c]), vp(self.h_m[c]),
+                             vp(self.h_v[c]), vp(self.h_grad[c]), vp(self.h_param[c]),
+                             self.shard[c], 0, None, None)
+
+    def finish_step(self) -> None:
+        for fut in list(self.updates.values()):
+            fut.result()
+
+    # ------------------------------------------------- saved-tensor hooks --
+    def pack(self, t: torch.Tensor):
+        k = self._slot_ptr.get(t.untyped_storage().data_ptr())
+        if k is None:
+            return ("t", t)
+        with self._lock:
+            c = next(ch for ch, kk in self.slot_of.items() if kk == k)
+        return ("ref", c, t.storage_offset(), tuple(t.shape), tuple(t.stride()))
+
+    def unpack(self, packed):
+        if packed[0] == "t":
+            return packed[1]
+        _, c, off, shape, stride = packed
+        buf = self.acquire(c, 2 * self.n_total - c, prefetch=c - 1)
+        return torch.as_strided(buf, shape, stride, off)
+
+
+class ChunkGather(torch.autograd.Function):
+    """Forward: the parameters of chunk c as views of its gathered buffer.
+    Backward: hands this use's gradients of the chunk to the pool, which
+    drains the chunk once all uses have reported."""
+
+    @staticmethod
+    def forward(ctx, anchor, pool, c, specs, position, prefetch):
+        buf = pool.acquire(c, position, prefetch)
+        ctx.pool, ctx.c, ctx.specs = pool, c, specs
+        outs = []
+        for lo, shape in specs:
+            n = 1
+            for d in shape:
+                n *= d
+            outs.append(buf[lo:lo + n].view(shape))
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *grads):
+        pool, c = ctx.pool, ctx.c
+        flat = torch.zeros(pool.numel[c], dtype=BF16, device=pool.device)
+        for (lo, shape), g in zip(ctx.specs, grads):
+            if g is not None:
+                flat[lo:lo + g.numel()] = g.reshape(-1)
+        pool.add_grad(c, flat)
+        return (None,) * 6

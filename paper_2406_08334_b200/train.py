@@ -72,9 +72,13 @@ def op_param_shapes(shape: GPT2Shape) -> list[tuple[str, list[tuple[str, tuple[i
 class ChunkedGPT2:
     """GPT-2 whose parameters are views into a ChunkSet's gathered buffers."""
 
-    def __init__(self, shape: GPT2Shape, layout: dict, chunks: ChunkSet, trace_ops: list[dict]):
+    def __init__(self, shape: GPT2Shape, layout: dict, chunks: ChunkSet, trace_ops: list[dict],
+                 pool=None):
+        """`chunks` holds the persistent chunks (all of them without a pool);
+        `pool` (offload.ChunkPool) the non-persistent chunks pool.first.."""
         self.shape = shape
         self.chunks = chunks
+        self.pool = pool
         specs = op_param_shapes(shape)
         if len(specs) != len(trace_ops):
             raise ValueError(f"model has {len(specs)} ops, trace has {len(trace_ops)}")
@@ -87,24 +91,45 @@ class ChunkedGPT2:
         self.params: dict[str, torch.Tensor] = {}
         self.blocks: list[dict[str, torch.Tensor]] = [dict() for _ in range(shape.blocks)]
         self._hooks = []
+        # non-persistent chunks: parameter specs for ChunkGather, where each
+        # param goes (None = top level, else block id), and init staging
+        first_pooled = pool.first if pool is not None else len(layout["chunks"])
+        self.pool_specs: dict[int, list] = {}
+        self.pool_keys: dict[int, list] = {}
+        self._init_buf: dict[int, torch.Tensor] = {}
+        self.block_chunk = [None] * shape.blocks
         for i, ((name, plist), top) in enumerate(zip(specs, trace_ops)):
             assert top["name"] == name, (top["name"], name)
             n_el = sum(math.prod(s) for _, s in plist)
             assert 2 * n_el == top["param_bytes"], (name, 2 * n_el, top["param_bytes"])
             ci = chunk_of[i]
-            cs = chunks.chunks[ci]
+            where = int(name.split(".")[1]) if "." in name else None
+            if where is not None:
+                self.block_chunk[where] = ci
             for pname, pshape in plist:
                 numel = math.prod(pshape)
                 lo = offset[ci]
-                p = cs.param[lo:lo + numel].view(pshape)
-                p.requires_grad_(True)
-                g = cs.grad[lo:lo + numel].view(pshape)
-                self._hooks.append(p.register_post_accumulate_grad_hook(_stash_into(g)))
                 offset[ci] += numel
-                if "." in name:
-                    self.blocks[int(name.split(".")[1])][pname] = p
+                if ci < first_pooled:
+                    cs = chunks.chunks[ci]
+                    p = cs.param[lo:lo + numel].view(pshape)
+                    p.requires_grad_(True)
+                    g = cs.grad[lo:lo + numel].view(pshape)
+                    self._hooks.append(p.register_post_accumulate_grad_hook(_stash_into(g)))
+                else:
+                    buf = self._init_buf.setdefault(
+                        ci, torch.zeros(pool.shard[ci] * pool.world, dtype=BF16,
+                                        device=pool.device))
+                    p = buf[lo:lo + numel].view(pshape)  # init-time stand-in only
+                    self.pool_specs.setdefault(ci, []).append((lo, pshape))
+                    self.pool_keys.setdefault(ci, []).append((where, pname))
+                if where is not None:
+                    self.blocks[where][pname] = p
                 else:
                     self.params[pname] = p
+        self.wte_chunk = chunk_of[0]
+        self.anchors = {c: torch.zeros((), device=pool.device, requires_grad=True)
+                        for c in self.pool_specs} if pool is not None else {}
         for ci, c in enumerate(layout["chunks"]):
             assert 2 * offset[ci] == c["used_bytes"], "chunk payload mismatch"
 
@@ -129,6 +154,48 @@ class ChunkedGPT2:
                 c.master.copy_(c.param_shard().float())
                 c.exp_avg.zero_()
                 c.exp_avg_sq.zero_()
+            for ci, buf in self._init_buf.items():  # non-persistent: to the host shards
+                self.pool.load_initial(ci, buf)
+                for where, pname in self.pool_keys[ci]:  # drop the init stand-ins
+                    (self.params if where is None else self.blocks[where])[pname] = None
+        self._init_buf.clear()
+
+    def pool_uses(self) -> dict[int, int]:
+        """ChunkGather nodes per non-persistent chunk in one forward (the tied
+        embedding's chunk is gathered again for the head)."""
+        uses = {c: 1 for c in self.pool_specs}
+        if self.wte_chunk in uses:
+            uses[self.wte_chunk] += 1
+        return uses
+
+    def _loss_pooled(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        from .offload import ChunkGather
+        sh, pool = self.shape, self.pool
+        params = dict(self.params)
+        blocks = [dict(b) for b in self.blocks]
+        done: set[int] = set()
+
+        def gather(c, position, prefetch):
+            outs = ChunkGather.apply(self.anchors[c], pool, c, self.pool_specs[c], position,
+                                     prefetch)
+            for (where, pname), t in zip(self.pool_keys[c], outs):
+                (params if where is None else blocks[where])[pname] = t
+
+        def ensure(c):  # forward reaches chunk c: gather it, prefetch c+1
+            if c in self.pool_specs and c not in done:
+                gather(c, c + 1, c + 1)
+                done.add(c)
+
+        b, s = tokens.shape
+        ensure(self.wte_chunk)
+        x = F.embedding(tokens, params["wte"]) + params["wpe"][:s]
+        for blk_id in range(sh.blocks):
+            ensure(self.block_chunk[blk_id])
+            x = block_forward(sh, blocks[blk_id], x)
+        if self.wte_chunk in self.pool_specs:  # tied head: second use of chunk 0
+            gather(self.wte_chunk, pool.n_total, None)
+        logits = F.linear(x, params["wte"])
+        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
 
     def set_block_schedule(self, strategies: list[str]) -> None:
         """Per-block activation policy from the planner's BlockSchedule
@@ -143,6 +210,12 @@ class ChunkedGPT2:
                                      for c in self.chunks.chunks})
 
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        pool = getattr(self, "pool", None)
+        if pool is not None:
+            if any(st != "none" for st in (getattr(self, "strategies", None) or [])):
+                raise NotImplementedError("swap/checkpoint blocks with non-persistent chunks")
+            with torch.autograd.graph.saved_tensors_hooks(pool.pack, pool.unpack):
+                return self._loss_pooled(tokens, targets)
         sh = self.shape
         b, s = tokens.shape
         x = F.embedding(tokens, self.params["wte"]) + self.params["wpe"][:s]
@@ -224,7 +297,10 @@ def train_step(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
                hyper: AdamHyper) -> torch.Tensor:
     """One iteration; returns the (device) loss. Gradient slots of the chunk
     buffers are fully overwritten by the hooks each step (padding stays 0)."""
+    pool = getattr(model, "pool", None)
+    if pool is not None:
+        pool.begin_step(model.chunks.step_count + 1, hyper, model.pool_uses())
     loss = model.loss(tokens, targets)
     loss.backward()
-    model.chunks.step(hyper)
+    model.chunks.step(hyper)  # persistent chunks; pooled chunks drained during backward
     return loss.detach()
