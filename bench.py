@@ -241,9 +241,13 @@ def run_gpu(args):
         cs.close_ipc_peers()
     del cs
     torch.cuda.empty_cache()
-    train = None
+    train = train_offload = None
     if args.train_steps > 0 and args.workload == "cfg2":
         train = run_train(args, world, rank, dev, comm)
+        if args.offload_persist >= 0:
+            train_offload = run_train(args, world, rank, dev, comm,
+                                      n_persist=args.offload_persist,
+                                      n_buffer=args.offload_buffers)
     copy_peak = live_copy_peak()
 
     result = None
@@ -281,6 +285,7 @@ def run_gpu(args):
                                                      1e9 / copy_peak, 4)),
             "e2e": e2e,
             "train": train,
+            "train_offload": train_offload,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "grad_stats": {"sumsq": sumsq, "nonfinite": nonfinite},
@@ -371,22 +376,29 @@ def live_copy_peak():
     return round(2 * 2 * (1 << 30) / (best * 1e-3) / 1e9, 1)
 
 
-def run_train(args, world, rank, dev, comm):
+def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     """tokens/s of a full training iteration of the cfg2 model (GPT-2 1.5B,
     b8, seq 1024) whose parameters live in the planner's chunk buffers:
     forward + backward in PyTorch (bf16 GEMMs / SDPA), then the chunk step
-    (RS -> fused Adam -> AG) through the C-ABI. Random-init weights, synthetic
-    uniform tokens; CUDA-event time over the timed iterations, max over ranks."""
+    (RS -> fused Adam -> AG) through the C-ABI. With n_persist < n_chunk the
+    remaining chunks are non-persistent: pinned host shards fetched into
+    n_buffer device slots, drained to the host Adam during backward (the
+    iteration's time includes the last host update). Random-init weights,
+    synthetic tokens; CUDA-event time over the timed iterations, max over ranks."""
     import torch
     from paper_2406_08334_b200 import planner
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
     from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
     trace = planner.trace_for("gpt2-1.5b_b8")
     layout = planner.layout_for("gpt2-1.5b_b8")
     numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
-    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    np_ = len(numels) if n_persist is None else n_persist
+    cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev)
+            if np_ < len(numels) else None)
     shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
-    model = ChunkedGPT2(shape, layout, cs, trace["ops"])
+    model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(seed=0)
     batch = int(trace["meta"]["batch_size"])
     n_iter = args.warmup + args.train_steps
@@ -405,19 +417,29 @@ def run_train(args, world, rank, dev, comm):
     t0.record(stream)
     for i in range(args.warmup, n_iter):
         losses.append(train_step(model, tokens[i], targets[i], hyper))
+    if pool is not None:
+        pool.finish_step()  # the last host updates belong to the timed iterations
     t1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     ms = max_over_ranks(t0.elapsed_time(t1) / args.train_steps, world)
     loss_vals = [float(x) for x in losses]
-    del model, cs
+    out = {"tokens_per_s": round(batch * shape.seq * world / (ms * 1e-3), 1),
+           "ms_per_iter": round(ms, 3), "iters": args.train_steps,
+           "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, no final LN as in the trace), "
+                    f"b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
+           "plan": {"n_chunk": len(numels), "n_persist": np_, "n_buffer": n_buffer if pool else 0},
+           "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
+           "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
+    if pool is not None:
+        out["offload"] = {"pinned_host_GB": round(pool.host_bytes / 1e9, 3),
+                          "buffer_GB": round(pool.device_bytes / 1e9, 3),
+                          "fetches": pool.counters["fetch"], "evictions": pool.counters["evict"],
+                          "h2d_GB": round(pool.counters["h2d_bytes"] / 1e9, 2),
+                          "d2h_GB": round(pool.counters["d2h_bytes"] / 1e9, 2)}
+    del model, cs, pool
     torch.cuda.empty_cache()
-    return {"tokens_per_s": round(batch * shape.seq * world / (ms * 1e-3), 1),
-            "ms_per_iter": round(ms, 3), "iters": args.train_steps,
-            "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, no final LN as in the trace), "
-                     f"b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
-            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
-            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
+    return out
 
 
 def run_e2e(cs, hyper, args, world):
@@ -594,6 +616,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--offload-persist", type=int, default=1,
+                    help="also time training with chunks >= this index non-persistent "
+                         "(pinned host + host Adam); -1 = skip")
+    ap.add_argument("--offload-buffers", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
