@@ -160,13 +160,26 @@ class ChunkedGPT2:
                     (self.params if where is None else self.blocks[where])[pname] = None
         self._init_buf.clear()
 
+    def _strategies(self) -> list[str]:
+        return getattr(self, "strategies", None) or ["none"] * self.shape.blocks
+
     def pool_uses(self) -> dict[int, int]:
-        """ChunkGather nodes per non-persistent chunk in one forward (the tied
-        embedding's chunk is gathered again for the head)."""
-        uses = {c: 1 for c in self.pool_specs}
+        """ChunkGather nodes per non-persistent chunk in one forward: one
+        shared by the chunk's plain operators, one per checkpointed block (its
+        gather lives inside the recomputable function), and one more for the
+        tied embedding's chunk at the head."""
+        strategies = self._strategies()
+        uses = {c: 0 for c in self.pool_specs}
+        plain = {self.wte_chunk} | {self.block_chunk[b] for b, st in enumerate(strategies)
+                                    if st != "checkpoint"}
+        for c in uses:
+            uses[c] += 1 if c in plain else 0
+        for b, st in enumerate(strategies):
+            if st == "checkpoint" and self.block_chunk[b] in uses:
+                uses[self.block_chunk[b]] += 1
         if self.wte_chunk in uses:
             uses[self.wte_chunk] += 1
-        return uses
+        return {c: n for c, n in uses.items() if n > 0}
 
     def _loss_pooled(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         from .offload import ChunkGather
@@ -175,25 +188,44 @@ class ChunkedGPT2:
         blocks = [dict(b) for b in self.blocks]
         done: set[int] = set()
 
-        def gather(c, position, prefetch):
+        def gather_into(c, position, prefetch, p_dict, b_list):
             outs = ChunkGather.apply(self.anchors[c], pool, c, self.pool_specs[c], position,
                                      prefetch)
             for (where, pname), t in zip(self.pool_keys[c], outs):
-                (params if where is None else blocks[where])[pname] = t
+                (p_dict if where is None else b_list[where])[pname] = t
 
         def ensure(c):  # forward reaches chunk c: gather it, prefetch c+1
             if c in self.pool_specs and c not in done:
-                gather(c, c + 1, c + 1)
+                gather_into(c, c + 1, c + 1, params, blocks)
                 done.add(c)
+
+        def checkpointed(blk_id):
+            c = self.block_chunk[blk_id]
+
+            def fn(x):
+                # the gather is part of the recomputed function: the recompute
+                # in backward re-acquires the chunk (it may have been evicted)
+                local = [dict(b) for b in blocks]
+                if c in self.pool_specs:
+                    gather_into(c, c + 1, c + 1, {}, local)
+                return block_forward(sh, local[blk_id], x)
+            return fn
 
         b, s = tokens.shape
         ensure(self.wte_chunk)
         x = F.embedding(tokens, params["wte"]) + params["wpe"][:s]
-        for blk_id in range(sh.blocks):
+        for blk_id, strategy in enumerate(self._strategies()):
+            if strategy == "checkpoint":
+                x = torch.utils.checkpoint.checkpoint(checkpointed(blk_id), x, use_reentrant=False)
+                continue
             ensure(self.block_chunk[blk_id])
-            x = block_forward(sh, blocks[blk_id], x)
-        if self.wte_chunk in self.pool_specs:  # tied head: second use of chunk 0
-            gather(self.wte_chunk, pool.n_total, None)
+            if strategy == "swap":
+                with torch.autograd.graph.saved_tensors_hooks(self._swap.pack, self._swap.unpack):
+                    x = block_forward(sh, blocks[blk_id], x)
+            else:
+                x = block_forward(sh, blocks[blk_id], x)
+        if self.wte_chunk in self.pool_specs:  # tied head: another use of chunk 0
+            gather_into(self.wte_chunk, pool.n_total, None, params, blocks)
         logits = F.linear(x, params["wte"])
         return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
 
@@ -207,13 +239,11 @@ class ChunkedGPT2:
             raise ValueError("one strategy per block")
         self.strategies = list(strategies)
         self._swap = ActivationSwap({c.param.untyped_storage().data_ptr()
-                                     for c in self.chunks.chunks})
+                                     for c in self.chunks.chunks}, getattr(self, "pool", None))
 
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         pool = getattr(self, "pool", None)
         if pool is not None:
-            if any(st != "none" for st in (getattr(self, "strategies", None) or [])):
-                raise NotImplementedError("swap/checkpoint blocks with non-persistent chunks")
             with torch.autograd.graph.saved_tensors_hooks(pool.pack, pool.unpack):
                 return self._loss_pooled(tokens, targets)
         sh = self.shape
@@ -256,13 +286,17 @@ class ActivationSwap:
     its device memory released to the allocator once that copy is done
     (record_stream), and copied back on the side stream when backward needs
     it (swap-in), the compute stream waiting only on that copy. Tensors that
-    live in the chunk buffers (parameters) are never swapped."""
+    live in the chunk buffers (parameters) are never swapped; parameters of
+    non-persistent chunks (pool slots) are handed to the pool's own hooks."""
 
-    def __init__(self, param_storages: set[int]):
+    def __init__(self, param_storages: set[int], pool=None):
         self.params = param_storages
+        self.pool = pool
         self.side = torch.cuda.Stream()
 
     def pack(self, t: torch.Tensor):
+        if self.pool is not None and t.untyped_storage().data_ptr() in self.pool._slot_ptr:
+            return ("pool", self.pool.pack(t))
         if not t.is_cuda or t.untyped_storage().data_ptr() in self.params:
             return ("keep", t)
         cur = torch.cuda.current_stream()
@@ -276,6 +310,8 @@ class ActivationSwap:
     def unpack(self, packed):
         if packed[0] == "keep":
             return packed[1]
+        if packed[0] == "pool":
+            return self.pool.unpack(packed[1])
         _, host, device = packed
         cur = torch.cuda.current_stream()
         self.side.wait_stream(cur)

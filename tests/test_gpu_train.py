@@ -118,8 +118,11 @@ def test_block_schedule_swap_checkpoint_is_exact(tmp_path, cuda_device, schedule
     assert torch.equal(runs[0][1], runs[1][1])
 
 
-@pytest.mark.parametrize("n_persist,n_buffer", [(1, 1), (0, 2), (1, 2)])
-def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_persist, n_buffer):
+@pytest.mark.parametrize("n_persist,n_buffer,schedule", [
+    (1, 1, None), (0, 2, None), (1, 2, None),
+    (0, 1, ["checkpoint", "swap"]), (1, 1, ["swap", "checkpoint"]), (0, 2, ["checkpoint", "checkpoint"])])
+def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_persist, n_buffer,
+                                                     schedule):
     """ZeRO-offload inside the training model: non-persistent chunks live in
     pinned host memory, are fetched into n_buffer device slots before use
     (re-gathered in backward when evicted), their gradients are offloaded and
@@ -131,8 +134,8 @@ def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_pe
     from paper_2406_08334_b200.offload import ChunkPool
     from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
 
-    def run(np_, nb):
-        d = _fresh(tmp_path, f"np{np_}nb{nb}")
+    def run(np_, nb, sched=None):
+        d = _fresh(tmp_path, f"np{np_}nb{nb}{sched}")
         spec = d / "spec.json"
         spec.write_text(json.dumps({"hidden_size": 256, "n_blocks": 2, "n_heads": 4,
                                     "vocab_size": 1000, "seq_len": 128}))
@@ -145,6 +148,8 @@ def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_pe
         shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
         model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
         model.init_weights(seed=0)
+        if sched:
+            model.set_block_schedule(sched)
         g = torch.Generator(device=cuda_device).manual_seed(0)
         losses = []
         for _ in range(4):
@@ -162,7 +167,7 @@ def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_pe
         return losses, [m[:n] for m, n in zip(masters, numels)], counters
 
     ref_losses, ref_masters, _ = run(3, 0)
-    losses, masters, counters = run(n_persist, n_buffer)
+    losses, masters, counters = run(n_persist, n_buffer, schedule)
     assert losses == ref_losses
     for a, b in zip(masters, ref_masters):
         assert torch.equal(a, b)
