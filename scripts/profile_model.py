@@ -78,8 +78,65 @@ def main():
            "trace_act_bytes": sum(o["act_bytes"] for o in measured["ops"]),
            "m_fwd": measured["m_fwd"], "measured_profile": hw,
            "tokens_per_s_real": 8 * 1024 / real}
-    print(json.dumps(row, indent=1))
-    json.dump(row, open(os.path.join(OUT, "profile_model.json"), "w"), indent=1)
+    # 5. a memory-constrained plan (the search must offload / swap / checkpoint),
+    #    trained for real with exactly that plan, vs the cost model's estimate
+    rows = [row]
+    for budget in (40e9, 30e9):
+        cplan = json.loads(subprocess.run(
+            [MEMPLAN, "plan", "--trace", tpath, "--hw", prof, "--gpu-mem", str(int(budget))],
+            check=True, capture_output=True, text=True).stdout)
+        cfg = cplan["config"]
+        real_c, info = train_with_plan(cfg, cplan["strategies"], x, y)
+        rows.append({"gpu_mem_budget": budget, "plan": cfg,
+                     "strategies": "".join(s[0] for s in cplan["strategies"]),
+                     "cost_model_t_iter_s": cplan["estimate"]["t_iter"],
+                     "cost_model_m_peak": cplan["estimate"]["m_peak"],
+                     "real_train_step_s": real_c,
+                     "rel_err": abs(real_c - cplan["estimate"]["t_iter"]) / real_c,
+                     "tokens_per_s_real": 8 * 1024 / real_c, **info})
+    print(json.dumps(rows, indent=1))
+    json.dump(rows, open(os.path.join(OUT, "profile_model.json"), "w"), indent=1)
+
+
+def train_with_plan(cfg, strategies, x, y, iters=5):
+    """Train the cfg2 model with a planner config: first n_persist chunks on
+    the device, the rest pooled in n_buffer slots, the block schedule."""
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    dev = x.device
+    trace = planner.trace_for("gpt2-1.5b_b8")
+    layout = planner.layout_for("gpt2-1.5b_b8")
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    np_ = cfg["n_persist"]
+    cs = ChunkSet(numels[:np_], device=dev)
+    pool = ChunkPool(numels, np_, cfg["n_buffer"], device=dev) if np_ < len(numels) else None
+    shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
+    model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
+    model.init_weights(0)
+    model.set_block_schedule(strategies)
+    hyper = AdamHyper(lr=1e-4)
+    torch.cuda.reset_peak_memory_stats()
+    for _ in range(2):
+        train_step(model, x, y, hyper)
+    if pool is not None:
+        pool.finish_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        train_step(model, x, y, hyper)
+    if pool is not None:
+        pool.finish_step()
+    e1.record()
+    torch.cuda.synchronize()
+    info = {"device_peak_allocated_GB": torch.cuda.max_memory_allocated() / 1e9}
+    if pool is not None:
+        info["pool"] = dict(pool.counters)
+    del model, cs, pool
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / iters * 1e-3, info
 
 
 if __name__ == "__main__":
