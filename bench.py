@@ -397,7 +397,7 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode="nccl", comm=comm)
     pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev)
             if np_ < len(numels) else None)
-    shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
+    shape = GPT2Shape.from_trace(trace)
     model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(seed=0)
     batch = int(trace["meta"]["batch_size"])

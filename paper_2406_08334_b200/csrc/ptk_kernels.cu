@@ -321,6 +321,31 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// Variants with an L2 eviction-priority hint (createpolicy evict_first): the
+// chunk bytes are touched once per step, so they need not compete for L2.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint32_t bytes,
+                                               uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::
+                   "l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src)), "r"(bytes)
@@ -346,7 +371,7 @@ struct TmaStage {
   uint16_t param[kTile];
 };
 
-template <int kTile, int kStages, int kThr, bool kStats>
+template <int kTile, int kStages, int kThr, bool kStats, bool kHint>
 __global__ void __launch_bounds__(kThr, 1)
 chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
                       float* __restrict__ exp_avg_sq, const uint16_t* __restrict__ grad,
@@ -375,15 +400,24 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
   }
   __syncthreads();
 
+  const uint64_t policy = kHint ? evict_first_policy() : 0;
+  auto load = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    if (kHint) bulk_load_hint(dst, src, bytes, bar, policy);
+    else bulk_load(dst, src, bytes, bar);
+  };
+  auto store = [&](void* dst, const void* src, uint32_t bytes) {
+    if (kHint) bulk_store_hint(dst, src, bytes, policy);
+    else bulk_store(dst, src, bytes);
+  };
   auto issue_load = [&](int64_t k) {  // k-th tile of this CTA
     const int st = static_cast<int>(k % kStages);
     const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
     TmaStage<kTile>& S = stage[st];
     mbar_expect_tx(&full[st], kLoadBytes);
-    bulk_load(S.master, master + e, kTile * 4, &full[st]);
-    bulk_load(S.m, exp_avg + e, kTile * 4, &full[st]);
-    bulk_load(S.v, exp_avg_sq + e, kTile * 4, &full[st]);
-    bulk_load(S.grad, grad + e, kTile * 2, &full[st]);
+    load(S.master, master + e, kTile * 4, &full[st]);
+    load(S.m, exp_avg + e, kTile * 4, &full[st]);
+    load(S.v, exp_avg_sq + e, kTile * 4, &full[st]);
+    load(S.grad, grad + e, kTile * 2, &full[st]);
   };
 
   constexpr int kAhead = kStages - 2;
@@ -429,10 +463,10 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     __syncthreads();
     if (tid == 0) {
       const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
-      bulk_store(master + e, S.master, kTile * 4);
-      bulk_store(exp_avg + e, S.m, kTile * 4);
-      bulk_store(exp_avg_sq + e, S.v, kTile * 4);
-      if (has_param) bulk_store(param_out + e, S.param, kTile * 2);
+      store(master + e, S.master, kTile * 4);
+      store(exp_avg + e, S.m, kTile * 4);
+      store(exp_avg_sq + e, S.v, kTile * 4);
+      if (has_param) store(param_out + e, S.param, kTile * 2);
       bulk_commit();
     }
   }
@@ -646,17 +680,20 @@ constexpr int kUnroll = 2;
 
 // Kernel variant of the bf16-gradient chunk Adam. Selected once per process
 // from PTK_ADAM_VARIANT (benchmarking aid); the default is the measured best.
-// TMA pipeline shapes: (name, tile elements, ring stages, CTAs per SM, threads).
-#define PTK_TMA_VARIANTS(X)               \
-  X(Tma1536x8t384, 1536, 8, 1, 384)       \
-  X(Tma2048x6, 2048, 6, 1, 256)           \
-  X(Tma1536x8t192, 1536, 8, 1, 192)       \
-  X(Tma3072x4t384, 3072, 4, 1, 384)       \
-  X(Tma1792x7t448, 1792, 7, 1, 448)       \
-  X(Tma1536x9t384, 1536, 9, 1, 384)       \
-  X(Tma1280x10t320, 1280, 10, 1, 320)
+// TMA pipeline shapes: (name, tile elements, ring stages, CTAs per SM,
+// threads, L2 evict-first hint).
+#define PTK_TMA_VARIANTS(X)                     \
+  X(Tma1536x8t384, 1536, 8, 1, 384, false)      \
+  X(Tma1536x8t384h, 1536, 8, 1, 384, true)      \
+  X(Tma1536x9t384, 1536, 9, 1, 384, false)      \
+  X(Tma1536x9t384h, 1536, 9, 1, 384, true)      \
+  X(Tma1536x4x2t384, 1536, 4, 2, 384, false)    \
+  X(Tma2048x6, 2048, 6, 1, 256, false)          \
+  X(Tma2048x6h, 2048, 6, 1, 256, true)          \
+  X(Tma3072x4t384, 3072, 4, 1, 384, false)      \
+  X(Tma1792x7t448, 1792, 7, 1, 448, false)
 
-#define PTK_ENUM_ENTRY(V, T, S, P, THR) V,
+#define PTK_ENUM_ENTRY(V, T, S, P, THR, H) V,
 enum class AdamVariant { Ldg, LdgOcc, PTK_TMA_VARIANTS(PTK_ENUM_ENTRY) };
 #undef PTK_ENUM_ENTRY
 
@@ -668,7 +705,7 @@ AdamVariant adam_variant() {
     for (auto& ch : name) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
     if (name == "ldg") return AdamVariant::Ldg;
     if (name == "ldg_occ") return AdamVariant::LdgOcc;
-#define PTK_NAME_ENTRY(V, T, S, P, THR)                                   \
+#define PTK_NAME_ENTRY(V, T, S, P, THR, H)                                \
     {                                                                     \
       std::string tag = #V;                                               \
       for (auto& ch : tag) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch))); \
@@ -700,12 +737,12 @@ void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
   launch_counter()++;
 }
 
-template <int kTile, int kStages, int kPerSm, int kThr, bool kStats>
+template <int kTile, int kStages, int kPerSm, int kThr, bool kStats, bool kHint>
 int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
                const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                cudaStream_t st) {
-  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats>;
+  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint>;
   constexpr int kSmem = kStages * static_cast<int>(sizeof(TmaStage<kTile>));
   static bool configured = false;
   if (!configured) {
@@ -724,14 +761,14 @@ int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
 
 // One launch per chunk: full tiles through the TMA ring, the partial tile by
 // the last CTA.
-template <int kTile, int kStages, int kPerSm, int kThr>
+template <int kTile, int kStages, int kPerSm, int kThr, bool kHint>
 int adam_tma_then_tail(const ptk_adam_scalars& s, float* master, float* m, float* v,
                        const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
                        ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                        cudaStream_t st) {
-  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true>(
+  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true, kHint>(
                      s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st)
-               : launch_tma<kTile, kStages, kPerSm, kThr, false>(
+               : launch_tma<kTile, kStages, kPerSm, kThr, false, kHint>(
                      s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st);
 }
 
@@ -754,10 +791,10 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
   int rc = PTK_OK;
   if constexpr (std::is_same_v<G, GradBf16>) {
     switch (adam_variant()) {
-#define PTK_TMA_CASE(V, T, S, P, THR)                                                       \
+#define PTK_TMA_CASE(V, T, S, P, THR, H)                                                    \
   case AdamVariant::V:                                                                       \
-    rc = adam_tma_then_tail<T, S, P, THR>(s, master, m, v, grad, param_out, n, ws, stats,    \
-                                          gscale_dev, skip_dev, st);                         \
+    rc = adam_tma_then_tail<T, S, P, THR, H>(s, master, m, v, grad, param_out, n, ws, stats, \
+                                             gscale_dev, skip_dev, st);                      \
     return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
       PTK_TMA_VARIANTS(PTK_TMA_CASE)
 #undef PTK_TMA_CASE
@@ -808,9 +845,9 @@ const char* ptk_adam_kernel_name(void) {
   switch (adam_variant()) {
     case AdamVariant::Ldg: return "ldg";
     case AdamVariant::LdgOcc: return "ldg_occ";
-#define PTK_NAME_CASE(V, T, S, P, THR) \
-  case AdamVariant::V:                 \
-    return "tma tile=" #T " stages=" #S " ctas/sm=" #P " threads=" #THR;
+#define PTK_NAME_CASE(V, T, S, P, THR, H) \
+  case AdamVariant::V:                    \
+    return "tma tile=" #T " stages=" #S " ctas/sm=" #P " threads=" #THR " l2_evict_first=" #H;
     PTK_TMA_VARIANTS(PTK_NAME_CASE)
 #undef PTK_NAME_CASE
   }

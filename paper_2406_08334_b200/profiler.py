@@ -22,7 +22,7 @@ import statistics
 import torch
 import torch.nn.functional as F
 
-from .train import ChunkedGPT2, block_forward, op_param_shapes
+from .train import ChunkedGPT2, block_forward, embed, head_logits, op_param_shapes
 
 
 def profile_trace(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
@@ -75,13 +75,12 @@ def profile_trace(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tenso
         with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
             ev_f[0].record()
             b, s = tokens.shape
-            x = F.embedding(tokens, model.params["wte"]) + model.params["wpe"][:s]
-            x = mark_global(0, x)
+            x = mark_global(0, embed(sh, model.params, tokens))
             idx = 1
             for blk in model.blocks:
                 x = block_forward(sh, blk, x, mark=lambda k, out, base=idx: mark_global(base + k, out))
                 idx += 8
-            logits = mark_global(idx, F.linear(x, model.params["wte"]))
+            logits = mark_global(idx, head_logits(sh, model.params, x))
             loss = mark_global(idx + 1, F.cross_entropy(logits.view(-1, sh.vocab).float(),
                                                         targets.reshape(-1)))
         torch.cuda.synchronize()

@@ -37,35 +37,85 @@ BF16 = torch.bfloat16
 
 @dataclass
 class GPT2Shape:
+    """Decoder shape of a trace. Defaults are GPT-2 (biases, 4h MLP, tied
+    embeddings, learned positions); the Llama family of the reference's
+    presets (proj/src/presets.cpp:24-37) is gated (SwiGLU), bias-free
+    (RMSNorm), untied, rotary, with grouped KV heads."""
     hidden: int = 1600
     blocks: int = 48
     heads: int = 25
     vocab: int = 50257
     seq: int = 1024
+    ffn: int = 0          # 0 -> 4 * hidden
+    kv_heads: int = 0     # 0 -> heads
+    gated: bool = False
+    bias: bool = True
+    tied: bool = True
+    learned_pos: bool = True
+
+    @property
+    def ffn_dim(self) -> int:
+        return self.ffn or 4 * self.hidden
+
+    @property
+    def kv_dim(self) -> int:
+        return (self.hidden // self.heads) * (self.kv_heads or self.heads)
 
     @staticmethod
     def from_trace_meta(meta: dict, n_blocks: int) -> "GPT2Shape":
         return GPT2Shape(int(meta["hidden_size"]), n_blocks, int(meta["n_heads"]),
                          int(meta["vocab_size"]), int(meta["seq_len"]))
 
+    @staticmethod
+    def from_trace(trace: dict) -> "GPT2Shape":
+        """Recover the architecture from the trace's parameter bytes (the
+        meta carries only hidden/heads/vocab/seq, proj/src/trace.cpp:275-282)."""
+        meta, ops = trace["meta"], trace["ops"]
+        h, heads = int(meta["hidden_size"]), int(meta["n_heads"])
+        v, s = int(meta["vocab_size"]), int(meta["seq_len"])
+        dt = int(meta.get("dtype_bytes", 2))
+        p = {o["name"].split(".")[0]: o["param_bytes"] // dt for o in ops if o["name"].endswith(".0")
+             or "." not in o["name"]}
+        bias = p["attn_norm"] == 2 * h
+        qkv = p["attn_qkv"] // (h + (1 if bias else 0))  # h + 2*kv_dim
+        kv_dim = (qkv - h) // 2
+        up = p["mlp_up"] // (h + (1 if bias else 0))
+        down_f = (p["mlp_down"] - (h if bias else 0)) // h
+        gated = up == 2 * down_f
+        learned = p["embedding"] == (v + s) * h
+        tied = p["lm_head"] == 0
+        head_dim = h // heads
+        return GPT2Shape(h, trace["n_blocks"], heads, v, s, ffn=down_f,
+                         kv_heads=kv_dim // head_dim, gated=gated, bias=bias, tied=tied,
+                         learned_pos=learned)
+
 
 def op_param_shapes(shape: GPT2Shape) -> list[tuple[str, list[tuple[str, tuple[int, ...]]]]]:
-    """(op name, [(param name, shape)...]) in trace order, GPT-2 with biases and
-    tied embeddings (proj/src/trace.cpp:213-242)."""
-    h, v, s = shape.hidden, shape.vocab, shape.seq
-    ops = [("embedding", [("wte", (v, h)), ("wpe", (s, h))])]
+    """(op name, [(param name, shape)...]) in trace order, weights then biases
+    per op, as synthesize_trace counts them (proj/src/trace.cpp:213-242,316-340)."""
+    h, v, s, f, kv = shape.hidden, shape.vocab, shape.seq, shape.ffn_dim, shape.kv_dim
+    up = 2 * f if shape.gated else f
+
+    def wb(name, out, inp):
+        return [(f"{name}_w", (out, inp))] + ([(f"{name}_b", (out,))] if shape.bias else [])
+
+    def norm(name):
+        return [(f"{name}_w", (h,))] + ([(f"{name}_b", (h,))] if shape.bias else [])
+
+    emb = [("wte", (v, h))] + ([("wpe", (s, h))] if shape.learned_pos else [])
+    ops = [("embedding", emb)]
     for b in range(shape.blocks):
         ops += [
-            (f"attn_norm.{b}", [("ln1_w", (h,)), ("ln1_b", (h,))]),
-            (f"attn_qkv.{b}", [("qkv_w", (3 * h, h)), ("qkv_b", (3 * h,))]),
+            (f"attn_norm.{b}", norm("ln1")),
+            (f"attn_qkv.{b}", wb("qkv", h + 2 * kv, h)),
             (f"attn_core.{b}", []),
-            (f"attn_out.{b}", [("out_w", (h, h)), ("out_b", (h,))]),
-            (f"mlp_norm.{b}", [("ln2_w", (h,)), ("ln2_b", (h,))]),
-            (f"mlp_up.{b}", [("up_w", (4 * h, h)), ("up_b", (4 * h,))]),
+            (f"attn_out.{b}", wb("out", h, h)),
+            (f"mlp_norm.{b}", norm("ln2")),
+            (f"mlp_up.{b}", wb("up", up, h)),
             (f"mlp_act.{b}", []),
-            (f"mlp_down.{b}", [("down_w", (h, 4 * h)), ("down_b", (h,))]),
+            (f"mlp_down.{b}", wb("down", h, f)),
         ]
-    ops += [("lm_head", []), ("cross_entropy", [])]
+    ops += [("lm_head", [] if shape.tied else [("head_w", (v, h))]), ("cross_entropy", [])]
     return ops
 
 
@@ -128,19 +178,22 @@ class ChunkedGPT2:
                 else:
                     self.params[pname] = p
         self.wte_chunk = chunk_of[0]
+        self.head_chunk = chunk_of[len(specs) - 2]  # the lm_head operator's chunk
         self.anchors = {c: torch.zeros((), device=pool.device, requires_grad=True)
                         for c in self.pool_specs} if pool is not None else {}
         for ci, c in enumerate(layout["chunks"]):
             assert 2 * offset[ci] == c["used_bytes"], "chunk payload mismatch"
 
     def init_weights(self, seed: int = 0) -> None:
-        """GPT-2 style init, written straight into the chunk buffers; the
-        fp32 master copies are refreshed from them."""
-        g = torch.Generator(device=self.chunks.device).manual_seed(seed)
+        """GPT-2 / Llama style init, written straight into the chunk buffers;
+        the fp32 master copies are refreshed from them."""
+        dev = self.chunks.device if self.chunks.chunks or self.pool is None else self.pool.device
+        g = torch.Generator(device=dev).manual_seed(seed)
         std = 0.02
         with torch.no_grad():
-            for p in [self.params["wte"], self.params["wpe"]]:
-                p.normal_(0.0, std, generator=g)
+            for name in ("wte", "wpe", "head_w"):
+                if name in self.params:
+                    self.params[name].normal_(0.0, std, generator=g)
             for blk in self.blocks:
                 for k, p in blk.items():
                     if k.endswith("_w") and p.dim() == 2:
@@ -172,12 +225,14 @@ class ChunkedGPT2:
         uses = {c: 0 for c in self.pool_specs}
         plain = {self.wte_chunk} | {self.block_chunk[b] for b, st in enumerate(strategies)
                                     if st != "checkpoint"}
+        if not self.shape.tied:
+            plain.add(self.head_chunk)
         for c in uses:
             uses[c] += 1 if c in plain else 0
         for b, st in enumerate(strategies):
             if st == "checkpoint" and self.block_chunk[b] in uses:
                 uses[self.block_chunk[b]] += 1
-        if self.wte_chunk in uses:
+        if self.shape.tied and self.wte_chunk in uses:
             uses[self.wte_chunk] += 1
         return {c: n for c, n in uses.items() if n > 0}
 
@@ -211,9 +266,8 @@ class ChunkedGPT2:
                 return block_forward(sh, local[blk_id], x)
             return fn
 
-        b, s = tokens.shape
         ensure(self.wte_chunk)
-        x = F.embedding(tokens, params["wte"]) + params["wpe"][:s]
+        x = embed(sh, params, tokens)
         for blk_id, strategy in enumerate(self._strategies()):
             if strategy == "checkpoint":
                 x = torch.utils.checkpoint.checkpoint(checkpointed(blk_id), x, use_reentrant=False)
@@ -224,10 +278,11 @@ class ChunkedGPT2:
                     x = block_forward(sh, blocks[blk_id], x)
             else:
                 x = block_forward(sh, blocks[blk_id], x)
-        if self.wte_chunk in self.pool_specs:  # tied head: another use of chunk 0
+        if sh.tied and self.wte_chunk in self.pool_specs:  # tied head: another use of chunk 0
             gather_into(self.wte_chunk, pool.n_total, None, params, blocks)
-        logits = F.linear(x, params["wte"])
-        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
+        elif not sh.tied:
+            ensure(self.head_chunk)
+        return head_loss(sh, params, x, targets)
 
     def set_block_schedule(self, strategies: list[str]) -> None:
         """Per-block activation policy from the planner's BlockSchedule
@@ -247,8 +302,7 @@ class ChunkedGPT2:
             with torch.autograd.graph.saved_tensors_hooks(pool.pack, pool.unpack):
                 return self._loss_pooled(tokens, targets)
         sh = self.shape
-        b, s = tokens.shape
-        x = F.embedding(tokens, self.params["wte"]) + self.params["wpe"][:s]
+        x = embed(sh, self.params, tokens)
         strategies = getattr(self, "strategies", None) or ["none"] * len(self.blocks)
         for blk, strategy in zip(self.blocks, strategies):
             if strategy == "checkpoint":
@@ -258,26 +312,79 @@ class ChunkedGPT2:
                     x = block_forward(sh, blk, x)
             else:
                 x = block_forward(sh, blk, x)
-        logits = F.linear(x, self.params["wte"])  # tied lm_head
-        return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
+        return head_loss(sh, self.params, x, targets)
+
+
+def embed(sh: GPT2Shape, params: dict, tokens: torch.Tensor) -> torch.Tensor:
+    """The trace's `embedding` operator (token + learned position, or token
+    only for rotary models)."""
+    x = F.embedding(tokens, params["wte"])
+    if sh.learned_pos:
+        x = x + params["wpe"][: tokens.shape[1]]
+    return x
+
+
+def head_logits(sh: GPT2Shape, params: dict, x: torch.Tensor) -> torch.Tensor:
+    """`lm_head` (tied to the embedding, or its own weight)."""
+    return F.linear(x, params["wte"] if sh.tied else params["head_w"])
+
+
+def head_loss(sh: GPT2Shape, params: dict, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+    logits = head_logits(sh, params, x)
+    return F.cross_entropy(logits.view(-1, sh.vocab).float(), targets.reshape(-1))
+
+
+_ROPE_CACHE: dict = {}
+
+
+def _rope(x: torch.Tensor) -> torch.Tensor:
+    """Rotary position embedding on (b, s, heads, head_dim), half-split form."""
+    s, d = x.shape[1], x.shape[-1]
+    key = (s, d, x.device, x.dtype)
+    if key not in _ROPE_CACHE:
+        inv = 1.0 / (10000 ** (torch.arange(0, d, 2, device=x.device, dtype=torch.float32) / d))
+        ang = torch.outer(torch.arange(s, device=x.device, dtype=torch.float32), inv)
+        _ROPE_CACHE[key] = (ang.cos()[None, :, None, :].to(x.dtype),
+                            ang.sin()[None, :, None, :].to(x.dtype))
+    cos, sin = _ROPE_CACHE[key]
+    x1, x2 = x[..., : d // 2], x[..., d // 2:]
+    return torch.cat((x1 * cos - x2 * sin, x2 * cos + x1 * sin), dim=-1)
+
+
+def _norm(sh: GPT2Shape, x, w, b):
+    if sh.bias:
+        return F.layer_norm(x, (sh.hidden,), w, b)
+    return F.rms_norm(x, (sh.hidden,), w)
 
 
 def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor, mark=None) -> torch.Tensor:
     """One transformer block: the trace's attn_norm .. mlp_down operators.
+    GPT-2: LayerNorm, fused QKV with bias, GELU MLP. Llama: RMSNorm, rotary
+    q/k, grouped KV heads, SwiGLU MLP, no biases.
     `mark(k, out)` (profiler only) is called after operator k with its output."""
     mark = mark or (lambda k, out: out)
     b, s, _ = x.shape
-    y = mark(0, F.layer_norm(x, (sh.hidden,), blk["ln1_w"], blk["ln1_b"]))
-    qkv = mark(1, F.linear(y, blk["qkv_w"], blk["qkv_b"]))
-    q, k, v = qkv.view(b, s, 3, sh.heads, sh.hidden // sh.heads).unbind(2)
+    hd = sh.hidden // sh.heads
+    kvh = sh.kv_heads or sh.heads
+    y = mark(0, _norm(sh, x, blk["ln1_w"], blk.get("ln1_b")))
+    qkv = mark(1, F.linear(y, blk["qkv_w"], blk.get("qkv_b")))
+    q, k, v = qkv.split([sh.hidden, sh.kv_dim, sh.kv_dim], dim=-1)
+    q, k, v = q.view(b, s, sh.heads, hd), k.view(b, s, kvh, hd), v.view(b, s, kvh, hd)
+    if not sh.learned_pos:
+        q, k = _rope(q), _rope(k)
     a = mark(2, F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
-                                               v.transpose(1, 2), is_causal=True))
+                                               v.transpose(1, 2), is_causal=True,
+                                               enable_gqa=kvh != sh.heads))
     x = mark(3, x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"],
-                             blk["out_b"]))
-    y = mark(4, F.layer_norm(x, (sh.hidden,), blk["ln2_w"], blk["ln2_b"]))
-    y = mark(5, F.linear(y, blk["up_w"], blk["up_b"]))
-    y = mark(6, F.gelu(y, approximate="tanh"))
-    return mark(7, x + F.linear(y, blk["down_w"], blk["down_b"]))
+                             blk.get("out_b")))
+    y = mark(4, _norm(sh, x, blk["ln2_w"], blk.get("ln2_b")))
+    y = mark(5, F.linear(y, blk["up_w"], blk.get("up_b")))
+    if sh.gated:
+        gate, up = y.chunk(2, dim=-1)
+        y = mark(6, F.silu(gate) * up)
+    else:
+        y = mark(6, F.gelu(y, approximate="tanh"))
+    return mark(7, x + F.linear(y, blk["down_w"], blk.get("down_b")))
 
 
 class ActivationSwap:

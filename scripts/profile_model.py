@@ -34,7 +34,7 @@ def main():
     trace = planner.trace_for("gpt2-1.5b_b8")
     layout = planner.layout_for("gpt2-1.5b_b8")
     cs = ChunkSet([c["used_bytes"] // 2 for c in layout["chunks"]], device=dev)
-    shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
+    shape = GPT2Shape.from_trace(trace)
     model = ChunkedGPT2(shape, layout, cs, trace["ops"])
     model.init_weights(0)
     g = torch.Generator(device=dev).manual_seed(0)
@@ -112,7 +112,7 @@ def train_with_plan(cfg, strategies, x, y, iters=5):
     np_ = cfg["n_persist"]
     cs = ChunkSet(numels[:np_], device=dev)
     pool = ChunkPool(numels, np_, cfg["n_buffer"], device=dev) if np_ < len(numels) else None
-    shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
+    shape = GPT2Shape.from_trace(trace)
     model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(0)
     model.set_block_schedule(strategies)

@@ -176,6 +176,54 @@ def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_pe
     assert counters["d2h_bytes"] > 0 and counters["h2d_bytes"] > 0
 
 
+LLAMA_SPEC = {"hidden_size": 256, "n_blocks": 2, "n_heads": 4, "n_kv_heads": 2, "ffn_hidden": 688,
+              "vocab_size": 1000, "seq_len": 128, "gated_mlp": True, "bias": False,
+              "tied_embeddings": False, "learned_pos_embedding": False}
+
+
+def test_llama_shape_trains_and_offloads_bit_identically(tmp_path, cuda_device):
+    """The Llama family (RMSNorm, rotary, grouped KV, SwiGLU, untied head):
+    the architecture is recovered from the trace's parameter bytes, trains,
+    and with every chunk non-persistent (host Adam, 2 device buffers) gives
+    the all-persistent run's losses and masters bit for bit."""
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+
+    spec = tmp_path / "llama.json"
+    spec.write_text(json.dumps(LLAMA_SPEC))
+    tpath = planner.trace_file(["--spec", str(spec), "--batch", "4"], str(tmp_path / "t.json"))
+    trace = json.load(open(tpath))
+    layout = planner.pack(tpath, grid="2Mi")
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    shape = GPT2Shape.from_trace(trace)
+    assert shape.gated and not shape.bias and not shape.tied and shape.kv_heads == 2
+
+    def run(np_, nb):
+        cs = ChunkSet(numels[:np_], device=cuda_device)
+        pool = ChunkPool(numels, np_, nb, device=cuda_device) if np_ < len(numels) else None
+        model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
+        model.init_weights(seed=0)
+        g = torch.Generator(device=cuda_device).manual_seed(0)
+        losses = []
+        for _ in range(4):
+            x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device, generator=g)
+            losses.append(float(train_step(model, x, (x + 1) % shape.vocab, AdamHyper(lr=1e-3))))
+        torch.cuda.synchronize()
+        ms = [c.master.cpu() for c in cs.chunks]
+        if pool is not None:
+            pool.finish_step()
+            ms += [pool.h_master[c].clone() for c in sorted(pool.numel)]
+        return losses, [m[:n] for m, n in zip(ms, numels)]
+
+    ref_l, ref_m = run(len(numels), 0)
+    l, m = run(0, 2)
+    assert l == ref_l and ref_l[-1] < ref_l[0]
+    for a, b in zip(m, ref_m):
+        assert torch.equal(a, b)
+
+
 def test_profiler_measures_a_loadable_trace(tmp_path, cuda_device):
     """The profiler's measured trace has the synthesized trace's operators and
     parameter bytes, positive measured times that add up to the measured
