@@ -27,6 +27,7 @@ proj/src/sim.cpp:275-451) driven by autograd instead of a trace.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 
@@ -44,9 +45,12 @@ def _sh(stream: torch.cuda.Stream) -> ctypes.c_void_p:
 
 class ChunkPool:
     def __init__(self, numels: list[int], first: int, n_buffer: int, world: int = 1, rank: int = 0,
-                 comm=None, device=None):
+                 comm=None, device=None, cpu_threads: int | None = None):
         if n_buffer < 1:
             raise ValueError("non-persistent chunks need at least one buffer")
+        # the host Adam must not starve the threads that launch the GPU work
+        # (Python main thread + autograd's device thread): leave two cores
+        self.cpu_threads = cpu_threads or max(1, (os.cpu_count() or 4) - 2)
         self.device = torch.device(device or "cuda")
         self.first, self.world, self.rank, self.comm = first, world, rank, comm
         self.n_total = len(numels)
@@ -185,7 +189,7 @@ class ChunkPool:
         d2h_done.synchronize()
         nat.lib.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c]), vp(self.h_m[c]),
                              vp(self.h_v[c]), vp(self.h_grad[c]), vp(self.h_param[c]),
-                             self.shard[c], 0, None, None)
+                             self.shard[c], self.cpu_threads, None, None)
 
     def finish_step(self) -> None:
         for fut in list(self.updates.values()):
