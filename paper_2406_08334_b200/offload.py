@@ -29,6 +29,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import time
 from concurrent.futures import ThreadPoolExecutor
 
 import torch
@@ -69,6 +70,7 @@ class ChunkPool:
         self.host_bytes = sum(16 * s for s in self.shard.values())
         self.slot_of: dict[int, int] = {}
         self.free = list(range(n_buffer - 1, -1, -1))
+        self.slot_released: list = [None] * n_buffer  # compute event at the slot's release
         self.ready: dict[int, torch.cuda.Event] = {}
         self.h2d, self.d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
         self.worker = ThreadPoolExecutor(max_workers=1)
@@ -103,15 +105,27 @@ class ChunkPool:
             return bwd
         return 1 << 30
 
-    def _fetch(self, c: int, keep: int) -> None:
-        """Issue the fetch of chunk c (host update -> H2D shard -> all-gather)."""
+    def _fetch(self, c: int, keep: int, blocking: bool = True) -> bool:
+        """Issue the fetch of chunk c (host update -> H2D shard -> all-gather).
+        A prefetch (blocking=False) never stalls the launching thread on the
+        chunk's pending host update: it is skipped and retried later."""
         if c in self.slot_of:
-            return
-        fut = self.updates.pop(c, None)
+            return True
+        fut = self.updates.get(c)
         if fut is not None:
+            if not blocking and not fut.done():
+                self.counters["prefetch_deferred"] = self.counters.get("prefetch_deferred", 0) + 1
+                return False
+            t0 = time.perf_counter()
             fut.result()  # the previous step's host Adam of this chunk
+            self.counters["host_wait_s"] = self.counters.get("host_wait_s", 0.0) + \
+                time.perf_counter() - t0
+            self.updates.pop(c, None)
         if self.free:
             k = self.free.pop()
+            # compute that used the slot before it was freed must be done
+            if self.slot_released[k] is not None:
+                self.h2d.wait_event(self.slot_released[k])
         else:
             victims = [(self._next_use(v), v) for v in self.slot_of if v not in (c, keep)]
             if not victims:
@@ -120,9 +134,9 @@ class ChunkPool:
             k = self.slot_of.pop(v)
             self.ready.pop(v, None)
             self.counters["evict"] += 1
+            # the evicted chunk may still be read by compute already issued
+            self.h2d.wait_stream(torch.cuda.current_stream(self.device))
         self.slot_of[c] = k
-        # the slot may still be read by compute already issued (evicted chunk)
-        self.h2d.wait_stream(torch.cuda.current_stream(self.device))
         s = self.shard[c]
         dst = self.slots[k][self.rank * s:(self.rank + 1) * s]
         nat.lib.ptk_memcpy_h2d_async(vp(dst), vp(self.h_param[c]), 2 * s, _sh(self.h2d))
@@ -133,6 +147,7 @@ class ChunkPool:
         ev.record(self.h2d)
         self.ready[c] = ev
         self.counters["fetch"] += 1
+        return True
 
     def acquire(self, c: int, position: int, prefetch: int | None = None) -> torch.Tensor:
         """Make chunk c resident for the compute stream; returns its gathered
@@ -144,7 +159,7 @@ class ChunkPool:
             view = self.slots[self.slot_of[c]][: self.shard[c] * self.world]
             if prefetch is not None and prefetch in self.numel and prefetch not in self.slot_of:
                 if self.free or len(self.slot_of) > 1:
-                    self._fetch(prefetch, c)
+                    self._fetch(prefetch, c, blocking=False)
             return view
 
     # --------------------------------------------------------------- drain --
@@ -180,16 +195,24 @@ class ChunkPool:
         done.record(self.d2h)
         cfg = self.hyper.config(self.step, self.world)
         # the device copy is stale once the host update runs: release the slot
+        # (a later fetch into it waits for the compute issued until now)
         if c in self.slot_of:
-            self.free.append(self.slot_of.pop(c))
+            k = self.slot_of.pop(c)
+            released = torch.cuda.Event()
+            released.record(cur)
+            self.slot_released[k] = released
+            self.free.append(k)
             self.ready.pop(c, None)
         self.updates[c] = self.worker.submit(self._host_adam, c, done, cfg)
 
     def _host_adam(self, c: int, d2h_done: torch.cuda.Event, cfg) -> None:
         d2h_done.synchronize()
+        t0 = time.perf_counter()
         nat.lib.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c]), vp(self.h_m[c]),
                              vp(self.h_v[c]), vp(self.h_grad[c]), vp(self.h_param[c]),
                              self.shard[c], self.cpu_threads, None, None)
+        self.counters["host_adam_s"] = self.counters.get("host_adam_s", 0.0) + \
+            time.perf_counter() - t0
 
     def finish_step(self) -> None:
         for fut in list(self.updates.values()):

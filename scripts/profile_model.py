@@ -124,6 +124,8 @@ def train_with_plan(cfg, strategies, x, y, iters=5):
         pool.finish_step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if pool is not None:
+        pool.counters.update(host_wait_s=0.0, host_adam_s=0.0)
     e0.record()
     for _ in range(iters):
         train_step(model, x, y, hyper)
@@ -131,9 +133,30 @@ def train_with_plan(cfg, strategies, x, y, iters=5):
         pool.finish_step()
     e1.record()
     torch.cuda.synchronize()
-    info = {"device_peak_allocated_GB": torch.cuda.max_memory_allocated() / 1e9}
+    counters = dict(pool.counters) if pool is not None else None
+    phase = {"fwd": 0.0, "bwd": 0.0, "step": 0.0}
+    for _ in range(iters):
+        # diagnosis only (synchronised): train_step phase by phase
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
+        if pool is not None:
+            pool.begin_step(model.chunks.step_count + 1, hyper, model.pool_uses())
+        loss = model.loss(x, y)
+        ev[1].record()
+        loss.backward()
+        ev[2].record()
+        model.chunks.step(hyper)
+        ev[3].record()
+        torch.cuda.synchronize()
+        phase["fwd"] += ev[0].elapsed_time(ev[1]) / iters
+        phase["bwd"] += ev[1].elapsed_time(ev[2]) / iters
+        phase["step"] += ev[2].elapsed_time(ev[3]) / iters
     if pool is not None:
-        info["pool"] = dict(pool.counters)
+        pool.finish_step()
+    info = {"device_peak_allocated_GB": torch.cuda.max_memory_allocated() / 1e9,
+            "phase_ms_synchronised": {k: round(v, 2) for k, v in phase.items()}}
+    if counters is not None:
+        info["pool"] = counters
     del model, cs, pool
     torch.cuda.empty_cache()
     return e0.elapsed_time(e1) / iters * 1e-3, info
