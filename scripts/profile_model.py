@@ -86,7 +86,14 @@ def main():
             [MEMPLAN, "plan", "--trace", tpath, "--hw", prof, "--gpu-mem", str(int(budget))],
             check=True, capture_output=True, text=True).stdout)
         cfg = cplan["config"]
+        cpath = os.path.join(OUT, f"plan_measured_{int(budget / 1e9)}GB.json")
+        json.dump(cplan, open(cpath, "w"), indent=1)
+        sim = json.loads(subprocess.run([MEMPLAN, "simulate", "--trace", tpath, "--hw", prof,
+                                         "--plan", cpath], check=True, capture_output=True,
+                                        text=True).stdout)
         real_c, info = train_with_plan(cfg, cplan["strategies"], x, y)
+        info["simulator_t_iter_s"] = sim["t_iter"]
+        info["simulator_m_peak"] = sim["m_peak"]
         rows.append({"gpu_mem_budget": budget, "plan": cfg,
                      "strategies": "".join(s[0] for s in cplan["strategies"]),
                      "cost_model_t_iter_s": cplan["estimate"]["t_iter"],
