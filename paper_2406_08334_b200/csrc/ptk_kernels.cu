@@ -713,7 +713,7 @@ AdamVariant adam_variant() {
     }
     PTK_TMA_VARIANTS(PTK_NAME_ENTRY)
 #undef PTK_NAME_ENTRY
-    return AdamVariant::Tma1536x8t384;
+    return AdamVariant::Tma1536x9t384;  // profiles/README.md, interleaved sweep
   }();
   return v;
 }

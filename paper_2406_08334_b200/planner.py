@@ -51,14 +51,8 @@ def pack(trace_path: str, grid: str | None = None) -> dict:
 
 
 def layout_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
-    """Chunk layout of a named trace, produced by the clean-room planner."""
-    if not os.path.exists(MEMPLAN_BIN):
-        # Planner binary not built in this tree: use the committed pack output
-        # of the reference (byte-identical to ours, tests/test_planner_golden.py).
-        with open(os.path.join(GOLDEN_DIR, f"pack_{name}.json")) as f:
-            out = json.load(f)
-        out.setdefault("bytes_per_param", 2)
-        return out
+    """Chunk layout of a named trace, produced by the clean-room planner
+    (raises if build/memplan is missing: no fallback to stored layouts)."""
     os.makedirs(scratch, exist_ok=True)
     trace = os.path.join(scratch, f"trace_{name}.json")
     run_memplan(["gen-trace"] + TRACE_ARGS[name] + ["-o", trace])
