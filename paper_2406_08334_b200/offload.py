@@ -159,7 +159,9 @@ class ChunkPool:
             view = self.slots[self.slot_of[c]][: self.shard[c] * self.world]
             if prefetch is not None and prefetch in self.numel and prefetch not in self.slot_of:
                 if self.free or len(self.slot_of) > 1:
-                    self._fetch(prefetch, c, blocking=False)
+                    # w > 1: the prefetch's all-gather must be issued in the same
+                    # order on every rank, so it may not depend on host timing
+                    self._fetch(prefetch, c, blocking=self.world > 1)
             return view
 
     # --------------------------------------------------------------- drain --
