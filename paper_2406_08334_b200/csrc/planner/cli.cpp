@@ -302,10 +302,39 @@ int verb_plan(const Args& a, std::ostream& out) {
   const HardwareProfile hw = hardware_from(a);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
-  const SearchOutcome res = find_optimal(w.trace, w.layout, hw, opts);
+  SearchOutcome res = find_optimal(w.trace, w.layout, hw, opts);
+  const int refine = a.num<int>("--refine-sim", 0);
+  if (refine <= 0) {  // the reference's behaviour, byte for byte
+    const BlockSchedule sched = build_block_schedule(res.best.n_block, res.best.n_swap,
+                                                     res.best.n_checkpoint, res.best.n_interval);
+    emit(a.str("--out"), plan_to_json(res.best, w.layout, sched, &res), out);
+    return 0;
+  }
+  // B200 extension: pick among the top-k analytic candidates by simulation
+  const auto ranked = refine_with_simulation(w.trace, w.layout, hw, res, refine);
+  const PlanConfig analytic = res.best;
+  res.best = ranked.front().config;
   const BlockSchedule sched = build_block_schedule(res.best.n_block, res.best.n_swap,
                                                    res.best.n_checkpoint, res.best.n_interval);
-  emit(a.str("--out"), plan_to_json(res.best, w.layout, sched, &res), out);
+  res.estimate = estimate_iteration(w.trace, w.layout, sched, res.best, hw, opts);
+  nlohmann::ordered_json j = nlohmann::ordered_json::parse(plan_to_json(res.best, w.layout, sched, &res));
+  nlohmann::ordered_json r;
+  r["analytic_best"] = {{"n_persist", analytic.n_persist}, {"n_buffer", analytic.n_buffer},
+                        {"n_swap", analytic.n_swap}, {"n_checkpoint", analytic.n_checkpoint}};
+  r["candidates"] = nlohmann::ordered_json::array();
+  for (const RefinedChoice& c : ranked) {
+    nlohmann::ordered_json row;
+    row["n_persist"] = c.config.n_persist;
+    row["n_buffer"] = c.config.n_buffer;
+    row["n_swap"] = c.config.n_swap;
+    row["n_checkpoint"] = c.config.n_checkpoint;
+    row["estimate_t_iter"] = c.estimate_t_iter;
+    row["simulated_t_iter"] = c.simulated_t_iter;
+    row["simulated_m_peak"] = c.simulated_m_peak;
+    r["candidates"].push_back(std::move(row));
+  }
+  j["refined"] = std::move(r);
+  emit(a.str("--out"), j.dump(2) + "\n", out);
   return 0;
 }
 
@@ -485,7 +514,7 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
         {{"--act-coeff"}}, {{"--spike-frac"}}, {{"--residual"}}, {{"-o", "--out"}}}},
       {"pack", {{{"--trace"}, true}, {{"--grid"}}, {{"-o", "--out"}}}},
       {"plan", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--alpha"}}, {{"--s-chunk"}},
-                        {{"-o", "--out"}}})},
+                        {{"--refine-sim"}}, {{"-o", "--out"}}})},
       {"estimate", est_flags},
       {"simulate", sim_flags},
       {"validate", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--samples"}}, {{"--seed"}},

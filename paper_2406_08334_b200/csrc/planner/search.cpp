@@ -27,6 +27,7 @@
 #include "digest.hpp"
 #include "memplan/errors.hpp"
 #include "memplan/search.hpp"
+#include "memplan/sim.hpp"
 
 namespace memplan {
 
@@ -257,6 +258,80 @@ SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
       outcome.best.n_block, outcome.best.n_swap, outcome.best.n_checkpoint, outcome.best.n_interval);
   outcome.estimate = estimate_iteration(trace, layout, best_sched, outcome.best, hw, opts);
   return outcome;
+}
+
+namespace {
+
+// The analytically fastest feasible candidate for every n_persist value: the
+// frontier alone is blind to plans that Eq.2 under-rates (e.g. keeping every
+// chunk on the device and checkpointing more, when the host optimizer cannot
+// hide behind the backward pass).
+std::vector<std::pair<PlanConfig, double>> best_per_persist(const ModelTrace& trace,
+                                                            const ChunkLayout& layout,
+                                                            const HardwareProfile& hw) {
+  const std::vector<Candidate> stream = candidate_stream(layout, trace, hw, CostOptions{});
+  const detail::TraceDigest digest(trace, layout);
+  const detail::LinkDigest links(digest, hw);
+  std::map<std::pair<int, int>, std::unique_ptr<detail::ScheduleDigest>> sdig;
+  std::map<int, std::pair<PlanConfig, double>> best;
+  std::map<int, std::int64_t> best_peak;
+  for (const Candidate& cand : stream) {
+    if (cand.m_peak >= hw.gpu_mem) break;
+    if (!config_feasible(trace, cand.config, cand.m_peak, hw)) continue;
+    const PlanConfig& c = cand.config;
+    const auto key = std::make_pair(c.n_swap, c.n_checkpoint);
+    if (!sdig.count(key)) {
+      const BlockSchedule s = build_block_schedule(c.n_block, c.n_swap, c.n_checkpoint, c.n_interval);
+      sdig.emplace(key, std::make_unique<detail::ScheduleDigest>(digest, s, hw));
+    }
+    const detail::ScheduleDigest& sd = *sdig.at(key);
+    const auto [gpu, cpu] = estimate_optim(layout, c, hw);
+    const double t = detail::fwd_time(digest, sd, links, c.n_persist, nullptr) +
+                     std::max(detail::bwd_time(digest, sd, links, c.n_persist, c.n_buffer, nullptr) +
+                                  gpu,
+                              cpu);
+    auto it = best.find(c.n_persist);
+    if (it == best.end() || config_preferred(t, c, cand.m_peak, it->second.second, it->second.first,
+                                             best_peak[c.n_persist])) {
+      best[c.n_persist] = {c, t};
+      best_peak[c.n_persist] = cand.m_peak;
+    }
+  }
+  std::vector<std::pair<PlanConfig, double>> out;
+  for (auto& [np, v] : best) out.push_back(v);
+  return out;
+}
+
+bool same_config(const PlanConfig& a, const PlanConfig& b) {
+  return a.n_persist == b.n_persist && a.n_buffer == b.n_buffer && a.n_swap == b.n_swap &&
+         a.n_checkpoint == b.n_checkpoint;
+}
+
+}  // namespace
+
+std::vector<RefinedChoice> refine_with_simulation(const ModelTrace& trace, const ChunkLayout& layout,
+                                                  const HardwareProfile& hw,
+                                                  const SearchOutcome& outcome, int top_k) {
+  std::vector<std::pair<PlanConfig, double>> pool;
+  const int k = std::min<int>(top_k, static_cast<int>(outcome.frontier.size()));
+  for (int i = 0; i < k; ++i) pool.push_back(outcome.frontier[i]);
+  for (const auto& cand : best_per_persist(trace, layout, hw)) {
+    bool dup = false;
+    for (const auto& p : pool) dup = dup || same_config(p.first, cand.first);
+    if (!dup) pool.push_back(cand);
+  }
+  std::vector<RefinedChoice> out;
+  for (const auto& [cfg, t_est] : pool) {
+    const BlockSchedule sched =
+        build_block_schedule(cfg.n_block, cfg.n_swap, cfg.n_checkpoint, cfg.n_interval);
+    const SimulationResult sim = simulate(trace, layout, sched, cfg, hw);
+    out.push_back({cfg, t_est, sim.t_iter, sim.m_peak});
+  }
+  std::stable_sort(out.begin(), out.end(), [](const RefinedChoice& a, const RefinedChoice& b) {
+    return config_preferred(a.simulated_t_iter, a.config, a.simulated_m_peak, b.simulated_t_iter,
+                            b.config, b.simulated_m_peak);
+  });
+  return out;
 }
 
 }  // namespace memplan

@@ -81,12 +81,13 @@ def main():
     # 5. a memory-constrained plan (the search must offload / swap / checkpoint),
     #    trained for real with exactly that plan, vs the cost model's estimate
     rows = [row]
-    for budget in (40e9, 30e9):
+    for budget, refine in ((40e9, 0), (40e9, 16), (30e9, 0), (30e9, 16)):
         cplan = json.loads(subprocess.run(
-            [MEMPLAN, "plan", "--trace", tpath, "--hw", prof, "--gpu-mem", str(int(budget))],
+            [MEMPLAN, "plan", "--trace", tpath, "--hw", prof, "--gpu-mem", str(int(budget))] +
+            (["--refine-sim", str(refine)] if refine else []),
             check=True, capture_output=True, text=True).stdout)
         cfg = cplan["config"]
-        cpath = os.path.join(OUT, f"plan_measured_{int(budget / 1e9)}GB.json")
+        cpath = os.path.join(OUT, f"plan_measured_{int(budget / 1e9)}GB{'_refined' if refine else ''}.json")
         json.dump(cplan, open(cpath, "w"), indent=1)
         sim = json.loads(subprocess.run([MEMPLAN, "simulate", "--trace", tpath, "--hw", prof,
                                          "--plan", cpath], check=True, capture_output=True,
@@ -94,7 +95,7 @@ def main():
         real_c, info = train_with_plan(cfg, cplan["strategies"], x, y)
         info["simulator_t_iter_s"] = sim["t_iter"]
         info["simulator_m_peak"] = sim["m_peak"]
-        rows.append({"gpu_mem_budget": budget, "plan": cfg,
+        rows.append({"gpu_mem_budget": budget, "refine_sim": refine, "plan": cfg,
                      "strategies": "".join(s[0] for s in cplan["strategies"]),
                      "cost_model_t_iter_s": cplan["estimate"]["t_iter"],
                      "cost_model_m_peak": cplan["estimate"]["m_peak"],
