@@ -7,7 +7,7 @@
  *   ptk_chunk_adam            <- GPU optimizer time `persist_params / gpu_optim_rate`
  *                                (proj/src/cost.cpp:206-219) and the Sim `GpuOptim`
  *                                task per persistent chunk (proj/src/sim.cpp:245-250)
- *   ptk_grad_stats            <- "gradient-chunk cast/scale" of north_star (not modeled)
+ *   ptk_grad_prep/_stats      <- "gradient-chunk cast/scale" of north_star (not modeled)
  *   ptk_chunk_allgather       <- `gather_time(used_bytes)` (proj/src/hardware.cpp:29-34),
  *                                Sim Gather (proj/src/sim.cpp:335-338)
  *   ptk_chunk_reduce_scatter  <- `reduce_time(used_bytes)` (proj/src/hardware.cpp:36-38),
@@ -18,6 +18,10 @@
  *                                (proj/src/cost.cpp:213-218, proj/src/sim.cpp:446-451)
  *   ptk_memcpy_h2d/d2h_async  <- `transfer_time(shard_bytes, h2d/d2h)` upload/offload
  *                                (proj/src/cost.cpp:126-127,186-187; sim.cpp:352-368)
+ *   ptk_profile_*             <- the calibration constants of HardwareProfile
+ *                                (proj/include/memplan/hardware.hpp:15-27)
+ *   ptk_execute_plan          <- memplan::simulate (proj/include/memplan/sim.hpp:48-50),
+ *                                executed with real transfers and kernels
  *
  * Conventions: plain pointers and sizes only; the caller owns
  * all memory; every call is asynchronous and stream-ordered on the given
@@ -106,6 +110,11 @@ int ptk_chunk_adam_f32grad(const ptk_adam_config* cfg, float* master,
 int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale,
                    float* out_f32 /* nullable */, ptk_grad_stats_t* stats,
                    void* workspace, void* stream);
+/* K2 as SURVEY §8(b) names it: out_f32[i] = float(grad[i]) * scale (the
+ * bf16 -> fp32 cast with scale = 1/(world*loss_scale)), plus the same
+ * statistics; out_f32 is required. */
+int ptk_grad_prep(const uint16_t* grad, int64_t n, float scale, float* out_f32,
+                  ptk_grad_stats_t* stats, void* workspace, void* stream);
 int ptk_stats_reset(ptk_grad_stats_t* stats, void* stream);
 /* coef_out = max_norm > 0 ? min(1, max_norm / (sqrt(sumsq) + 1e-6)) : 1;
  * skip_out (nullable) = nonfinite != 0 */
@@ -203,6 +212,21 @@ int ptk_execute_plan(const char* trace_path, const char* plan_path, const char* 
  * JSON and writes the measured profile JSON to out_path. */
 int ptk_measure_profile(const char* base_profile_path, void* comm, int32_t world,
                         const char* out_path);
+/* The individual probes measure_profile composes (host-synchronising; best
+ * of several repetitions on a private stream):
+ *   ptk_profile_copy_bw        pinned H2D / D2H bytes/s of a `bytes` copy
+ *                              -> HardwareProfile::h2d_bw / d2h_bw
+ *   ptk_profile_collective     alpha (s) of an 8 KiB all-gather and beta
+ *                              (wire bytes/s) of a chunk_bytes all-gather,
+ *                              the gather_time model of proj/src/hardware.cpp:29-34
+ *                              -> coll_alpha / coll_bw
+ *   ptk_profile_gpu_adam_rate  ptk_chunk_adam params/s over n params -> gpu_optim_rate
+ *   ptk_profile_cpu_adam_rate  ptk_cpu_adam params/s over n params   -> cpu_optim_rate */
+int ptk_profile_copy_bw(int64_t bytes, double* h2d_bw, double* d2h_bw);
+int ptk_profile_collective(ptk_comm* comm, int32_t world, int64_t chunk_bytes, double* alpha,
+                           double* bw);
+int ptk_profile_gpu_adam_rate(int64_t n, double* params_per_s);
+int ptk_profile_cpu_adam_rate(int64_t n, double* params_per_s);
 
 /* ---- streams / events / timing helpers used by the host runtime ------- */
 int ptk_stream_create(void** out, int32_t high_priority);

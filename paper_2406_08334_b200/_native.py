@@ -61,6 +61,8 @@ _SIGNATURES = {
                                          c_void_p, c_void_p, c_void_p]),
     "ptk_grad_stats": (c_int32, [c_void_p, c_int64, c_float, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),
+    "ptk_grad_prep": (c_int32, [c_void_p, c_int64, c_float, c_void_p, c_void_p, c_void_p,
+                                c_void_p]),
     "ptk_stats_reset": (c_int32, [c_void_p, c_void_p]),
     "ptk_clip_coef": (c_int32, [c_void_p, c_double, c_void_p, c_void_p, c_void_p]),
     "ptk_fused_rs_adam_ag": (c_int32, [POINTER(AdamConfig), POINTER(c_void_p), POINTER(c_void_p),
@@ -89,6 +91,11 @@ _SIGNATURES = {
     "ptk_execute_plan": (c_int32, [c_char_p, c_char_p, c_char_p, c_void_p, c_int32, c_double,
                                    c_int32, c_char_p, c_char_p]),
     "ptk_measure_profile": (c_int32, [c_char_p, c_void_p, c_int32, c_char_p]),
+    "ptk_profile_copy_bw": (c_int32, [c_int64, POINTER(c_double), POINTER(c_double)]),
+    "ptk_profile_collective": (c_int32, [c_void_p, c_int32, c_int64, POINTER(c_double),
+                                         POINTER(c_double)]),
+    "ptk_profile_gpu_adam_rate": (c_int32, [c_int64, POINTER(c_double)]),
+    "ptk_profile_cpu_adam_rate": (c_int32, [c_int64, POINTER(c_double)]),
     "ptk_stream_create": (c_int32, [POINTER(c_void_p), c_int32]),
     "ptk_stream_destroy": (c_int32, [c_void_p]),
     "ptk_event_create": (c_int32, [POINTER(c_void_p)]),

@@ -889,6 +889,12 @@ int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale, float* out_f32,
   return check_cuda(cudaGetLastError(), "grad_stats_kernel launch");
 }
 
+int ptk_grad_prep(const uint16_t* grad, int64_t n, float scale, float* out_f32,
+                  ptk_grad_stats_t* stats, void* workspace, void* stream) {
+  if (!out_f32) return fail(PTK_EINVAL, "ptk_grad_prep: null fp32 output");
+  return ptk_grad_stats(grad, n, scale, out_f32, stats, workspace, stream);
+}
+
 int ptk_stats_reset(ptk_grad_stats_t* stats, void* stream) {
   if (!stats) return fail(PTK_EINVAL, "ptk_stats_reset: null stats");
   stats_reset_kernel<<<1, 1, 0, as_stream(stream)>>>(stats);

@@ -1,13 +1,15 @@
 // Profiler re-feed: measure the HardwareProfile fields
 // the reference takes as calibration constants (proj/include/memplan/hardware.hpp:15-27,
 // presets flagged "for calibration" in proj/src/presets.cpp:154-159) on this
-// machine, with the same primitives the runtime uses:
-//   h2d_bw / d2h_bw      pinned cudaMemcpyAsync of 512 MiB, best of 5
-//   coll_alpha/coll_bw   NCCL all-gather of 8 KiB (alpha) and 512 MiB (beta)
-//   gpu_optim_rate       fused chunk Adam over 256 Mi params (params/s)
-//   cpu_optim_rate       host Adam over 32 Mi params, all threads (params/s)
+// machine, with the same primitives the runtime uses. Each field has its own
+// C-ABI probe (the `ptk_profile_*` set of SURVEY §8(b)):
+//   h2d_bw / d2h_bw      ptk_profile_copy_bw       pinned cudaMemcpyAsync, best of 5
+//   coll_alpha/coll_bw   ptk_profile_collective    NCCL all-gather of 8 KiB (alpha) and
+//                                                  a large shard (beta)
+//   gpu_optim_rate       ptk_profile_gpu_adam_rate fused chunk Adam (params/s)
+//   cpu_optim_rate       ptk_profile_cpu_adam_rate host Adam, all threads (params/s)
 //   gpu_mem / cpu_mem    cudaMemGetInfo total / physical host pages
-// and the C-ABI used by Python to run the executor and the profiler.
+// measure_profile composes them; the C-ABI also runs the executor.
 #include <cuda_runtime.h>
 #include <unistd.h>
 
@@ -15,7 +17,9 @@
 #include <chrono>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <sstream>
+#include <stdexcept>
 #include <vector>
 
 #include <json.hpp>
@@ -25,15 +29,41 @@
 #include "memplan/execute.hpp"
 #include "../ptk_common.h"
 
-namespace memplan {
-
 namespace {
+
+void check(int rc, const char* what) {
+  if (rc != PTK_OK) throw std::runtime_error(std::string(what) + ": " + ptk_last_error());
+}
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Stream {
+  void* s = nullptr;
+  Stream() { check(ptk_stream_create(&s, 0), "stream"); }
+  ~Stream() { ptk_stream_destroy(s); }
+};
+
+struct DeviceBuf {
+  void* p = nullptr;
+  explicit DeviceBuf(std::size_t bytes) { check_cuda(cudaMalloc(&p, bytes), "cudaMalloc"); }
+  ~DeviceBuf() { cudaFree(p); }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  explicit PinnedBuf(std::size_t bytes) { check(ptk_host_alloc_pinned(&p, bytes), "pinned"); }
+  ~PinnedBuf() { ptk_host_free_pinned(p); }
+};
 
 struct Timer {
   void *a = nullptr, *b = nullptr;
   Timer() {
-    ptk_event_create(&a);
-    ptk_event_create(&b);
+    check(ptk_event_create(&a), "event");
+    check(ptk_event_create(&b), "event");
   }
   ~Timer() {
     ptk_event_destroy(a);
@@ -43,88 +73,106 @@ struct Timer {
   double best_seconds(void* stream, int reps, F&& body) {
     double best = 1e30;
     for (int i = 0; i < reps; ++i) {
-      ptk_event_record(a, stream);
+      check(ptk_event_record(a, stream), "record");
       body();
-      ptk_event_record(b, stream);
-      ptk_stream_synchronize(stream);
+      check(ptk_event_record(b, stream), "record");
+      check(ptk_stream_synchronize(stream), "synchronize");
       float ms = 0;
-      ptk_event_elapsed_ms(a, b, &ms);
+      check(ptk_event_elapsed_ms(a, b, &ms), "elapsed");
       best = std::min(best, static_cast<double>(ms) * 1e-3);
     }
     return best;
   }
 };
 
-}  // namespace
-
-HardwareProfile measure_profile(const HardwareProfile& base, void* comm, int world) {
-  HardwareProfile hw = base;
-  void* s = nullptr;
-  ptk_stream_create(&s, 0);
+void copy_bw(std::size_t bytes, double* h2d, double* d2h) {
+  Stream s;
   Timer timer;
-  const std::size_t copy_bytes = 512ull << 20;
-  void *host = nullptr, *dev = nullptr;
-  ptk_host_alloc_pinned(&host, copy_bytes);
-  cudaMalloc(&dev, copy_bytes);
-  std::memset(host, 1, copy_bytes);
-  hw.h2d_bw = copy_bytes / timer.best_seconds(s, 5, [&] { ptk_memcpy_h2d_async(dev, host, copy_bytes, s); });
-  hw.d2h_bw = copy_bytes / timer.best_seconds(s, 5, [&] { ptk_memcpy_d2h_async(host, dev, copy_bytes, s); });
-
-  if (comm != nullptr && world > 1) {
-    auto* c = static_cast<ptk_comm*>(comm);
-    const std::int64_t small = 4096, large = static_cast<std::int64_t>(copy_bytes / 2 / world);
-    const double t_small = timer.best_seconds(s, 10, [&] { ptk_chunk_allgather(c, dev, small, 0, s); });
-    const double t_large = timer.best_seconds(s, 5, [&] { ptk_chunk_allgather(c, dev, large, 0, s); });
-    hw.coll_alpha = t_small;
-    const double moved = 2.0 * large * world * (world - 1) / world;  // bytes*(w-1)/w of the chunk
-    hw.coll_bw = moved / std::max(1e-9, t_large - t_small);
-    hw.world_size = world;
-  }
-
-  // device Adam rate on a 256 Mi-parameter chunk
-  const std::int64_t n = 256ll << 20;
-  float *master, *m, *v;
-  uint16_t *g, *p;
-  cudaMalloc(&master, 4 * n);
-  cudaMalloc(&m, 4 * n);
-  cudaMalloc(&v, 4 * n);
-  cudaMalloc(&g, 2 * n);
-  cudaMalloc(&p, 2 * n);
-  cudaMemsetAsync(m, 0, 4 * n, static_cast<cudaStream_t>(s));
-  cudaMemsetAsync(v, 0, 4 * n, static_cast<cudaStream_t>(s));
-  ptk_fill_uniform_f32(master, n, 1, 0, 0.05f, s);
-  ptk_fill_uniform_bf16(g, n, 2, 0, 1e-3f, s);
-  int step = 0;
-  const double t_adam = timer.best_seconds(s, 5, [&] {
-    const ptk_adam_config cfg{1e-3, 0.9, 0.999, 1e-8, 0.0, 0, ++step, 1.0};
-    ptk_chunk_adam(&cfg, master, m, v, g, p, n, nullptr, nullptr, nullptr, nullptr, s);
+  PinnedBuf host(bytes);
+  DeviceBuf dev(bytes);
+  std::memset(host.p, 1, bytes);
+  *h2d = bytes / timer.best_seconds(s.s, 5, [&] {
+    check(ptk_memcpy_h2d_async(dev.p, host.p, bytes, s.s), "h2d");
   });
-  hw.gpu_optim_rate = n / t_adam;
-  for (void* q : {static_cast<void*>(master), static_cast<void*>(m), static_cast<void*>(v),
-                  static_cast<void*>(g), static_cast<void*>(p)})
-    cudaFree(q);
+  *d2h = bytes / timer.best_seconds(s.s, 5, [&] {
+    check(ptk_memcpy_d2h_async(host.p, dev.p, bytes, s.s), "d2h");
+  });
+}
 
-  // host Adam rate
-  const std::int64_t hn = 32ll << 20;
-  std::vector<float> hmaster(hn, 0.01f), hm(hn, 0.0f), hv(hn, 0.0f);
-  std::vector<uint16_t> hg(hn, 0x3a83), hp(hn, 0);
+// alpha = time of a tiny all-gather; beta = wire bytes (chunk * (w-1)/w)
+// over the large all-gather's time above alpha -- the reference's
+// gather_time model alpha + b*(w-1)/(w*beta) (proj/src/hardware.cpp:29-34)
+void collective(ptk_comm* c, int world, std::size_t chunk_bytes, double* alpha, double* bw) {
+  Stream s;
+  Timer timer;
+  DeviceBuf dev(chunk_bytes);
+  const std::int64_t small = 4096;
+  const std::int64_t large = static_cast<std::int64_t>(chunk_bytes / 2 / world);
+  const double t_small = timer.best_seconds(s.s, 10, [&] {
+    check(ptk_chunk_allgather(c, dev.p, small, 0, s.s), "allgather");
+  });
+  const double t_large = timer.best_seconds(s.s, 5, [&] {
+    check(ptk_chunk_allgather(c, dev.p, large, 0, s.s), "allgather");
+  });
+  *alpha = t_small;
+  const double moved = 2.0 * large * world * (world - 1) / world;
+  *bw = moved / std::max(1e-9, t_large - t_small);
+}
+
+double gpu_adam_rate(std::int64_t n) {
+  Stream s;
+  Timer timer;
+  DeviceBuf master(4 * n), m(4 * n), v(4 * n), g(2 * n), p(2 * n);
+  auto* cs = static_cast<cudaStream_t>(s.s);
+  check_cuda(cudaMemsetAsync(m.p, 0, 4 * n, cs), "memset");
+  check_cuda(cudaMemsetAsync(v.p, 0, 4 * n, cs), "memset");
+  check(ptk_fill_uniform_f32(master.as<float>(), n, 1, 0, 0.05f, s.s), "fill");
+  check(ptk_fill_uniform_bf16(g.as<uint16_t>(), n, 2, 0, 1e-3f, s.s), "fill");
+  int step = 0;
+  const double t = timer.best_seconds(s.s, 5, [&] {
+    const ptk_adam_config cfg{1e-3, 0.9, 0.999, 1e-8, 0.0, 0, ++step, 1.0};
+    check(ptk_chunk_adam(&cfg, master.as<float>(), m.as<float>(), v.as<float>(),
+                         g.as<uint16_t>(), p.as<uint16_t>(), n, nullptr, nullptr, nullptr,
+                         nullptr, s.s),
+          "chunk_adam");
+  });
+  return n / t;
+}
+
+double cpu_adam_rate(std::int64_t n) {
+  std::vector<float> master(n, 0.01f), m(n, 0.0f), v(n, 0.0f);
+  std::vector<uint16_t> g(n, 0x3a83), p(n, 0);
   double best = 1e30;
   for (int r = 1; r <= 3; ++r) {
     const ptk_adam_config cfg{1e-3, 0.9, 0.999, 1e-8, 0.0, 0, r, 1.0};
     const auto t0 = std::chrono::steady_clock::now();
-    ptk_cpu_adam(&cfg, hmaster.data(), hm.data(), hv.data(), hg.data(), hp.data(), hn, 0, nullptr,
-                 nullptr);
-    best = std::min(best, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    check(ptk_cpu_adam(&cfg, master.data(), m.data(), v.data(), g.data(), p.data(), n, 0,
+                       nullptr, nullptr),
+          "cpu_adam");
+    best = std::min(best,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
   }
-  hw.cpu_optim_rate = hn / best;
+  return n / best;
+}
 
+}  // namespace
+
+namespace memplan {
+
+HardwareProfile measure_profile(const HardwareProfile& base, void* comm, int world) {
+  HardwareProfile hw = base;
+  const std::size_t chunk_bytes = 512ull << 20;
+  copy_bw(chunk_bytes, &hw.h2d_bw, &hw.d2h_bw);
+  if (comm != nullptr && world > 1) {
+    collective(static_cast<ptk_comm*>(comm), world, chunk_bytes, &hw.coll_alpha, &hw.coll_bw);
+    hw.world_size = world;
+  }
+  hw.gpu_optim_rate = gpu_adam_rate(256ll << 20);
+  hw.cpu_optim_rate = cpu_adam_rate(32ll << 20);
   size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
+  check_cuda(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   hw.gpu_mem = static_cast<std::int64_t>(total_b);
   hw.cpu_mem = static_cast<std::int64_t>(sysconf(_SC_PHYS_PAGES)) * sysconf(_SC_PAGE_SIZE);
-  cudaFree(dev);
-  ptk_host_free_pinned(host);
-  ptk_stream_destroy(s);
   hw.validate();
   return hw;
 }
@@ -204,6 +252,48 @@ int ptk_measure_profile(const char* base_profile_path, void* comm, int32_t world
     const memplan::HardwareProfile hw = memplan::measure_profile(base, comm, world);
     std::ofstream out(out_path);
     memplan::save_profile(hw, out);
+    return PTK_OK;
+  } catch (const std::exception& e) {
+    return report(e);
+  }
+}
+
+int ptk_profile_copy_bw(int64_t bytes, double* h2d_bw, double* d2h_bw) {
+  if (bytes <= 0 || !h2d_bw || !d2h_bw) return ptk::fail(PTK_EINVAL, "ptk_profile_copy_bw: bad argument");
+  try {
+    copy_bw(static_cast<std::size_t>(bytes), h2d_bw, d2h_bw);
+    return PTK_OK;
+  } catch (const std::exception& e) {
+    return report(e);
+  }
+}
+
+int ptk_profile_collective(ptk_comm* comm, int32_t world, int64_t chunk_bytes, double* alpha,
+                           double* bw) {
+  if (!comm || world < 2 || chunk_bytes < 16 * world || !alpha || !bw)
+    return ptk::fail(PTK_EINVAL, "ptk_profile_collective: bad argument");
+  try {
+    collective(comm, world, static_cast<std::size_t>(chunk_bytes), alpha, bw);
+    return PTK_OK;
+  } catch (const std::exception& e) {
+    return report(e);
+  }
+}
+
+int ptk_profile_gpu_adam_rate(int64_t n, double* params_per_s) {
+  if (n <= 0 || !params_per_s) return ptk::fail(PTK_EINVAL, "ptk_profile_gpu_adam_rate: bad argument");
+  try {
+    *params_per_s = gpu_adam_rate(n);
+    return PTK_OK;
+  } catch (const std::exception& e) {
+    return report(e);
+  }
+}
+
+int ptk_profile_cpu_adam_rate(int64_t n, double* params_per_s) {
+  if (n <= 0 || !params_per_s) return ptk::fail(PTK_EINVAL, "ptk_profile_cpu_adam_rate: bad argument");
+  try {
+    *params_per_s = cpu_adam_rate(n);
     return PTK_OK;
   } catch (const std::exception& e) {
     return report(e);

@@ -150,6 +150,13 @@ def test_grad_stats_and_clip_coef(cuda_device):
     norm = np.sqrt(sq)
     assert abs(float(coef[0]) - min(1.0, 1.0 / (norm + 1e-6))) <= 1e-6
     assert int(skip[0]) == 0
+    # ptk_grad_prep (SURVEY §8(b) K2 name) = the cast/scale with a required output
+    out2 = torch.zeros_like(out)
+    stats2 = torch.zeros_like(stats)
+    assert nat.raw.ptk_grad_prep(_vp(gd), n, 0.5, None, _vp(stats2), _vp(ws), s) != nat.PTK_OK
+    nat.lib.ptk_grad_prep(_vp(gd), n, 0.5, _vp(out2), _vp(stats2), _vp(ws), s)
+    torch.cuda.synchronize()
+    assert torch.equal(out2, out) and torch.equal(stats2, stats)
 
 
 def test_gscale_dev_multiplies(cuda_device):

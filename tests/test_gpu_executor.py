@@ -13,6 +13,7 @@ must hold per chunk (upload_end < first fwd_start of the chunk; offload after
 the chunk's last bwd_end; update after offload).
 """
 import collections
+import ctypes
 import json
 import os
 import subprocess
@@ -112,4 +113,11 @@ def test_measured_profile_is_sane(tmp_path, cuda_device):
     assert hw["gpu_optim_rate"] > 5e10      # >= 1.4 TB/s of 28 B/param
     assert hw["cpu_optim_rate"] > 1e7
     assert hw["gpu_mem"] > 100e9
+    # the individual ptk_profile_* probes agree with the composed profile's ranges
+    from paper_2406_08334_b200 import _native as nat
+    h2d, d2h, rate = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    nat.lib.ptk_profile_copy_bw(64 << 20, ctypes.byref(h2d), ctypes.byref(d2h))
+    assert 5e9 < h2d.value < 2e11 and 5e9 < d2h.value < 2e11
+    nat.lib.ptk_profile_gpu_adam_rate(64 << 20, ctypes.byref(rate))
+    assert rate.value > 5e10
     subprocess.run([MEMPLAN, "list-presets"], check=True, capture_output=True)

@@ -82,3 +82,14 @@ def test_errors_are_reported():
     assert rc == nat.PTK_OK - 1
     assert "ptk_cpu_adam" in nat.last_error()
     assert nat.shard_elems(-1, 1) == -1
+
+
+def test_host_profile_probe_and_argument_checks():
+    """ptk_profile_cpu_adam_rate is host-only (K6): it runs without a GPU."""
+    from paper_2406_08334_b200 import _native as nat
+    rate = ctypes.c_double()
+    assert nat.raw.ptk_profile_cpu_adam_rate(1 << 20, ctypes.byref(rate)) == nat.PTK_OK
+    assert rate.value > 1e6
+    assert nat.raw.ptk_profile_cpu_adam_rate(0, ctypes.byref(rate)) != nat.PTK_OK
+    assert "ptk_profile_cpu_adam_rate" in nat.last_error()
+    assert nat.raw.ptk_profile_collective(None, 2, 1 << 20, None, None) != nat.PTK_OK
