@@ -514,6 +514,7 @@ def run_e2e(cs, hyper, args, world):
         comp.wait_stream(d2h)
         nat.lib.ptk_memcpy_d2h_async(vp(host_stats), vp(cs.stats), 16, sc)
 
+    link = pcie_ceiling(h2d, d2h, comp)
     steps = max(1, min(args.steps, args.e2e_steps))
     for _ in range(max(1, args.warmup)):
         one_step()
@@ -533,10 +534,51 @@ def run_e2e(cs, hyper, args, world):
     return {"value": round(value, 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
             "steps": steps,
+            # the bound of this number is the host link, not HBM: the same
+            # bytes moved by bare concurrent pinned copies (no kernel)
+            "pcie_ceiling": {**link, "copy_only_ms": round(
+                max(h2d_bytes / link["h2d_gbs_concurrent"], d2h_bytes / link["d2h_gbs_concurrent"])
+                / 1e6, 3)},
+            "frac_of_pcie_ceiling": round(
+                max(h2d_bytes / link["h2d_gbs_concurrent"],
+                    d2h_bytes / link["d2h_gbs_concurrent"]) / 1e6 / ms, 3),
             "path": ("C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
                      f"pinned host buffers, {piece}-element pieces on 3 streams") if world == 1 else
                     ("C-ABI per chunk: H2D local grad chunk -> ptk_chunk_reduce_scatter -> "
                      "ptk_chunk_adam -> ptk_chunk_allgather -> D2H gathered params, 3 streams")}
+
+
+def pcie_ceiling(h2d, d2h, comp, nbytes=1 << 30, reps=3):
+    """Concurrent pinned H2D + D2H of nbytes each (both directions at once,
+    as in the e2e step): the host-link ceiling the e2e number is bound by."""
+    import torch
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import stream_handle
+    hsrc = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    hdst = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    da = torch.empty(nbytes, dtype=torch.uint8, device=torch.cuda.current_device())
+    db = torch.empty_like(da)
+    best = None
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        h2d.wait_stream(comp)
+        d2h.wait_stream(comp)
+        ev[0].record(h2d)
+        ev[2].record(d2h)
+        nat.lib.ptk_memcpy_h2d_async(ctypes.c_void_p(da.data_ptr()), ctypes.c_void_p(hsrc.data_ptr()),
+                                     nbytes, stream_handle(h2d))
+        nat.lib.ptk_memcpy_d2h_async(ctypes.c_void_p(hdst.data_ptr()), ctypes.c_void_p(db.data_ptr()),
+                                     nbytes, stream_handle(d2h))
+        ev[1].record(h2d)
+        ev[3].record(d2h)
+        torch.cuda.synchronize()
+        up, down = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
+        cur = (nbytes / up / 1e6, nbytes / down / 1e6)
+        best = cur if best is None or sum(cur) > sum(best) else best
+    del hsrc, hdst, da, db
+    return {"h2d_gbs_concurrent": round(best[0], 2), "d2h_gbs_concurrent": round(best[1], 2),
+            "bytes_each_way": nbytes}
 
 
 # ------------------------------------------------------------------ CPU arm --

@@ -180,7 +180,9 @@ int ptk_ipc_close_handle(void* dev_ptr);
  * Each call bumps `epoch` (monotone, identical on all ranks), stores it into
  * slot [rank] of every peer and spins until all slots of its own array
  * reached epoch. Orders all prior stream work before later stream work
- * across the world. */
+ * across the world. A peer that does not arrive within
+ * PTK_PEER_BARRIER_TIMEOUT_MS (env, default 60000) of device time makes the
+ * barrier trap: the launch fails instead of hanging the device. */
 int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank,
                      int32_t epoch, void* stream);
 

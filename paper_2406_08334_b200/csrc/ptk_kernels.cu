@@ -24,6 +24,7 @@
 
 #include <cctype>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -599,7 +600,11 @@ struct SignalTable {
   int32_t* slot[PTK_MAX_PEERS];
 };
 
-__global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int epoch) {
+// A peer that never arrives (crashed rank, mismatched epochs) must not hang
+// the device: after timeout_ns of device time the barrier traps, which fails
+// the launch (and every later call of this context) loudly instead.
+__global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int epoch,
+                                    int64_t timeout_ns) {
   const int t = threadIdx.x;
   if (t >= world) return;
   __threadfence_system();
@@ -607,9 +612,19 @@ __global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int ep
                : "memory");
   const int32_t* mine = sig.slot[rank] + t;
   int32_t seen;
-  do {
+  uint64_t t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
     asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
-  } while (seen < epoch);
+    if (seen >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (static_cast<int64_t>(now - t0) > timeout_ns) {
+      printf("ptk_peer_barrier: rank %d timed out waiting for rank %d (epoch %d, seen %d)\n",
+             rank, t, epoch, seen);
+      __trap();
+    }
+    __nanosleep(64);
+  }
 }
 
 // Occupies the stream for `ns` nanoseconds of device time (global timer).
@@ -959,7 +974,12 @@ int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank, 
     if (!signal_peers[r]) return fail(PTK_EINVAL, "ptk_peer_barrier: null signal slot");
     t.slot[r] = signal_peers[r];
   }
-  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch);
+  static const int64_t timeout_ns = [] {
+    const char* e = std::getenv("PTK_PEER_BARRIER_TIMEOUT_MS");
+    const long long ms = e ? std::atoll(e) : 60000;
+    return static_cast<int64_t>(ms > 0 ? ms : 60000) * 1000000;
+  }();
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch, timeout_ns);
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "peer_barrier_kernel launch");
 }
