@@ -19,6 +19,7 @@
 #include "memplan/cli.hpp"
 #include "memplan/errors.hpp"
 #include "memplan/presets.hpp"
+#include "digest.hpp"
 
 namespace memplan {
 
@@ -571,13 +572,9 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
 std::vector<PlanConfig> sample_feasible_configs(const ModelTrace& trace, const ChunkLayout& layout,
                                                 const HardwareProfile& hw, int n_samples,
                                                 unsigned long long seed, const CostOptions& opts) {
-  std::vector<PlanConfig> pool;
-  for (const PlanConfig& c : enumerate_candidates(layout, trace, hw, opts)) {
-    const BlockSchedule sched = build_block_schedule(c.n_block, c.n_swap, c.n_checkpoint,
-                                                     c.n_interval);
-    const PeakMemoryBreakdown mem = estimate_peak_memory(trace, sched, c, hw, opts);
-    if (config_feasible(trace, c, mem.total, hw)) pool.push_back(c);
-  }
+  // same pool as filtering enumerate_candidates by estimate_peak_memory +
+  // config_feasible (proj/src/cli.cpp:272-293), with the stream's cached peaks
+  std::vector<PlanConfig> pool = detail::feasible_candidates(layout, trace, hw, opts);
   // Fisher-Yates with mt19937_64(seed), then keep the first n_samples.
   std::mt19937_64 rng(seed);
   for (std::size_t i = 0; i + 1 < pool.size(); ++i) {

@@ -74,4 +74,10 @@ double bwd_time(const TraceDigest& d, const ScheduleDigest& s, const LinkDigest&
 std::int64_t replay_peak(const ModelTrace& trace, const BlockSchedule& schedule, int n_swap,
                          int n_checkpoint);
 
+// The feasible candidates in enumerate_candidates order (what
+// `validate` samples from), with each peak taken from the cached replay of
+// the candidate stream instead of a fresh estimate_peak_memory per config.
+std::vector<PlanConfig> feasible_candidates(const ChunkLayout& layout, const ModelTrace& trace,
+                                            const HardwareProfile& hw, const CostOptions& opts);
+
 }  // namespace memplan::detail

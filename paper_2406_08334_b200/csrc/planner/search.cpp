@@ -18,8 +18,10 @@
 // frontier is built by the same std::sort over the same sequence, so the
 // result is bit-identical and independent of the thread count.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
+#include <limits>
 #include <map>
 #include <memory>
 #include <thread>
@@ -66,37 +68,56 @@ std::int64_t largest_block_act(const ModelTrace& trace) {
   return *std::max_element(act.begin(), act.end());
 }
 
-bool candidate_before(const Candidate& a, const Candidate& b) {
-  if (a.m_peak != b.m_peak) return a.m_peak < b.m_peak;
-  const PlanConfig& x = a.config;
-  const PlanConfig& y = b.config;
-  if (x.n_persist != y.n_persist) return x.n_persist < y.n_persist;
-  if (x.n_buffer != y.n_buffer) return x.n_buffer < y.n_buffer;
-  if (x.n_swap != y.n_swap) return x.n_swap < y.n_swap;
-  return x.n_checkpoint < y.n_checkpoint;
+// config_feasible with the per-trace largest block activation passed in
+bool feasible_with(const PlanConfig& c, std::int64_t m_peak, const HardwareProfile& hw,
+                   std::int64_t biggest_block) {
+  if (m_peak >= hw.gpu_mem) return false;
+  // swap-ins need one block of activation headroom on the device
+  if (c.n_swap > 0 && hw.gpu_mem - m_peak < biggest_block) return false;
+  return persistent_chunk_bytes(c.s_chunk) * (c.n_chunk - c.n_persist) <= hw.cpu_mem;
 }
 
 // The memory-ordered candidate stream. Peaks come from one activation replay
 // per (n_swap, n_checkpoint) plus the model-state bytes of (n_persist,
 // n_buffer).
+// Sorts v by `less` on up to worker_count threads: sorted runs, then pairwise
+// merges. `less` must be a strict total order (the result is then unique).
+template <typename T, typename Less>
+void sort_unique_keys(std::vector<T>& v, Less less);
+
+// With `cap`, only candidates whose peak is below it are materialised (the
+// walk never passes the first one at or above capacity); `total` receives the
+// size of the full stream.
 std::vector<Candidate> candidate_stream(const ChunkLayout& layout, const ModelTrace& trace,
-                                        const HardwareProfile& hw, const CostOptions& opts) {
+                                        const HardwareProfile& hw, const CostOptions& opts,
+                                        std::int64_t cap = std::numeric_limits<std::int64_t>::max(),
+                                        std::size_t* total = nullptr) {
   const int n_chunk = layout.n_chunk();
   const int n_block = trace.n_blocks;
   const int n_interval = compute_interval(trace, hw);
   const int max_swaps = std::min(swap_cap_layout(n_block, n_interval), swap_cap_bandwidth(trace, hw));
   const int ns_hi = std::min(max_swaps, n_block);
 
-  std::map<std::pair<int, int>, std::int64_t> replay;
+  // replay[ns][nc]: activation peak of one schedule (independent of np, nb)
+  std::vector<std::vector<std::int64_t>> replay(static_cast<std::size_t>(ns_hi) + 1);
   for (int ns = 0; ns <= ns_hi; ++ns) {
     const int nc_lo = ns > 1 ? (ns - 1) * n_interval : 0;
+    replay[ns].assign(static_cast<std::size_t>(std::max(0, n_block - ns)) + 1, 0);
     for (int nc = nc_lo; nc <= n_block - ns; ++nc) {
       const BlockSchedule sched = build_block_schedule(n_block, ns, nc, n_interval);
-      replay[{ns, nc}] = detail::replay_peak(trace, sched, ns, nc);
+      replay[ns][nc] = detail::replay_peak(trace, sched, ns, nc);
     }
   }
 
-  std::vector<Candidate> out;
+  // Sort compact keys (peak, then np/nb/ns/nc packed in 16-bit fields, which
+  // orders exactly like candidate_before) and build the candidates after.
+  struct Key {
+    std::int64_t peak;
+    std::uint64_t rest;
+    std::int64_t before_alpha;
+  };
+  std::vector<Key> keys;
+  std::size_t n_all = 0;
   for (int np = 0; np <= n_chunk; ++np) {
     const int nb_lo = np == n_chunk ? 0 : std::min(3, n_chunk - np);
     const int nb_hi = np == n_chunk ? 0 : n_chunk - np;
@@ -106,28 +127,85 @@ std::vector<Candidate> candidate_stream(const ChunkLayout& layout, const ModelTr
       for (int ns = 0; ns <= ns_hi; ++ns) {
         const int nc_lo = ns > 1 ? (ns - 1) * n_interval : 0;
         for (int nc = nc_lo; nc <= n_block - ns; ++nc) {
-          Candidate c;
-          c.config = PlanConfig{layout.s_chunk, n_chunk, np, nb, n_block, n_interval, ns, nc};
-          c.m_peak_before_alpha = replay.at({ns, nc}) + states;
-          c.m_peak = static_cast<std::int64_t>(
-              std::llround(opts.alpha * static_cast<double>(c.m_peak_before_alpha)));
-          out.push_back(c);
+          const std::int64_t before = replay[ns][nc] + states;
+          const auto peak = static_cast<std::int64_t>(
+              std::llround(opts.alpha * static_cast<double>(before)));
+          ++n_all;
+          if (peak >= cap) continue;
+          keys.push_back({peak,
+                          (static_cast<std::uint64_t>(np) << 48) |
+                              (static_cast<std::uint64_t>(nb) << 32) |
+                              (static_cast<std::uint64_t>(ns) << 16) | static_cast<std::uint64_t>(nc),
+                          before});
         }
       }
     }
   }
+  if (n_chunk >= (1 << 16) || n_block >= (1 << 16))
+    throw InvariantViolation("candidate_stream: more than 65535 chunks or blocks");
   // All five keys together identify a candidate, so any correct sort yields
   // the reference's stable order.
-  std::sort(out.begin(), out.end(), candidate_before);
+  sort_unique_keys(keys, [](const Key& a, const Key& b) {
+    return a.peak != b.peak ? a.peak < b.peak : a.rest < b.rest;
+  });
+  if (total) *total = n_all;
+  std::vector<Candidate> out(keys.size());
+  for (std::size_t i = 0; i < keys.size(); ++i) {
+    const std::uint64_t r = keys[i].rest;
+    Candidate& c = out[i];
+    c.config = PlanConfig{layout.s_chunk, n_chunk, static_cast<int>(r >> 48),
+                          static_cast<int>((r >> 32) & 0xffff), n_block, n_interval,
+                          static_cast<int>((r >> 16) & 0xffff), static_cast<int>(r & 0xffff)};
+    c.m_peak = keys[i].peak;
+    c.m_peak_before_alpha = keys[i].before_alpha;
+  }
   return out;
 }
 
 int worker_count(std::size_t work) {
   int n = g_threads.load();
+  if (n <= 0) {  // not set by the caller: MEMPLAN_THREADS, else every core
+    const char* e = std::getenv("MEMPLAN_THREADS");
+    n = e ? std::atoi(e) : 0;
+  }
   if (n <= 0) n = static_cast<int>(std::thread::hardware_concurrency());
   if (n <= 0) n = 1;
   const int by_work = static_cast<int>(work / 4096) + 1;  // tiny searches stay serial
   return std::max(1, std::min(n, by_work));
+}
+
+template <typename T, typename Less>
+void sort_unique_keys(std::vector<T>& v, Less less) {
+  const int workers = worker_count(v.size() / 16);
+  if (workers <= 1) {
+    std::sort(v.begin(), v.end(), less);
+    return;
+  }
+  const std::size_t per = (v.size() + workers - 1) / workers;
+  std::vector<std::size_t> bounds;
+  for (std::size_t lo = 0; lo < v.size(); lo += per) bounds.push_back(lo);
+  bounds.push_back(v.size());
+  {
+    std::vector<std::thread> pool;
+    for (std::size_t k = 0; k + 1 < bounds.size(); ++k)
+      pool.emplace_back([&, k] { std::sort(v.begin() + bounds[k], v.begin() + bounds[k + 1], less); });
+    for (auto& t : pool) t.join();
+  }
+  while (bounds.size() > 2) {  // merge neighbouring runs, in parallel per level
+    std::vector<std::size_t> next;
+    std::vector<std::thread> pool;
+    for (std::size_t k = 0; k + 1 < bounds.size(); k += 2) {
+      next.push_back(bounds[k]);
+      if (k + 2 < bounds.size())
+        pool.emplace_back([&, k] {
+          std::inplace_merge(v.begin() + bounds[k], v.begin() + bounds[k + 1],
+                             v.begin() + bounds[k + 2], less);
+        });
+    }
+    next.push_back(v.size());
+    for (auto& t : pool) t.join();
+    bounds = std::move(next);
+  }
 }
 
 }  // namespace
@@ -141,14 +219,22 @@ std::vector<PlanConfig> enumerate_candidates(const ChunkLayout& layout, const Mo
   return out;
 }
 
+namespace detail {
+
+std::vector<PlanConfig> feasible_candidates(const ChunkLayout& layout, const ModelTrace& trace,
+                                            const HardwareProfile& hw, const CostOptions& opts) {
+  const std::int64_t biggest_block = largest_block_act(trace);
+  std::vector<PlanConfig> out;
+  for (const Candidate& c : candidate_stream(layout, trace, hw, opts, hw.gpu_mem))
+    if (feasible_with(c.config, c.m_peak, hw, biggest_block)) out.push_back(c.config);
+  return out;
+}
+
+}  // namespace detail
+
 bool config_feasible(const ModelTrace& trace, const PlanConfig& config, std::int64_t m_peak,
                      const HardwareProfile& hw) {
-  if (m_peak >= hw.gpu_mem) return false;
-  // swap-ins need one block of activation headroom on the device
-  if (config.n_swap > 0 && hw.gpu_mem - m_peak < largest_block_act(trace)) return false;
-  const std::int64_t offloaded =
-      persistent_chunk_bytes(config.s_chunk) * (config.n_chunk - config.n_persist);
-  return offloaded <= hw.cpu_mem;
+  return feasible_with(config, m_peak, hw, largest_block_act(trace));
 }
 
 bool config_preferred(double t_iter_a, const PlanConfig& a, std::int64_t peak_a, double t_iter_b,
@@ -164,13 +250,12 @@ bool config_preferred(double t_iter_a, const PlanConfig& a, std::int64_t peak_a,
 SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
                            const HardwareProfile& hw, const CostOptions& opts) {
   hw.validate();
-  const std::vector<Candidate> stream = candidate_stream(layout, trace, hw, opts);
-
-  // Memory-ordered: the first candidate past capacity ends the walk.
-  const auto past = std::partition_point(stream.begin(), stream.end(), [&](const Candidate& c) {
-    return c.m_peak < hw.gpu_mem;
-  });
-  const std::size_t walk = static_cast<std::size_t>(past - stream.begin());
+  // Memory-ordered: the first candidate past capacity ends the walk, so only
+  // the candidates below it are materialised.
+  std::size_t stream_size = 0;
+  const std::vector<Candidate> stream =
+      candidate_stream(layout, trace, hw, opts, hw.gpu_mem, &stream_size);
+  const std::size_t walk = stream.size();
 
   // Shared digests; one schedule digest per (n_swap, n_checkpoint).
   const detail::TraceDigest digest(trace, layout);
@@ -181,10 +266,7 @@ SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
   std::vector<char> feasible(walk, 0);
   for (std::size_t i = 0; i < walk; ++i) {
     const PlanConfig& c = stream[i].config;
-    // config_feasible with the per-trace maximum hoisted out of the loop
-    bool ok = stream[i].m_peak < hw.gpu_mem;
-    if (ok && c.n_swap > 0 && hw.gpu_mem - stream[i].m_peak < biggest_block) ok = false;
-    if (ok && persistent_chunk_bytes(c.s_chunk) * (c.n_chunk - c.n_persist) > hw.cpu_mem) ok = false;
+    const bool ok = feasible_with(c, stream[i].m_peak, hw, biggest_block);
     feasible[i] = ok;
     if (!ok) continue;
     const auto key = std::make_pair(c.n_swap, c.n_checkpoint);
@@ -197,15 +279,25 @@ SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
 
   // Evaluate the feasible prefix in parallel (each t_iter in reference order).
   std::vector<double> t_iter(walk, 0.0);
-  const auto optim = [&](const PlanConfig& c) { return estimate_optim(layout, c, hw); };
+  // estimate_optim depends on n_persist only: one call per value
+  std::vector<std::pair<double, double>> optim(static_cast<std::size_t>(layout.n_chunk()) + 1);
+  for (int np = 0; np <= layout.n_chunk(); ++np) {
+    PlanConfig c = walk ? stream[0].config : PlanConfig{};
+    c.n_persist = np;
+    optim[np] = estimate_optim(layout, c, hw);
+  }
+  std::vector<const detail::ScheduleDigest*> sd_of(walk, nullptr);
+  for (std::size_t i = 0; i < walk; ++i)
+    if (feasible[i])
+      sd_of[i] = sched_digest.at({stream[i].config.n_swap, stream[i].config.n_checkpoint}).get();
   const auto eval_range = [&](std::size_t lo, std::size_t hi) {
     for (std::size_t i = lo; i < hi; ++i) {
       if (!feasible[i]) continue;
       const PlanConfig& c = stream[i].config;
-      const detail::ScheduleDigest& sd = *sched_digest.at({c.n_swap, c.n_checkpoint});
+      const detail::ScheduleDigest& sd = *sd_of[i];
       const double f = detail::fwd_time(digest, sd, links, c.n_persist, nullptr);
       const double b = detail::bwd_time(digest, sd, links, c.n_persist, c.n_buffer, nullptr);
-      const auto [gpu, cpu] = optim(c);
+      const auto [gpu, cpu] = optim[c.n_persist];
       t_iter[i] = f + std::max(b + gpu, cpu);
     }
   };
@@ -244,7 +336,7 @@ SearchOutcome find_optimal(const ModelTrace& trace, const ChunkLayout& layout,
       outcome.best = cand.config;
     }
   }
-  outcome.n_pruned += static_cast<std::int64_t>(stream.size() - walk);
+  outcome.n_pruned += static_cast<std::int64_t>(stream_size - walk);
   if (!have) throw NoFeasibleConfig("even the maximum-savings configuration exceeds device memory");
 
   // Frontier: the same (unstable) introsort over the same sequence as the
@@ -269,7 +361,7 @@ namespace {
 std::vector<std::pair<PlanConfig, double>> best_per_persist(const ModelTrace& trace,
                                                             const ChunkLayout& layout,
                                                             const HardwareProfile& hw) {
-  const std::vector<Candidate> stream = candidate_stream(layout, trace, hw, CostOptions{});
+  const std::vector<Candidate> stream = candidate_stream(layout, trace, hw, CostOptions{}, hw.gpu_mem);
   const detail::TraceDigest digest(trace, layout);
   const detail::LinkDigest links(digest, hw);
   std::map<std::pair<int, int>, std::unique_ptr<detail::ScheduleDigest>> sdig;
