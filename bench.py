@@ -190,11 +190,19 @@ def run_gpu(args):
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet, stream_handle, vp
 
     world, rank, local = dist_setup()
+    mode = args.exchange
+    if args.shared_device:
+        # flow validation on a one-GPU box: every rank on cuda:0, peers mapped
+        # through cudaIpc as on an NVLink node; NCCL refuses duplicate devices,
+        # so only the fused exchange runs and the timings are not a bench value
+        if mode != "fused":
+            raise SystemExit("--shared-device needs --exchange fused")
+        local = 0
+        args.train_steps = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     numels, desc = chunk_numels(args.workload)
-    comm = make_comm(world, rank)
-    mode = args.exchange
+    comm = None if args.shared_device else make_comm(world, rank)
     cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode=mode, comm=comm)
     stream = torch.cuda.current_stream()
     cs.init_synthetic()
@@ -238,6 +246,8 @@ def run_gpu(args):
     sumsq, nonfinite = cs.grad_stats()
     nvl_bytes_rank = cs.algorithmic_nvlink_bytes()
     if mode == "fused" and world > 1:
+        torch.cuda.synchronize()
+        barrier(world)   # no rank unmaps / frees while a peer may still store into it
         cs.close_ipc_peers()
     del cs
     torch.cuda.empty_cache()
@@ -278,6 +288,8 @@ def run_gpu(args):
                 "l2": "inputs larger than L2 (%.1f GB touched per step)" % (bytes_rank / 1e9),
                 "algorithmic_bytes_per_step_per_rank": bytes_rank,
                 "nvlink_bytes_per_step_per_rank": nvl_bytes_rank,
+                **({"shared_device_validation": "all ranks on cuda:0: flow check, not a bench value"}
+                   if args.shared_device else {}),
             },
             "roofline": dict(roofline(kern, hbm_peak, peak_kind, args.workload),
                              live_copy_gbs_this_box=copy_peak,
@@ -465,7 +477,23 @@ def run_e2e(cs, hyper, args, world):
         hg.copy_((c.grad_shard() if world == 1 else c.grad).cpu())
     sc, sh, sd = stream_handle(comp), stream_handle(h2d), stream_handle(d2h)
 
+    def one_step_fused():
+        # all local gradient chunks in, then the fused RS->Adam->AG step
+        # (peer barriers inside), then the gathered parameters out
+        h2d.wait_stream(comp)
+        for c, hg in zip(cs.chunks, host_g):
+            nat.lib.ptk_memcpy_h2d_async(vp(c.grad), ctypes.c_void_p(hg.data_ptr()), 2 * c.n_pad, sh)
+        comp.wait_stream(h2d)
+        cs.step(hyper, stream=comp)
+        d2h.wait_stream(comp)
+        for c, hp in zip(cs.chunks, host_p):
+            nat.lib.ptk_memcpy_d2h_async(ctypes.c_void_p(hp.data_ptr()), vp(c.param), 2 * c.n_pad, sd)
+        comp.wait_stream(d2h)
+        nat.lib.ptk_memcpy_d2h_async(vp(host_stats), vp(cs.stats), 16, sc)
+
     def one_step_sharded():
+        if cs.mode == "fused":
+            return one_step_fused()
         cs.step_count += 1
         cfg = hyper.config(cs.step_count, world)
         nat.lib.ptk_stats_reset(vp(cs.stats), sc)
@@ -544,6 +572,8 @@ def run_e2e(cs, hyper, args, world):
                     d2h_bytes / link["d2h_gbs_concurrent"]) / 1e6 / ms, 3),
             "path": ("C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
                      f"pinned host buffers, {piece}-element pieces on 3 streams") if world == 1 else
+                    ("C-ABI: H2D local grad chunks -> ptk_peer_barrier -> ptk_fused_rs_adam_ag "
+                     "-> ptk_peer_barrier -> D2H gathered params") if cs.mode == "fused" else
                     ("C-ABI per chunk: H2D local grad chunk -> ptk_chunk_reduce_scatter -> "
                      "ptk_chunk_adam -> ptk_chunk_allgather -> D2H gathered params, 3 streams")}
 
@@ -666,6 +696,9 @@ def main():
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shared-device", action="store_true",
+                    help="validation only: all ranks on cuda:0 (one-GPU box), fused exchange "
+                         "over cudaIpc; exercises the N>1 flow, its timings are not a bench value")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -10,6 +10,7 @@ from __future__ import annotations
 import json
 import os
 import subprocess
+import tempfile
 
 from . import REPO_DIR
 
@@ -28,8 +29,10 @@ TRACE_ARGS = {
 def run_memplan(args: list[str]) -> str:
     if not os.path.exists(MEMPLAN_BIN):
         raise FileNotFoundError(f"{MEMPLAN_BIN} not built: run `make planner`")
-    return subprocess.run([MEMPLAN_BIN] + args, check=True, capture_output=True,
-                          text=True).stdout
+    r = subprocess.run([MEMPLAN_BIN] + args, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"memplan {' '.join(args)} failed ({r.returncode}): {r.stderr.strip()}")
+    return r.stdout
 
 
 def trace_file(args: list[str], path: str) -> str:
@@ -38,10 +41,18 @@ def trace_file(args: list[str], path: str) -> str:
     return path
 
 
-def trace_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
-    os.makedirs(scratch, exist_ok=True)
-    with open(trace_file(TRACE_ARGS[name], os.path.join(scratch, f"trace_{name}.json"))) as f:
-        return json.load(f)
+def _with_trace(name: str, fn):
+    """Run fn(trace_path) on a freshly generated trace in a private scratch
+    directory: concurrent ranks of one job never share (or race on) a file."""
+    with tempfile.TemporaryDirectory(prefix="ptk_planner_") as d:
+        return fn(trace_file(TRACE_ARGS[name], os.path.join(d, f"trace_{name}.json")))
+
+
+def trace_for(name: str) -> dict:
+    def load(path):
+        with open(path) as f:
+            return json.load(f)
+    return _with_trace(name, load)
 
 
 def pack(trace_path: str, grid: str | None = None) -> dict:
@@ -50,12 +61,7 @@ def pack(trace_path: str, grid: str | None = None) -> dict:
     return out
 
 
-def layout_for(name: str, scratch: str = "/tmp/ptk_planner") -> dict:
+def layout_for(name: str) -> dict:
     """Chunk layout of a named trace, produced by the clean-room planner
     (raises if build/memplan is missing: no fallback to stored layouts)."""
-    os.makedirs(scratch, exist_ok=True)
-    trace = os.path.join(scratch, f"trace_{name}.json")
-    run_memplan(["gen-trace"] + TRACE_ARGS[name] + ["-o", trace])
-    out = json.loads(run_memplan(["pack", "--trace", trace]))
-    out.setdefault("bytes_per_param", 2)
-    return out
+    return _with_trace(name, pack)
