@@ -192,7 +192,10 @@ int ptk_host_free_pinned(void* ptr);
 int ptk_memcpy_h2d_async(void* dst, const void* src, size_t bytes, void* stream);
 int ptk_memcpy_d2h_async(void* dst, const void* src, size_t bytes, void* stream);
 
-/* ---- K6: host Adam over an offloaded shard (OpenMP, all cores) -------- */
+/* ---- K6: host Adam over an offloaded shard (OpenMP) -------------------
+ * n_threads <= 0: the OpenMP default (OMP_NUM_THREADS if set -- torchrun sets
+ * it to 1 -- else every core). The same update rule as ptk_chunk_adam, bit
+ * for bit; optional statistics of the scaled gradient. */
 int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
                  float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
                  int64_t n, int32_t n_threads, double* sumsq_out,

@@ -50,8 +50,10 @@ class ChunkPool:
         if n_buffer < 1:
             raise ValueError("non-persistent chunks need at least one buffer")
         # the host Adam must not starve the threads that launch the GPU work
-        # (Python main thread + autograd's device thread): leave two cores
-        self.cpu_threads = cpu_threads or max(1, (os.cpu_count() or 4) - 2)
+        # (Python main thread + autograd's device thread): leave two cores per
+        # rank, and split the host between the ranks of this node
+        local_world = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        self.cpu_threads = cpu_threads or max(1, (os.cpu_count() or 4) // local_world - 2)
         self.device = torch.device(device or "cuda")
         self.first, self.world, self.rank, self.comm = first, world, rank, comm
         self.n_total = len(numels)
