@@ -46,6 +46,8 @@ WORKLOADS = {
     "flat128": ("flat 128 MiB chunk", "flat:134217728"),
     "flat256": ("flat 256 MiB chunk", "flat:268435456"),
     "flat512": ("flat 512 MiB chunk", "flat:536870912"),
+    "cfg2flat": ("cfg2's 1,557,608,000 parameters as ONE flat chunk (per-launch overhead "
+                 "diagnostic)", "flat:3115216000"),
 }
 
 
@@ -54,9 +56,9 @@ def chunk_numels(workload: str) -> tuple[list[int], str]:
     kind, arg = src.split(":", 1)
     if kind == "flat":
         return [int(arg) // 2], desc
-    # The chunk table comes from the planner (pack_chunks / chunk_size_search);
-    # the clean-room planner's output is byte-identical to the committed
-    # reference golden (tests/test_planner_golden.py), which is read here.
+    # The chunk table comes from the planner (pack_chunks / chunk_size_search),
+    # run here; its output is byte-identical to the reference's
+    # (tests/test_planner.py against tests/golden/).
     from paper_2406_08334_b200 import planner
     layout = planner.layout_for(arg)
     return [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]], desc
