@@ -440,7 +440,7 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     loss_vals = [float(x) for x in losses]
     out = {"tokens_per_s": round(batch * shape.seq * world / (ms * 1e-3), 1),
            "ms_per_iter": round(ms, 3), "iters": args.train_steps,
-           "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, no final LN as in the trace), "
+           "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, parameter-free final LN: the trace has no ln_f), "
                     f"b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
            "plan": {"n_chunk": len(numels), "n_persist": np_, "n_buffer": n_buffer if pool else 0},
            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),

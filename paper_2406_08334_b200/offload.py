@@ -22,7 +22,14 @@ proj/src/sim.cpp:275-451) driven by autograd instead of a trace.
   (ChunkGather.backward), they are summed in a padded staging tensor,
   reduce-scattered (w > 1), the shard goes D2H on the d2h stream and a worker
   thread runs the host Adam (ptk_cpu_adam — bit-identical to the device rule)
-  producing the bf16 shard the next fetch uploads.
+  producing the bf16 shard the next fetch uploads;
+* pieces: the shard moves in `piece`-element pieces so the three stages
+  overlap inside a chunk — the host Adam of piece k starts as soon as its
+  D2H lands, and a fetch that finds the chunk's update still running uploads
+  each piece the moment the host has finished it (the chunk is still made
+  resident as a whole, as the reference's simulator models it,
+  proj/src/sim.cpp:335-368,438-451). The update is elementwise, so piecewise
+  results are bit-identical to one call over the shard.
 """
 from __future__ import annotations
 
@@ -46,7 +53,8 @@ def _sh(stream: torch.cuda.Stream) -> ctypes.c_void_p:
 
 class ChunkPool:
     def __init__(self, numels: list[int], first: int, n_buffer: int, world: int = 1, rank: int = 0,
-                 comm=None, device=None, cpu_threads: int | None = None):
+                 comm=None, device=None, cpu_threads: int | None = None,
+                 piece: int = 32 * 1024 * 1024):
         if n_buffer < 1:
             raise ValueError("non-persistent chunks need at least one buffer")
         # the host Adam must not starve the threads that launch the GPU work
@@ -77,6 +85,8 @@ class ChunkPool:
         self.h2d, self.d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
         self.worker = ThreadPoolExecutor(max_workers=1)
         self.updates: dict[int, object] = {}   # chunk -> Future of its host Adam
+        self.piece = max(8, piece // 8 * 8)
+        self.piece_done: dict[int, list[threading.Event]] = {}  # chunk -> per-piece host Adam done
         self.position = 0
         self.pending_uses: dict[int, int] = {}
         self.partial: dict[int, torch.Tensor] = {}
@@ -107,22 +117,22 @@ class ChunkPool:
             return bwd
         return 1 << 30
 
+    def _pieces(self, c: int):
+        s = self.shard[c]
+        return [(lo, min(self.piece, s - lo)) for lo in range(0, s, self.piece)]
+
     def _fetch(self, c: int, keep: int, blocking: bool = True) -> bool:
         """Issue the fetch of chunk c (host update -> H2D shard -> all-gather).
         A prefetch (blocking=False) never stalls the launching thread on the
-        chunk's pending host update: it is skipped and retried later."""
+        chunk's pending host update: it is skipped and retried later. A
+        blocking fetch of a chunk whose update is still running uploads it
+        piece by piece as the host finishes each piece."""
         if c in self.slot_of:
             return True
         fut = self.updates.get(c)
-        if fut is not None:
-            if not blocking and not fut.done():
-                self.counters["prefetch_deferred"] = self.counters.get("prefetch_deferred", 0) + 1
-                return False
-            t0 = time.perf_counter()
-            fut.result()  # the previous step's host Adam of this chunk
-            self.counters["host_wait_s"] = self.counters.get("host_wait_s", 0.0) + \
-                time.perf_counter() - t0
-            self.updates.pop(c, None)
+        if fut is not None and not blocking and not fut.done():
+            self.counters["prefetch_deferred"] = self.counters.get("prefetch_deferred", 0) + 1
+            return False
         if self.free:
             k = self.free.pop()
             # compute that used the slot before it was freed must be done
@@ -141,7 +151,19 @@ class ChunkPool:
         self.slot_of[c] = k
         s = self.shard[c]
         dst = self.slots[k][self.rank * s:(self.rank + 1) * s]
-        nat.lib.ptk_memcpy_h2d_async(vp(dst), vp(self.h_param[c]), 2 * s, _sh(self.h2d))
+        done = self.piece_done.get(c) if fut is not None else None
+        waited = 0.0
+        for i, (lo, n) in enumerate(self._pieces(c)):
+            if done is not None and not done[i].is_set():
+                t0 = time.perf_counter()
+                done[i].wait()   # the previous step's host Adam of this piece
+                waited += time.perf_counter() - t0
+            nat.lib.ptk_memcpy_h2d_async(vp(dst[lo:]), vp(self.h_param[c][lo:]), 2 * n,
+                                         _sh(self.h2d))
+        if fut is not None:
+            fut.result()   # surfaces a host-side failure
+            self.updates.pop(c, None)
+            self.counters["host_wait_s"] = self.counters.get("host_wait_s", 0.0) + waited
         self.counters["h2d_bytes"] += 2 * s
         if self.world > 1:
             nat.lib.ptk_chunk_allgather(self.comm, vp(self.slots[k]), s, 0, _sh(self.h2d))
@@ -191,12 +213,16 @@ class ChunkPool:
         if self.world > 1:
             nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
         self.d2h.wait_stream(cur)
-        nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c]), vp(staged[self.rank * s:]), 2 * s,
-                                     _sh(self.d2h))
+        src = staged[self.rank * s:]
+        landed = []
+        for lo, n in self._pieces(c):
+            nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c][lo:]), vp(src[lo:]), 2 * n,
+                                         _sh(self.d2h))
+            ev = torch.cuda.Event()
+            ev.record(self.d2h)
+            landed.append(ev)
         staged.record_stream(self.d2h)
         self.counters["d2h_bytes"] += 2 * s
-        done = torch.cuda.Event()
-        done.record(self.d2h)
         cfg = self.hyper.config(self.step, self.world)
         # the device copy is stale once the host update runs: release the slot
         # (a later fetch into it waits for the compute issued until now)
@@ -207,16 +233,25 @@ class ChunkPool:
             self.slot_released[k] = released
             self.free.append(k)
             self.ready.pop(c, None)
-        self.updates[c] = self.worker.submit(self._host_adam, c, done, cfg)
+        self.piece_done[c] = [threading.Event() for _ in landed]
+        self.updates[c] = self.worker.submit(self._host_adam, c, landed, cfg)
 
-    def _host_adam(self, c: int, d2h_done: torch.cuda.Event, cfg) -> None:
-        d2h_done.synchronize()
-        t0 = time.perf_counter()
-        nat.lib.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c]), vp(self.h_m[c]),
-                             vp(self.h_v[c]), vp(self.h_grad[c]), vp(self.h_param[c]),
-                             self.shard[c], self.cpu_threads, None, None)
-        self.counters["host_adam_s"] = self.counters.get("host_adam_s", 0.0) + \
-            time.perf_counter() - t0
+    def _host_adam(self, c: int, landed: list, cfg) -> None:
+        busy = 0.0
+        for (lo, n), ev, done in zip(self._pieces(c), landed, self.piece_done[c]):
+            ev.synchronize()   # this piece's gradients are in host memory
+            t0 = time.perf_counter()
+            rc = nat.raw.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c][lo:]),
+                                      vp(self.h_m[c][lo:]), vp(self.h_v[c][lo:]),
+                                      vp(self.h_grad[c][lo:]), vp(self.h_param[c][lo:]), n,
+                                      self.cpu_threads, None, None)
+            busy += time.perf_counter() - t0
+            done.set()   # set even on failure: a fetch waiting on it re-raises via result()
+            if rc != nat.PTK_OK:
+                for d in self.piece_done[c]:
+                    d.set()
+                raise RuntimeError(f"ptk_cpu_adam: {nat.last_error()}")
+        self.counters["host_adam_s"] = self.counters.get("host_adam_s", 0.0) + busy
 
     def finish_step(self) -> None:
         for fut in list(self.updates.values()):

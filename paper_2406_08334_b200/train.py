@@ -325,7 +325,13 @@ def embed(sh: GPT2Shape, params: dict, tokens: torch.Tensor) -> torch.Tensor:
 
 
 def head_logits(sh: GPT2Shape, params: dict, x: torch.Tensor) -> torch.Tensor:
-    """`lm_head` (tied to the embedding, or its own weight)."""
+    """`lm_head` (tied to the embedding, or its own weight), after a final
+    norm WITHOUT affine parameters: the reference's traces carry no final-norm
+    operator (proj/src/trace.cpp:320-340 -- embedding, 8 ops per block,
+    lm_head, cross_entropy), so the parameter bytes stay the trace's, while
+    the residual stream is still normalised before the vocabulary projection
+    (without it the 48-block stream makes the first Adam steps unstable)."""
+    x = _norm(sh, x, None, None)
     return F.linear(x, params["wte"] if sh.tied else params["head_w"])
 
 

@@ -144,7 +144,9 @@ def test_non_persistent_chunks_train_bit_identically(tmp_path, cuda_device, n_pe
         layout = planner.pack(tpath, grid="2Mi")
         numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
         cs = ChunkSet(numels[:np_], device=cuda_device)
-        pool = ChunkPool(numels, np_, nb, device=cuda_device) if np_ < len(numels) else None
+        # small ragged pieces: D2H -> host Adam -> H2D pipelined within a chunk
+        pool = (ChunkPool(numels, np_, nb, device=cuda_device, piece=65_544)
+                if np_ < len(numels) else None)
         shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
         model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
         model.init_weights(seed=0)
