@@ -41,6 +41,8 @@ WORKLOADS = {
              "layout:gpt2-1.5b_b8"),
     "cfg1": ("gpt2-1b b2 (reference test model), 4x512MiB chunks, all persistent",
              "layout:gpt2-1b_b2"),
+    "cfg3": ("gpt2-10b b8, 49x512MiB chunks, all persistent on one GPU (158 GB of chunk state)",
+             "layout:gpt2-10b_b8"),
     "flat32": ("flat 32 MiB chunk sweep point", "flat:33554432"),
     "flat64": ("flat 64 MiB chunk", "flat:67108864"),
     "flat128": ("flat 128 MiB chunk", "flat:134217728"),
