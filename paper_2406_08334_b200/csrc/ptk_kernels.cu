@@ -359,6 +359,9 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -397,7 +400,7 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
-    fence_async_smem();
+    fence_mbar_init();  // the inits are visible to the async proxy (complete_tx)
   }
   __syncthreads();
 
@@ -410,8 +413,13 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     if (kHint) bulk_store_hint(dst, src, bytes, policy);
     else bulk_store(dst, src, bytes);
   };
-  auto issue_load = [&](int64_t k) {  // k-th tile of this CTA
-    const int st = static_cast<int>(k % kStages);
+  // Ring positions are carried as (stage, phase) counters -- the pipeline
+  // state of CUTLASS -- rather than k % kStages: no 64-bit division per tile,
+  // and every mbarrier access is a plain [base + 8*stage] address.
+  int load_st = 0;
+  auto issue_load = [&](int64_t k) {  // k-th tile of this CTA, into stage load_st
+    const int st = load_st;
+    load_st = load_st + 1 == kStages ? 0 : load_st + 1;
     const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
     TmaStage<kTile>& S = stage[st];
     mbar_expect_tx(&full[st], kLoadBytes);
@@ -427,13 +435,14 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
 
   double sq = 0.0;
   unsigned bad = 0;
+  int st = 0;
+  uint32_t phase = 0;
   for (int64_t k = 0; k < my_tiles; ++k) {
     if (tid == 0 && k + kAhead < my_tiles) {
       bulk_wait_read<1>();  // the store of tile k-2 (same stage) has read its smem
       issue_load(k + kAhead);
     }
-    const int st = static_cast<int>(k % kStages);
-    mbar_wait(&full[st], static_cast<uint32_t>((k / kStages) & 1));
+    mbar_wait(&full[st], phase);
     TmaStage<kTile>& S = stage[st];
     float usq = 0.0f;
 #pragma unroll
@@ -469,6 +478,10 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
       store(exp_avg_sq + e, S.v, kTile * 4);
       if (has_param) store(param_out + e, S.param, kTile * 2);
       bulk_commit();
+    }
+    if (++st == kStages) {
+      st = 0;
+      phase ^= 1u;
     }
   }
   if (tid == 0) bulk_wait_all();

@@ -1,0 +1,64 @@
+#!/usr/bin/env python3
+"""Launch every libptk kernel once at small, ragged sizes (for
+compute-sanitizer racecheck / synccheck / initcheck, scripts/sanitize.sh):
+each chunk-Adam shape (TMA ring variants incl. the partial last tile, LDG),
+the f32-grad variant, grad stats / prep, clip coefficient, the fused
+RS->Adam->AG kernel over 2 virtual ranks, the peer barrier, fills."""
+import ctypes
+import os
+import sys
+
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def main():
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet, vp
+    dev = torch.device("cuda", 0)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    n = 3 * 148 * 1536 + 777          # several tiles per CTA plus a partial tile
+    master = torch.empty(n, dtype=torch.float32, device=dev)
+    m = torch.zeros_like(master)
+    v = torch.zeros_like(master)
+    g = torch.empty(n, dtype=torch.int16, device=dev)
+    g32 = torch.empty(n, dtype=torch.float32, device=dev)
+    p = torch.empty(n, dtype=torch.int16, device=dev)
+    ws = torch.zeros(int(nat.raw.ptk_stats_workspace_bytes()), dtype=torch.uint8, device=dev)
+    stats = torch.zeros(2, dtype=torch.float64, device=dev)
+    nat.lib.ptk_fill_uniform_f32(vp(master), n, 1, 0, ctypes.c_float(0.05), s)
+    nat.lib.ptk_fill_uniform_bf16(vp(g), n, 2, 0, ctypes.c_float(1e-3), s)
+    cfg = nat.adam_config(lr=1e-3, weight_decay=0.01, adamw=True, step=1)
+    nat.lib.ptk_stats_reset(vp(stats), s)
+    nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(master), vp(m), vp(v), vp(g), vp(p), n,
+                           vp(stats), vp(ws), None, None, s)
+    nat.lib.ptk_grad_prep(vp(g), n, ctypes.c_float(0.5), vp(g32), vp(stats), vp(ws), s)
+    nat.lib.ptk_chunk_adam_f32grad(ctypes.byref(cfg), vp(master), vp(m), vp(v), vp(g32), vp(p),
+                                   n, vp(stats), vp(ws), None, None, s)
+    coef = torch.zeros(1, dtype=torch.float32, device=dev)
+    skip = torch.zeros(1, dtype=torch.int32, device=dev)
+    nat.lib.ptk_clip_coef(vp(stats), ctypes.c_double(1.0), vp(coef), vp(skip), s)
+    nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(master), vp(m), vp(v), vp(g), vp(p), n,
+                           vp(stats), vp(ws), vp(coef), vp(skip), s)
+    torch.cuda.synchronize()
+    print("kernel shape in use:", nat.raw.ptk_adam_kernel_name().decode())
+
+    # fused exchange over 2 virtual ranks + the peer barrier on one device
+    sets = [ChunkSet([10_007, 4096], world=2, rank=r, device=dev, mode="fused") for r in range(2)]
+    for cs in sets:
+        cs.init_synthetic()
+        cs.fill_grads(0)
+        cs.attach_virtual_peers(sets)
+    for cs in sets:
+        cs.step(AdamHyper(lr=1e-3))
+    sig = torch.zeros(nat.PTK_MAX_PEERS, dtype=torch.int32, device=dev)
+    arr = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(sig.data_ptr())
+    nat.lib.ptk_peer_barrier(arr, 1, 0, 1, s)
+    torch.cuda.synchronize()
+    print("driver ok")
+
+
+if __name__ == "__main__":
+    main()
