@@ -125,6 +125,8 @@ class ChunkSet:
                  mode: str = "nccl", comm=None):
         if mode not in ("nccl", "fused"):
             raise ValueError(f"unknown exchange mode {mode!r}")
+        if mode == "nccl" and world > 1 and comm is None:
+            raise ValueError("world > 1 in nccl mode needs a ptk_comm communicator")
         self.world, self.rank, self.mode, self.comm = world, rank, mode, comm
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.chunks: list[ChunkShard] = []
@@ -231,12 +233,12 @@ class ChunkSet:
             self._step_fused(cfg, s, stats)
             return
         for c in self.chunks:
-            if self.world > 1:
+            if self.comm is not None:
                 nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
             nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
                                    vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
                                    c.shard, stats, vp(self.workspace), None, None, s)
-            if self.world > 1:
+            if self.comm is not None:
                 nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
 
     def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
@@ -244,11 +246,11 @@ class ChunkSet:
             self.clip_coef = torch.ones(1, dtype=F32, device=self.device)
             self.skip_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         for c in self.chunks:
-            if self.world > 1:
+            if self.comm is not None:
                 nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
             nat.lib.ptk_grad_stats(vp(c.grad_shard()), c.shard, ctypes.c_float(cfg.grad_scale),
                                    None, vp(self.stats), vp(self.workspace), s)
-        if self.world > 1:
+        if self.comm is not None:
             nat.lib.ptk_stats_allreduce(self.comm, vp(self.stats), s)
         nat.lib.ptk_clip_coef(vp(self.stats), max_grad_norm, vp(self.clip_coef),
                               vp(self.skip_flag) if skip_nonfinite else None, s)
@@ -257,7 +259,7 @@ class ChunkSet:
                                    vp(c.grad_shard()), vp(c.param_shard()), c.shard, None, None,
                                    vp(self.clip_coef), vp(self.skip_flag) if skip_nonfinite else None,
                                    s)
-            if self.world > 1:
+            if self.comm is not None:
                 nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
 
     def _step_fused(self, cfg, s, stats) -> None:

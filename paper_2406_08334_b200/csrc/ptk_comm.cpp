@@ -85,7 +85,7 @@ int ptk_comm_destroy(ptk_comm* c) {
 int ptk_chunk_allgather(ptk_comm* c, void* buf, int64_t shard_elems, int32_t dtype,
                         void* stream) {
   if (!c || !buf || shard_elems < 0) return ptk::fail(PTK_EINVAL, "ptk_chunk_allgather: bad arguments");
-  if (c->world == 1 || shard_elems == 0) return PTK_OK;
+  if (shard_elems == 0) return PTK_OK;  // w = 1 still goes through NCCL (a local copy)
   char* base = static_cast<char*>(buf);
   const void* send = base + static_cast<size_t>(c->rank) * shard_elems * elem_bytes(dtype);
   PTK_TRY_NCCL(ncclAllGather(send, buf, static_cast<size_t>(shard_elems), to_nccl(dtype), c->comm,
@@ -97,7 +97,7 @@ int ptk_chunk_reduce_scatter(ptk_comm* c, void* buf, int64_t shard_elems, int32_
                              void* stream) {
   if (!c || !buf || shard_elems < 0)
     return ptk::fail(PTK_EINVAL, "ptk_chunk_reduce_scatter: bad arguments");
-  if (c->world == 1 || shard_elems == 0) return PTK_OK;
+  if (shard_elems == 0) return PTK_OK;  // w = 1 still goes through NCCL (a local copy)
   char* base = static_cast<char*>(buf);
   void* recv = base + static_cast<size_t>(c->rank) * shard_elems * elem_bytes(dtype);
   PTK_TRY_NCCL(ncclReduceScatter(buf, recv, static_cast<size_t>(shard_elems), to_nccl(dtype),
@@ -107,7 +107,6 @@ int ptk_chunk_reduce_scatter(ptk_comm* c, void* buf, int64_t shard_elems, int32_
 
 int ptk_stats_allreduce(ptk_comm* c, ptk_grad_stats_t* stats, void* stream) {
   if (!c || !stats) return ptk::fail(PTK_EINVAL, "ptk_stats_allreduce: null argument");
-  if (c->world == 1) return PTK_OK;
   PTK_TRY_NCCL(ncclGroupStart());
   PTK_TRY_NCCL(ncclAllReduce(&stats->sumsq, &stats->sumsq, 1, ncclFloat64, ncclSum, c->comm,
                              ptk::as_stream(stream)));
@@ -119,7 +118,6 @@ int ptk_stats_allreduce(ptk_comm* c, ptk_grad_stats_t* stats, void* stream) {
 
 int ptk_comm_barrier(ptk_comm* c, void* stream) {
   if (!c) return ptk::fail(PTK_EINVAL, "ptk_comm_barrier: null comm");
-  if (c->world == 1) return PTK_OK;
   PTK_TRY_NCCL(ncclAllReduce(c->scratch, c->scratch, 1, ncclFloat32, ncclSum, c->comm,
                              ptk::as_stream(stream)));
   return PTK_OK;

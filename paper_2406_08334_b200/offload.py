@@ -57,6 +57,8 @@ class ChunkPool:
                  piece: int = 32 * 1024 * 1024):
         if n_buffer < 1:
             raise ValueError("non-persistent chunks need at least one buffer")
+        if world > 1 and comm is None:
+            raise ValueError("world > 1 needs a ptk_comm communicator")
         # the host Adam must not starve the threads that launch the GPU work
         # (Python main thread + autograd's device thread): leave two cores per
         # rank, and split the host between the ranks of this node
@@ -165,7 +167,7 @@ class ChunkPool:
             self.updates.pop(c, None)
             self.counters["host_wait_s"] = self.counters.get("host_wait_s", 0.0) + waited
         self.counters["h2d_bytes"] += 2 * s
-        if self.world > 1:
+        if self.comm is not None:
             nat.lib.ptk_chunk_allgather(self.comm, vp(self.slots[k]), s, 0, _sh(self.h2d))
         ev = torch.cuda.Event()
         ev.record(self.h2d)
@@ -210,7 +212,7 @@ class ChunkPool:
         cur = torch.cuda.current_stream(self.device)
         staged = torch.zeros(s * self.world, dtype=BF16, device=self.device)
         staged[: grad.numel()] = grad
-        if self.world > 1:
+        if self.comm is not None:
             nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
         self.d2h.wait_stream(cur)
         src = staged[self.rank * s:]

@@ -81,10 +81,22 @@ def test_fused_virtual_ranks_bit_exact(cuda_device, world):
             np.testing.assert_array_equal(_bf16_bits(sets[r].chunks[ci].param), gathered)
 
 
-def test_nccl_mode_single_rank_matches_oracle(cuda_device):
+def _world1_comm(nat):
+    """A real NCCL communicator of one rank: RS / AG / stats all-reduce then
+    go through NCCL (in place, a local copy) exactly as at w > 1."""
+    uid = (ctypes.c_uint8 * nat.PTK_UNIQUE_ID_BYTES)()
+    nat.lib.ptk_comm_unique_id(uid)
+    comm = ctypes.c_void_p()
+    nat.lib.ptk_comm_init(ctypes.byref(comm), 1, 0, uid)
+    return comm
+
+
+@pytest.mark.parametrize("with_comm", [False, True])
+def test_nccl_mode_single_rank_matches_oracle(cuda_device, with_comm):
     nat, ch = _modules()
     numels = [123_457, 65_536]
-    cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device, mode="nccl")
+    comm = _world1_comm(nat) if with_comm else None
+    cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device, mode="nccl", comm=comm)
     cs.init_synthetic()
     cs.fill_grads(0)
     hyper = ch.AdamHyper()
@@ -104,6 +116,20 @@ def test_nccl_mode_single_rank_matches_oracle(cuda_device):
             ol.adam_step(ol.scalars(step=step), mst, m, v, g, out)
         np.testing.assert_array_equal(_bits(c.master), mst.view(np.uint32))
         np.testing.assert_array_equal(_bf16_bits(c.param), out)
+    if comm is not None:
+        # clipping path: RS -> stats -> NCCL stats all-reduce -> clip -> Adam -> AG
+        cs.step(ch.AdamHyper(), max_grad_norm=1.0, skip_nonfinite=True)
+        torch.cuda.synchronize()
+        assert cs.grad_stats()[1] == 0
+        nat.lib.ptk_comm_barrier(comm, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        nat.lib.ptk_comm_destroy(comm)
+
+
+def test_multi_rank_nccl_needs_a_communicator(cuda_device):
+    _, ch = _modules()
+    with pytest.raises(ValueError, match="communicator"):
+        ch.ChunkSet([1024], world=2, rank=0, device=cuda_device, mode="nccl")
 
 
 FULL_SIZE = {  # workload -> (parameters, chunks): SURVEY §8(a) golden layouts
