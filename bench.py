@@ -224,18 +224,34 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier(world)
 
+    # The K timed steps. With --graph (default at N=1) they are captured once
+    # into a CUDA graph (each step with its own step number, so replaying it
+    # once performs exactly steps n+1..n+K) and the timed region is one replay:
+    # small chunks are then bound by the device, not by host launch latency.
+    use_graph = args.graph and world == 1
     launches0 = nat.launch_count()
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(args.steps):
+                cs.step(hyper)
+        torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         barrier(world)
         start.record(stream)
-        for _ in range(args.steps):
-            cs.step(hyper)
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(args.steps):
+                cs.step(hyper)
         end.record(stream)
         torch.cuda.synchronize()
         barrier(world)
     launches = nat.launch_count() - launches0
+    del graph
     ms = start.elapsed_time(end) / args.steps
     ms_max = max_over_ranks(ms, world)
     bytes_rank = cs.algorithmic_hbm_bytes()
@@ -243,7 +259,8 @@ def run_gpu(args):
     value = total_bytes / (ms_max * 1e-3) / 1e9
 
     # Dominant kernel, timed per launch with events on its own stream.
-    kern = time_dominant_kernel(cs, hyper, stream, world, reps=max(1, min(args.steps, 5)))
+    kern = time_dominant_kernel(cs, hyper, stream, world, reps=max(1, min(args.steps, 5)),
+                                use_graph=use_graph)
     hbm_peak, peak_kind = load_peaks()
 
     e2e = run_e2e(cs, hyper, args, world) if not args.no_e2e else None
@@ -289,6 +306,8 @@ def run_gpu(args):
                               "fused": "fused RS->Adam->AG kernel over NVLink peer memory"}[mode]
                              if world > 1 else f"none (w=1, {mode} path)"),
                 "parallelism": f"zero3-dp{world}",
+                "timed_steps": ("one CUDA-graph replay holding the K steps" if use_graph
+                                else "K host-launched steps"),
                 "l2": "inputs larger than L2 (%.1f GB touched per step)" % (bytes_rank / 1e9),
                 "algorithmic_bytes_per_step_per_rank": bytes_rank,
                 "nvlink_bytes_per_step_per_rank": nvl_bytes_rank,
@@ -312,47 +331,75 @@ def run_gpu(args):
     return result
 
 
-def time_dominant_kernel(cs, hyper, stream, world, reps):
+def time_dominant_kernel(cs, hyper, stream, world, reps, use_graph=False):
     """Average launch duration of the step's dominant kernel (CUDA events on
-    the stream it is launched on) and its algorithmic bytes per launch."""
+    the stream it is launched on) and its algorithmic bytes per launch.
+    Eager: events around every launch (includes its launch latency). Graph:
+    `reps` passes over the chunks captured back to back, events around one
+    replay on the launching stream, divided by the number of launches."""
     import torch
     from paper_2406_08334_b200 import _native as nat
     from paper_2406_08334_b200.chunks import stream_handle, vp
-    sh = stream_handle(stream)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in cs.chunks]
     cfg = hyper.config(cs.step_count + 1, world)
     ms, hbm, nvl = 0.0, 0, 0
     torch.cuda.synchronize()
-    for _ in range(reps):
-        for i, (c, (e0, e1)) in enumerate(zip(cs.chunks, ev)):
-            e0.record(stream)
-            if cs.mode == "fused":
-                nat.lib.ptk_fused_rs_adam_ag(ctypes.byref(cfg), cs.peer_grad_ptrs[i],
-                                             cs.peer_param_ptrs[i], world, cs.rank, c.shard,
-                                             vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq),
-                                             vp(cs.stats), vp(cs.workspace), sh)
-            else:
-                nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
-                                       vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
-                                       c.shard, vp(cs.stats), vp(cs.workspace), None, None, sh)
-            e1.record(stream)
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            sh = stream_handle(None)
+            for _ in range(reps):
+                for c in cs.chunks:
+                    _launch_dominant(cs, c, cfg, world, sh)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        for c, (e0, e1) in zip(cs.chunks, ev):
-            ms += e0.elapsed_time(e1)
-            p, w = c.numel, world
-            if cs.mode == "fused":
-                # local state 28P/w + grad shard reads 2P/w from each of w ranks
-                # + param shard writes to w ranks (counted once per byte moved)
-                hbm += 28 * p // w + 2 * p * (w - 1) // w * 2
-                nvl += 2 * p * (w - 1) // w
-            else:
-                hbm += 28 * p // w
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        del g
+    else:
+        sh = stream_handle(stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in cs.chunks]
+        for _ in range(reps):
+            for c, (e0, e1) in zip(cs.chunks, ev):
+                e0.record(stream)
+                _launch_dominant(cs, c, cfg, world, sh)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms += sum(e0.elapsed_time(e1) for e0, e1 in ev)
+    for c in cs.chunks:
+        p, w = c.numel, world
+        if cs.mode == "fused":
+            # local state 28P/w + grad shard reads 2P/w from each of w ranks
+            # + param shard writes to w ranks (counted once per byte moved)
+            hbm += 28 * p // w + 2 * p * (w - 1) // w * 2
+            nvl += 2 * p * (w - 1) // w
+        else:
+            hbm += 28 * p // w
+    hbm, nvl = hbm * reps, nvl * reps
     n = reps * len(cs.chunks)
     name = ("fused_peer_kernel<W>" if cs.mode == "fused"
             else "chunk_adam_tma_kernel (" + nat.raw.ptk_adam_kernel_name().decode() + ")")
     return {"kernel": name, "ms": ms, "hbm_bytes": hbm, "nvl_bytes": nvl, "launches": n,
-            "world": world}
+            "world": world, "timing": "graph of back-to-back launches" if use_graph
+            else "events around each launch"}
+
+
+def _launch_dominant(cs, c, cfg, world, sh):
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200.chunks import vp
+    i = c.chunk_id
+    if cs.mode == "fused":
+        nat.lib.ptk_fused_rs_adam_ag(ctypes.byref(cfg), cs.peer_grad_ptrs[i],
+                                     cs.peer_param_ptrs[i], world, cs.rank, c.shard,
+                                     vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq),
+                                     vp(cs.stats), vp(cs.workspace), sh)
+    else:
+        nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                               vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                               c.shard, vp(cs.stats), vp(cs.workspace), None, None, sh)
 
 
 def roofline(k, hbm_peak, peak_kind, workload):
@@ -369,6 +416,7 @@ def roofline(k, hbm_peak, peak_kind, workload):
             "traffic": traffic_from_profiles(workload),
             "bytes_per_launch": (k["nvl_bytes"] if nvl_bound else k["hbm_bytes"]) // k["launches"],
             "ms_per_launch": round(k["ms"] / k["launches"], 4),
+            "launch_timing": k["timing"],
             "frac_of_8tbs_spec": None if nvl_bound else round(achieved / 8000.0, 4)}
 
 
@@ -700,6 +748,9 @@ def main():
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="N=1: time the K steps as one replay of a CUDA graph holding them "
+                         "(default); --no-graph: host-launched steps")
     ap.add_argument("--shared-device", action="store_true",
                     help="validation only: all ranks on cuda:0 (one-GPU box), fused exchange "
                          "over cudaIpc; exercises the N>1 flow, its timings are not a bench value")

@@ -1,0 +1,248 @@
+#!/usr/bin/env python3
+"""BASELINE configs 3 and 4 end to end on one B200: train a model that does
+NOT fit on the device as all-persistent chunks (GPT-2 10B b8, Llama-2 13B b8)
+with exactly the plan the cost-model search picks from MEASURED inputs.
+
+  1. profile a K-block model of the same shape (same hidden / heads / ffn /
+     vocab, all chunks persistent) with the live profiler -> per-operator
+     measured times, saved activations and transient peaks;
+  2. the full-depth trace = the synthesized trace's operator list and
+     parameter bytes (proj/src/trace.cpp:260-344) with the measured values
+     (block operators: median over the profiled blocks; every block of these
+     models is identical);
+  3. measure the HardwareProfile (ptk_measure_profile);
+  4. `memplan plan` on measured trace + measured profile -> (np, nb, ns, nc);
+     `memplan simulate` on the same inputs;
+  5. train with that plan (persistent chunks in HBM, the rest in pinned host
+     memory behind n_buffer device slots with host Adam, swap / checkpoint
+     blocks) and report tokens/s, measured iteration time against the
+     estimate and the simulation, and the device peak against the model's.
+
+    python scripts/train_large.py --model llama-13b --batch 8
+Writes gpurun_out/train_large_<model>_b<batch>.json.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+OUT = os.path.join(REPO, "gpurun_out")
+MEMPLAN = os.path.join(REPO, "build", "memplan")
+
+
+def memplan(*args) -> dict:
+    r = subprocess.run([MEMPLAN, *map(str, args)], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"memplan {' '.join(map(str, args))}: {r.stderr.strip()}")
+    return json.loads(r.stdout)
+
+
+def spec_of(shape, n_blocks: int) -> dict:
+    return {"hidden_size": shape.hidden, "n_blocks": n_blocks, "n_heads": shape.heads,
+            "n_kv_heads": shape.kv_heads or shape.heads, "ffn_hidden": shape.ffn_dim,
+            "vocab_size": shape.vocab, "seq_len": shape.seq, "gated_mlp": shape.gated,
+            "bias": shape.bias, "tied_embeddings": shape.tied,
+            "learned_pos_embedding": shape.learned_pos}
+
+
+def host_available_bytes() -> int:
+    avail = None
+    with open("/proc/meminfo") as f:
+        for line in f:
+            if line.startswith("MemAvailable:"):
+                avail = int(line.split()[1]) * 1024
+    try:
+        with open("/sys/fs/cgroup/memory.max") as f:
+            lim = f.read().strip()
+        if lim != "max":
+            with open("/sys/fs/cgroup/memory.current") as f:
+                avail = min(avail, int(lim) - int(f.read().strip()))
+    except OSError:
+        pass
+    return avail
+
+
+def measured_full_trace(full: dict, shape, batch: int, k_blocks: int, dev, work: str) -> dict:
+    """Steps 1-2: profile a k-block model of the same shape, expand to full depth."""
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import ChunkSet
+    from paper_2406_08334_b200.profiler import profile_trace
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape
+    spath = os.path.join(work, "spec_small.json")
+    json.dump(spec_of(shape, k_blocks), open(spath, "w"))
+    tpath = planner.trace_file(["--spec", spath, "--batch", str(batch)],
+                               os.path.join(work, "trace_small.json"))
+    small = json.load(open(tpath))
+    lay = planner.pack(tpath)
+    cs = ChunkSet([c["used_bytes"] // 2 for c in lay["chunks"]], device=dev)
+    sshape = GPT2Shape.from_trace(small)
+    model = ChunkedGPT2(sshape, lay, cs, small["ops"])
+    model.init_weights(0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.randint(0, shape.vocab, (batch, shape.seq), device=dev, generator=g)
+    meas = profile_trace(model, x, (x + 1) % shape.vocab, reps=3)
+    del model, cs
+    torch.cuda.empty_cache()
+    by_kind: dict[str, list[dict]] = {}
+    top: dict[str, dict] = {}
+    for o in meas["ops"]:
+        if o["block_id"] is None:
+            top[o["name"]] = o
+        else:
+            by_kind.setdefault(o["name"].split(".")[0], []).append(o)
+    keys = ("t_fwd", "t_bwd", "act_bytes", "d_peak_op")
+    ops = []
+    for o in full["ops"]:
+        if o["block_id"] is None:
+            src = {k: top[o["name"]][k] for k in keys}
+        else:
+            group = by_kind[o["name"].split(".")[0]]
+            src = {k: statistics.median(m[k] for m in group) for k in keys}
+            src["act_bytes"] = int(src["act_bytes"])
+            src["d_peak_op"] = int(src["d_peak_op"])
+        ops.append(dict(o, **src, d_cur_prior=0, d_peak_prior=0, d_cur_op=0))
+    meta = dict(full["meta"], generator=f"profile_trace on a {k_blocks}-block model of the same "
+                "shape, block operators replicated (median over profiled blocks)",
+                timings="measured", device=torch.cuda.get_device_name())
+    return {"meta": meta, "m_fwd": meas["m_fwd"], "n_blocks": full["n_blocks"], "ops": ops}
+
+
+def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters: int,
+                    warmup: int) -> dict:
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    cfg = plan["config"]
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    np_ = cfg["n_persist"]
+    t0 = time.perf_counter()
+    cs = ChunkSet(numels[:np_], device=dev)
+    pool = ChunkPool(numels, np_, cfg["n_buffer"], device=dev) if np_ < len(numels) else None
+    shape = GPT2Shape.from_trace(full)
+    model = ChunkedGPT2(shape, layout, cs, full["ops"], pool=pool)
+    model.init_weights(0)
+    model.set_block_schedule(plan["strategies"])
+    setup_s = time.perf_counter() - t0
+    hyper = AdamHyper(lr=1e-4)
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.randint(0, shape.vocab, (batch, shape.seq), device=dev, generator=g)
+    y = (x + 1) % shape.vocab
+    losses = []
+    torch.cuda.reset_peak_memory_stats()
+    for _ in range(warmup):
+        losses.append(train_step(model, x, y, hyper))
+    if pool is not None:
+        pool.finish_step()
+        pool.counters.update(host_wait_s=0.0, host_adam_s=0.0, fetch=0, evict=0, h2d_bytes=0,
+                             d2h_bytes=0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    for _ in range(iters):
+        losses.append(train_step(model, x, y, hyper))
+    if pool is not None:
+        pool.finish_step()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - w0) / iters
+    t_iter = e0.elapsed_time(e1) / iters * 1e-3
+    out = {"t_iter_s": t_iter, "wall_iter_s": wall, "tokens_per_s": batch * shape.seq / t_iter,
+           "iters": iters, "warmup": warmup, "setup_s": round(setup_s, 1),
+           "losses": [round(float(v), 4) for v in losses],
+           "device_peak_allocated_GB": torch.cuda.max_memory_allocated() / 1e9,
+           "persistent_chunk_GB": sum(16 * c.shard for c in cs.chunks) / 1e9}
+    if pool is not None:
+        out["pool"] = {k: (round(v, 3) if isinstance(v, float) else v)
+                       for k, v in pool.counters.items()}
+        out["pool"]["per_iter_h2d_GB"] = pool.counters["h2d_bytes"] / iters / 1e9
+        out["pool"]["per_iter_d2h_GB"] = pool.counters["d2h_bytes"] / iters / 1e9
+        out["pinned_host_GB"] = pool.host_bytes / 1e9
+        out["buffer_GB"] = pool.device_bytes / 1e9
+    del model, cs, pool
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama-13b")
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--profile-blocks", type=int, default=4)
+    ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--host-frac", type=float, default=0.7,
+                    help="refuse a plan whose pinned host bytes exceed this fraction of the "
+                         "host memory available now (protects the box)")
+    ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
+    args = ap.parse_args()
+    from paper_2406_08334_b200 import planner, runtime
+    from paper_2406_08334_b200.train import GPT2Shape
+    os.makedirs(OUT, exist_ok=True)
+    dev = torch.device("cuda", 0)
+    tag = f"{args.model}_b{args.batch}"
+    work = tempfile.mkdtemp(prefix="train_large_")
+    full_path = planner.trace_file(["--model", args.model, "--batch", str(args.batch)],
+                                   os.path.join(work, "trace_synth.json"))
+    synth = json.load(open(full_path))
+    shape = GPT2Shape.from_trace(synth)
+    t0 = time.perf_counter()
+    full = measured_full_trace(synth, shape, args.batch, args.profile_blocks, dev, work)
+    profile_s = time.perf_counter() - t0
+    tpath = os.path.join(OUT, f"trace_{tag}_measured.json")
+    json.dump(full, open(tpath, "w"), indent=1)
+
+    base = os.path.join(work, "base_profile.json")
+    json.dump({"h2d_bw": 5.5e10, "d2h_bw": 5.5e10, "coll_alpha": 2e-5, "coll_bw": 7.7e11,
+               "world_size": 1, "gpu_mem": 180_000_000_000, "cpu_mem": 1_000_000_000_000,
+               "cpu_optim_rate": 1e9, "gpu_optim_rate": 1e11}, open(base, "w"))
+    prof = os.path.join(OUT, f"profile_{tag}.json")
+    hw = runtime.measure_profile(base, prof)
+    extra = ["--gpu-mem", args.gpu_mem] if args.gpu_mem else []
+    plan = memplan("plan", "--trace", tpath, "--hw", prof, *extra)
+    ppath = os.path.join(OUT, f"plan_{tag}_measured.json")
+    json.dump(plan, open(ppath, "w"), indent=1)
+    sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath)
+    layout = planner.pack(tpath)
+    cfg = plan["config"]
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    pinned = 16 * sum(numels[cfg["n_persist"]:])
+    swap_act = sum(o["act_bytes"] for o in full["ops"]
+                   if o["block_id"] is not None and plan["strategies"][o["block_id"]] == "swap")
+    avail = host_available_bytes()
+    row = {"model": args.model, "batch": args.batch, "seq": shape.seq, "n_gpus": 1,
+           "params": sum(numels), "plan": cfg,
+           "strategies": "".join(s[0] for s in plan["strategies"]),
+           "cost_model_t_iter_s": plan["estimate"]["t_iter"],
+           "cost_model_m_peak_GB": plan["estimate"]["m_peak"] / 1e9,
+           "simulator_t_iter_s": sim["t_iter"], "simulator_m_peak_GB": sim["m_peak"] / 1e9,
+           "trace_fwd_s": sum(o["t_fwd"] for o in full["ops"]),
+           "trace_bwd_s": sum(o["t_bwd"] for o in full["ops"]),
+           "profile_s": round(profile_s, 1), "measured_profile": hw,
+           "pinned_host_needed_GB": (pinned + swap_act) / 1e9,
+           "host_available_GB": avail / 1e9}
+    print(json.dumps(row), flush=True)
+    if pinned + swap_act > args.host_frac * avail:
+        row["skipped"] = (f"plan needs {(pinned + swap_act) / 1e9:.1f} GB pinned host memory, "
+                          f"more than {args.host_frac} x {avail / 1e9:.1f} GB available")
+    else:
+        res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup)
+        row.update(res)
+        row["rel_err_cost_model"] = abs(res["t_iter_s"] - row["cost_model_t_iter_s"]) / res["t_iter_s"]
+        row["rel_err_simulator"] = abs(res["t_iter_s"] - row["simulator_t_iter_s"]) / res["t_iter_s"]
+    print(json.dumps(row, indent=1))
+    json.dump(row, open(os.path.join(OUT, f"train_large_{tag}.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -126,6 +126,46 @@ def test_nccl_mode_single_rank_matches_oracle(cuda_device, with_comm):
         nat.lib.ptk_comm_destroy(comm)
 
 
+def test_cuda_graph_of_steps_matches_eager(cuda_device):
+    """bench.py times the K steps as ONE replay of a CUDA graph holding them
+    (each step captured with its own step number). That replay must leave
+    exactly the state of K host-launched steps: master / m / v / params bit
+    for bit, and the last step's gradient statistics."""
+    nat, ch = _modules()
+    numels = [1_000_003, 3 * 1536 * 148 + 77]   # partial tile + several full waves
+
+    def make():
+        cs = ch.ChunkSet(numels, device=cuda_device)
+        cs.init_synthetic()
+        cs.fill_grads(0)
+        return cs
+
+    hyper = ch.AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True)
+    eager, graphed = make(), make()
+    for _ in range(4):
+        eager.step(hyper)
+    launches0 = nat.launch_count()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(4):
+            graphed.step(hyper)
+    captured = nat.launch_count() - launches0
+    torch.cuda.synchronize()
+    # capture performs no work: the state is still the initial one
+    assert torch.equal(graphed.chunks[0].exp_avg, torch.zeros_like(graphed.chunks[0].exp_avg))
+    g.replay()
+    torch.cuda.synchronize()
+    assert captured == 4 * (1 + len(numels))   # stats reset + one Adam launch per chunk
+    for a, b in zip(eager.chunks, graphed.chunks):
+        for x, y in ((a.master, b.master), (a.exp_avg, b.exp_avg), (a.exp_avg_sq, b.exp_avg_sq),
+                     (a.param, b.param)):
+            assert torch.equal(x.view(torch.int32) if x.dtype == torch.float32 else
+                               x.view(torch.int16),
+                               y.view(torch.int32) if y.dtype == torch.float32 else
+                               y.view(torch.int16))
+    assert eager.grad_stats() == graphed.grad_stats()
+
+
 def test_multi_rank_nccl_needs_a_communicator(cuda_device):
     _, ch = _modules()
     with pytest.raises(ValueError, match="communicator"):
