@@ -22,7 +22,7 @@ PTK_CU   := $(PKG)/csrc/ptk_kernels.cu
 PTK_CPP  := $(PKG)/csrc/ptk_host.cpp $(PKG)/csrc/ptk_comm.cpp $(PKG)/csrc/ptk_cpu_adam.cpp
 PTK_OBJS := $(OBJ)/ptk_kernels.o $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(PTK_CPP))
 
-PLAN_SRC  := model serialize packing costmodel search simulator cli
+PLAN_SRC  := model serialize packing costmodel search simulator cli accounting
 PLAN_OBJS := $(addprefix $(OBJ)/planner_,$(addsuffix .o,$(PLAN_SRC)))
 PLANFLAGS := -std=c++20 -O2 -fPIC -pthread -ffp-contract=off -Wall -Wextra -Iinclude -I$(JSON_DIR)
 

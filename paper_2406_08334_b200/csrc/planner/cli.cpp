@@ -20,6 +20,7 @@
 #include "memplan/errors.hpp"
 #include "memplan/presets.hpp"
 #include "digest.hpp"
+#include "memplan/accounting.hpp"
 
 namespace memplan {
 
@@ -206,6 +207,16 @@ std::pair<int, int> int_range(const std::string& text) {
   return {std::stoi(text.substr(0, colon)), std::stoi(text.substr(colon + 1))};
 }
 
+// B200 extension: `--chunk-bytes used` charges chunk states by their used
+// bytes (include/memplan/accounting.hpp); "reference" (default) keeps the
+// reference's 8*s_chunk / s_chunk terms and its byte-identical outputs.
+std::optional<ScopedUsedBytesAccounting> chunk_accounting(const Args& a, const ChunkLayout& layout) {
+  const std::string mode = a.str("--chunk-bytes", "reference");
+  if (mode == "reference") return std::nullopt;
+  if (mode != "used") throw UsageError("--chunk-bytes must be 'reference' or 'used'");
+  return std::optional<ScopedUsedBytesAccounting>(std::in_place, layout);
+}
+
 struct Workspace {
   ModelTrace trace;
   ChunkLayout layout;
@@ -301,6 +312,7 @@ int verb_pack(const Args& a, std::ostream& out) {
 int verb_plan(const Args& a, std::ostream& out) {
   const Workspace w = open_trace(a.str("--trace"), a.num<std::int64_t>("--s-chunk", 0));
   const HardwareProfile hw = hardware_from(a);
+  const auto accounting = chunk_accounting(a, w.layout);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
   SearchOutcome res = find_optimal(w.trace, w.layout, hw, opts);
@@ -369,6 +381,7 @@ int verb_estimate_or_simulate(const Args& a, bool simulate_it, std::ostream& out
       config.s_chunk == w.s_chunk ? w.layout : pack_chunks(w.trace, config.s_chunk);
   const BlockSchedule sched =
       build_block_schedule(config.n_block, config.n_swap, config.n_checkpoint, config.n_interval);
+  const auto accounting = chunk_accounting(a, layout);
   if (!simulate_it) {
     CostOptions opts;
     opts.alpha = a.num<double>("--alpha", 1.05);
@@ -396,6 +409,7 @@ int verb_estimate_or_simulate(const Args& a, bool simulate_it, std::ostream& out
 int verb_validate(const Args& a, std::ostream& out, std::ostream& err) {
   const Workspace w = open_trace(a.str("--trace"), a.num<std::int64_t>("--s-chunk", 0));
   const HardwareProfile hw = hardware_from(a);
+  const auto accounting = chunk_accounting(a, w.layout);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
   const auto configs = sample_feasible_configs(w.trace, w.layout, hw, a.num<int>("--samples", 50),
@@ -414,6 +428,7 @@ int verb_validate(const Args& a, std::ostream& out, std::ostream& err) {
 int verb_sweep(const Args& a, std::ostream& out) {
   const Workspace w = open_trace(a.str("--trace"), a.num<std::int64_t>("--s-chunk", 0));
   const HardwareProfile hw = hardware_from(a);
+  const auto accounting = chunk_accounting(a, w.layout);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
   const int n_chunk = w.layout.n_chunk();
@@ -504,6 +519,7 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
                                                {{"--n-buffer"}},
                                                {{"--n-swap"}},
                                                {{"--n-checkpoint"}},
+                                               {{"--chunk-bytes"}},
                                                {{"-o", "--out"}}});
   std::vector<Spec> sim_flags = est_flags;
   sim_flags.push_back({{"--timeline"}});
@@ -515,14 +531,15 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
         {{"--act-coeff"}}, {{"--spike-frac"}}, {{"--residual"}}, {{"-o", "--out"}}}},
       {"pack", {{{"--trace"}, true}, {{"--grid"}}, {{"-o", "--out"}}}},
       {"plan", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--alpha"}}, {{"--s-chunk"}},
-                        {{"--refine-sim"}}, {{"-o", "--out"}}})},
+                        {{"--refine-sim"}}, {{"--chunk-bytes"}}, {{"-o", "--out"}}})},
       {"estimate", est_flags},
       {"simulate", sim_flags},
       {"validate", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--samples"}}, {{"--seed"}},
-                            {{"--alpha"}}, {{"--s-chunk"}}, {{"-o", "--out"}}})},
+                            {{"--alpha"}}, {{"--s-chunk"}}, {{"--chunk-bytes"}},
+                            {{"-o", "--out"}}})},
       {"sweep", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--n-persist"}},
                          {{"--n-buffer"}}, {{"--n-swap"}}, {{"--n-checkpoint"}}, {{"--alpha"}},
-                         {{"--s-chunk"}}, {{"-o", "--out"}}})},
+                         {{"--s-chunk"}}, {{"--chunk-bytes"}}, {{"-o", "--out"}}})},
       {"list-presets", {}},
   };
 

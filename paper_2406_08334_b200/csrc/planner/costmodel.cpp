@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "digest.hpp"
+#include "memplan/accounting.hpp"
 #include "memplan/cost.hpp"
 #include "memplan/errors.hpp"
 
@@ -274,8 +275,7 @@ PeakMemoryBreakdown estimate_peak_memory(const ModelTrace& trace, const BlockSch
     throw InvariantViolation("schedule strategy counts disagree with config");
   PeakMemoryBreakdown out;
   out.replay_peak = detail::replay_peak(trace, schedule, config.n_swap, config.n_checkpoint);
-  out.model_state_bytes = persistent_chunk_bytes(config.s_chunk) * config.n_persist +
-                          buffer_chunk_bytes(config.s_chunk) * config.n_buffer;
+  out.model_state_bytes = device_state_bytes(config);
   out.before_alpha = out.replay_peak + out.model_state_bytes;
   out.total =
       static_cast<std::int64_t>(std::llround(opts.alpha * static_cast<double>(out.before_alpha)));

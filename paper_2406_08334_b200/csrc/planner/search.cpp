@@ -27,6 +27,7 @@
 #include <thread>
 
 #include "digest.hpp"
+#include "memplan/accounting.hpp"
 #include "memplan/errors.hpp"
 #include "memplan/search.hpp"
 #include "memplan/sim.hpp"
@@ -74,7 +75,7 @@ bool feasible_with(const PlanConfig& c, std::int64_t m_peak, const HardwareProfi
   if (m_peak >= hw.gpu_mem) return false;
   // swap-ins need one block of activation headroom on the device
   if (c.n_swap > 0 && hw.gpu_mem - m_peak < biggest_block) return false;
-  return persistent_chunk_bytes(c.s_chunk) * (c.n_chunk - c.n_persist) <= hw.cpu_mem;
+  return host_state_bytes(c) <= hw.cpu_mem;
 }
 
 // The memory-ordered candidate stream. Peaks come from one activation replay
@@ -122,8 +123,12 @@ std::vector<Candidate> candidate_stream(const ChunkLayout& layout, const ModelTr
     const int nb_lo = np == n_chunk ? 0 : std::min(3, n_chunk - np);
     const int nb_hi = np == n_chunk ? 0 : n_chunk - np;
     for (int nb = nb_lo; nb <= nb_hi; ++nb) {
-      const std::int64_t states = persistent_chunk_bytes(layout.s_chunk) * np +
-                                  buffer_chunk_bytes(layout.s_chunk) * nb;
+      PlanConfig pc;
+      pc.s_chunk = layout.s_chunk;
+      pc.n_chunk = n_chunk;
+      pc.n_persist = np;
+      pc.n_buffer = nb;
+      const std::int64_t states = device_state_bytes(pc);
       for (int ns = 0; ns <= ns_hi; ++ns) {
         const int nc_lo = ns > 1 ? (ns - 1) * n_interval : 0;
         for (int nc = nc_lo; nc <= n_block - ns; ++nc) {

@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <thread>
 
+#include "memplan/accounting.hpp"
 #include "memplan/errors.hpp"
 #include "memplan/execute.hpp"
 #include "ptk.h"
@@ -814,8 +815,7 @@ SimulationResult Runtime::iterate() {
   must(ptk_stream_synchronize(s_gpu_), "sync");
   t0_host_ = host_ns();
   // model states + residual floor
-  alloc(persistent_chunk_bytes(cfg_.s_chunk) * cfg_.n_persist +
-            buffer_chunk_bytes(cfg_.s_chunk) * cfg_.n_buffer + tr_.m_fwd,
+  alloc(device_state_bytes(cfg_) + tr_.m_fwd,
         0);
   enqueue_until(1);
   std::int64_t now = 0;

@@ -19,11 +19,12 @@ with exactly the plan the cost-model search picks from MEASURED inputs.
      estimate and the simulation, and the device peak against the model's.
 
     python scripts/train_large.py --model llama-13b --batch 8
-Writes gpurun_out/train_large_<model>_b<batch>.json.
+Writes gpurun_out/train_large_<model>_b<batch>.json (one row per --chunk-bytes mode).
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -185,6 +186,12 @@ def main():
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")
     ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
+    ap.add_argument("--chunk-bytes", default="reference,used",
+                    help="comma list of planner chunk-state accountings to plan + train with "
+                         "(reference = 8*s_chunk per persistent chunk; used = 8*used bytes)")
+    ap.add_argument("--oom-retries", type=int, default=2,
+                    help="on a device OOM, re-plan with the budget lowered by --oom-step")
+    ap.add_argument("--oom-step", type=int, default=4_000_000_000)
     args = ap.parse_args()
     from paper_2406_08334_b200 import planner, runtime
     from paper_2406_08334_b200.train import GPT2Shape
@@ -208,40 +215,58 @@ def main():
                "cpu_optim_rate": 1e9, "gpu_optim_rate": 1e11}, open(base, "w"))
     prof = os.path.join(OUT, f"profile_{tag}.json")
     hw = runtime.measure_profile(base, prof)
-    extra = ["--gpu-mem", args.gpu_mem] if args.gpu_mem else []
-    plan = memplan("plan", "--trace", tpath, "--hw", prof, *extra)
-    ppath = os.path.join(OUT, f"plan_{tag}_measured.json")
-    json.dump(plan, open(ppath, "w"), indent=1)
-    sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath)
     layout = planner.pack(tpath)
-    cfg = plan["config"]
     numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
-    pinned = 16 * sum(numels[cfg["n_persist"]:])
-    swap_act = sum(o["act_bytes"] for o in full["ops"]
-                   if o["block_id"] is not None and plan["strategies"][o["block_id"]] == "swap")
-    avail = host_available_bytes()
-    row = {"model": args.model, "batch": args.batch, "seq": shape.seq, "n_gpus": 1,
-           "params": sum(numels), "plan": cfg,
-           "strategies": "".join(s[0] for s in plan["strategies"]),
-           "cost_model_t_iter_s": plan["estimate"]["t_iter"],
-           "cost_model_m_peak_GB": plan["estimate"]["m_peak"] / 1e9,
-           "simulator_t_iter_s": sim["t_iter"], "simulator_m_peak_GB": sim["m_peak"] / 1e9,
-           "trace_fwd_s": sum(o["t_fwd"] for o in full["ops"]),
-           "trace_bwd_s": sum(o["t_bwd"] for o in full["ops"]),
-           "profile_s": round(profile_s, 1), "measured_profile": hw,
-           "pinned_host_needed_GB": (pinned + swap_act) / 1e9,
-           "host_available_GB": avail / 1e9}
-    print(json.dumps(row), flush=True)
-    if pinned + swap_act > args.host_frac * avail:
-        row["skipped"] = (f"plan needs {(pinned + swap_act) / 1e9:.1f} GB pinned host memory, "
-                          f"more than {args.host_frac} x {avail / 1e9:.1f} GB available")
-    else:
-        res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup)
-        row.update(res)
-        row["rel_err_cost_model"] = abs(res["t_iter_s"] - row["cost_model_t_iter_s"]) / res["t_iter_s"]
-        row["rel_err_simulator"] = abs(res["t_iter_s"] - row["simulator_t_iter_s"]) / res["t_iter_s"]
-    print(json.dumps(row, indent=1))
-    json.dump(row, open(os.path.join(OUT, f"train_large_{tag}.json"), "w"), indent=1)
+    common = {"model": args.model, "batch": args.batch, "seq": shape.seq, "n_gpus": 1,
+              "params": sum(numels), "trace_fwd_s": sum(o["t_fwd"] for o in full["ops"]),
+              "trace_bwd_s": sum(o["t_bwd"] for o in full["ops"]),
+              "profile_s": round(profile_s, 1), "measured_profile": hw}
+    rows = []
+    for mode in args.chunk_bytes.split(","):
+        budget = args.gpu_mem or hw["gpu_mem"]
+        attempts = []
+        for attempt in range(args.oom_retries + 1):
+            row = dict(common, chunk_bytes=mode, gpu_mem_budget=budget)
+            acct = ["--chunk-bytes", mode, "--gpu-mem", budget]
+            plan = memplan("plan", "--trace", tpath, "--hw", prof, *acct)
+            ppath = os.path.join(OUT, f"plan_{tag}_{mode}.json")
+            json.dump(plan, open(ppath, "w"), indent=1)
+            sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct)
+            cfg = plan["config"]
+            pinned = 16 * sum(numels[cfg["n_persist"]:])
+            swap_act = sum(o["act_bytes"] for o in full["ops"] if o["block_id"] is not None
+                           and plan["strategies"][o["block_id"]] == "swap")
+            avail = host_available_bytes()
+            row.update({"plan": cfg, "strategies": "".join(s[0] for s in plan["strategies"]),
+                        "cost_model_t_iter_s": plan["estimate"]["t_iter"],
+                        "cost_model_m_peak_GB": plan["estimate"]["m_peak"] / 1e9,
+                        "simulator_t_iter_s": sim["t_iter"],
+                        "simulator_m_peak_GB": sim["m_peak"] / 1e9,
+                        "pinned_host_needed_GB": (pinned + swap_act) / 1e9,
+                        "host_available_GB": avail / 1e9})
+            print(json.dumps(row), flush=True)
+            if pinned + swap_act > args.host_frac * avail:
+                row["skipped"] = (f"plan needs {(pinned + swap_act) / 1e9:.1f} GB pinned host "
+                                  f"memory, more than {args.host_frac} x {avail / 1e9:.1f} GB")
+                break
+            res = None
+            try:
+                res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup)
+            except torch.OutOfMemoryError as e:
+                attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": str(e)[:300]})
+            if res is None:   # the failed model is released with the exception
+                gc.collect()
+                torch.cuda.empty_cache()
+                budget -= args.oom_step
+                continue
+            row.update(res)
+            row["rel_err_cost_model"] = abs(res["t_iter_s"] - row["cost_model_t_iter_s"]) / res["t_iter_s"]
+            row["rel_err_simulator"] = abs(res["t_iter_s"] - row["simulator_t_iter_s"]) / res["t_iter_s"]
+            break
+        row["oom_attempts"] = attempts
+        rows.append(row)
+        print(json.dumps(row, indent=1), flush=True)
+    json.dump(rows, open(os.path.join(OUT, f"train_large_{tag}.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
