@@ -33,7 +33,11 @@ import sys
 import tempfile
 import time
 
-import torch
+# Plans fill HBM to within a few GB: let the caching allocator grow segments
+# in place instead of fragmenting (set before torch initialises CUDA).
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
+import torch  # noqa: E402
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
@@ -140,6 +144,7 @@ def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters
     y = (x + 1) % shape.vocab
     losses = []
     torch.cuda.reset_peak_memory_stats()
+    torch.cuda.reset_accumulated_memory_stats()
     for _ in range(warmup):
         losses.append(train_step(model, x, y, hyper))
     if pool is not None:
@@ -162,6 +167,9 @@ def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters
            "iters": iters, "warmup": warmup, "setup_s": round(setup_s, 1),
            "losses": [round(float(v), 4) for v in losses],
            "device_peak_allocated_GB": torch.cuda.max_memory_allocated() / 1e9,
+           "device_peak_reserved_GB": torch.cuda.max_memory_reserved() / 1e9,
+           "alloc_retries": torch.cuda.memory_stats().get("num_alloc_retries", 0),
+           "alloc_conf": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""),
            "persistent_chunk_GB": sum(16 * c.shard for c in cs.chunks) / 1e9}
     if pool is not None:
         out["pool"] = {k: (round(v, 3) if isinstance(v, float) else v)
@@ -171,8 +179,17 @@ def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters
         out["pinned_host_GB"] = pool.host_bytes / 1e9
         out["buffer_GB"] = pool.device_bytes / 1e9
     del model, cs, pool
-    torch.cuda.empty_cache()
+    release_memory()
     return out
+
+
+def release_memory() -> None:
+    """Give device memory AND pinned host memory back: torch's caching host
+    allocator keeps freed pinned blocks (the pool's shards) otherwise."""
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch._C._host_emptyCache()
 
 
 def main():
@@ -186,7 +203,7 @@ def main():
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")
     ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
-    ap.add_argument("--chunk-bytes", default="reference,used",
+    ap.add_argument("--chunk-bytes", default="used,reference",
                     help="comma list of planner chunk-state accountings to plan + train with "
                          "(reference = 8*s_chunk per persistent chunk; used = 8*used bytes)")
     ap.add_argument("--oom-retries", type=int, default=2,
@@ -223,7 +240,11 @@ def main():
               "profile_s": round(profile_s, 1), "measured_profile": hw}
     rows = []
     for mode in args.chunk_bytes.split(","):
-        budget = args.gpu_mem or hw["gpu_mem"]
+        # the device budget is what this process can still allocate (the
+        # profile's gpu_mem is the device total, incl. context + workspaces)
+        release_memory()
+        free_now = torch.cuda.mem_get_info()[0] + torch.cuda.memory_reserved()
+        budget = args.gpu_mem or min(hw["gpu_mem"], free_now)
         attempts = []
         for attempt in range(args.oom_retries + 1):
             row = dict(common, chunk_bytes=mode, gpu_mem_budget=budget)
@@ -255,8 +276,7 @@ def main():
             except torch.OutOfMemoryError as e:
                 attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": str(e)[:300]})
             if res is None:   # the failed model is released with the exception
-                gc.collect()
-                torch.cuda.empty_cache()
+                release_memory()
                 budget -= args.oom_step
                 continue
             row.update(res)
