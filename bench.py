@@ -380,7 +380,7 @@ def time_dominant_kernel(cs, hyper, stream, world, reps, use_graph=False):
             hbm += 28 * p // w
     hbm, nvl = hbm * reps, nvl * reps
     n = reps * len(cs.chunks)
-    name = ("fused_peer_kernel<W>" if cs.mode == "fused"
+    name = (nat.raw.ptk_fused_kernel_name().decode() if cs.mode == "fused"
             else "chunk_adam_tma_kernel (" + nat.raw.ptk_adam_kernel_name().decode() + ")")
     return {"kernel": name, "ms": ms, "hbm_bytes": hbm, "nvl_bytes": nvl, "launches": n,
             "world": world, "timing": "graph of back-to-back launches" if use_graph

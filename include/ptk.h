@@ -83,6 +83,8 @@ int ptk_adam_derive(const ptk_adam_config* cfg, ptk_adam_scalars* out);
 int64_t ptk_shard_elems(int64_t n, int32_t world);
 /* name of the chunk-Adam kernel shape in use (PTK_ADAM_VARIANT or default) */
 const char* ptk_adam_kernel_name(void);
+/* name of the fused RS->Adam->AG kernel in use (PTK_FUSED_KERNEL=tma|ldg, default tma) */
+const char* ptk_fused_kernel_name(void);
 /* scratch: CTA partial buffer the reducing kernels need (bytes) */
 int64_t ptk_stats_workspace_bytes(void);
 

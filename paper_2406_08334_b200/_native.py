@@ -53,6 +53,7 @@ _SIGNATURES = {
     "ptk_shard_elems": (c_int64, [c_int64, c_int32]),
     "ptk_stats_workspace_bytes": (c_int64, []),
     "ptk_adam_kernel_name": (c_char_p, []),
+    "ptk_fused_kernel_name": (c_char_p, []),
     "ptk_chunk_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),

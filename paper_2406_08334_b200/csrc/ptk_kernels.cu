@@ -609,6 +609,158 @@ fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t s
   if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
 }
 
+// The same K1+K3+K4 step through the TMA ring of chunk_adam_tma_kernel: per
+// tile of kFusedTile owned elements one elected thread bulk-loads the local
+// fp32 master/m/v tiles and the owned tile of EVERY rank's gradient chunk
+// (peer memory, NVLink on a node) into one stage, the CTA sums the W
+// gradients in fp32 in rank order (bit-identical to fused_peer_kernel and
+// the oracle), applies Adam, and the elected thread bulk-stores the state
+// locally and the bf16 tile into every rank's parameter chunk (push
+// all-gather). Bytes in flight live in shared memory, not registers.
+// Tile shape per W (elements; threads = tile / 4), measured with virtual
+// ranks (profiles/README.md): W = 2 -> 2048, W = 1, 3 -> 1536, W >= 4 -> 1024.
+// Smaller W means smaller stages; the wider tile keeps ~140-150 KB of loads
+// in flight per SM (tile 1024 at W = 2 reached only 0.66 of HBM).
+constexpr int kFusedSmemBudget = 220 * 1024;
+template <int W>
+__host__ __device__ constexpr int fused_tile() { return W == 1 ? 1536 : W == 2 ? 2048 : W == 3 ? 1536 : 1024; }
+template <int W>
+__host__ __device__ constexpr int fused_threads() { return fused_tile<W>() / 4; }
+
+template <int W>
+struct FusedStage {
+  static constexpr int kTile = fused_tile<W>();
+  float master[kTile];
+  float m[kTile];
+  float v[kTile];
+  uint16_t grad[W][kTile];
+  uint16_t param[kTile];
+};
+
+template <int W>
+constexpr int fused_stages() {
+  constexpr int s = kFusedSmemBudget / static_cast<int>(sizeof(FusedStage<W>));
+  return s > 9 ? 9 : s;
+}
+
+template <int W, int kStages>
+__global__ void __launch_bounds__(fused_threads<W>(), 1)
+fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t shard,
+                      float* __restrict__ master, float* __restrict__ exp_avg,
+                      float* __restrict__ exp_avg_sq, StatsWorkspace* ws,
+                      ptk_grad_stats_t* stats) {
+  constexpr int kFusedTile = fused_tile<W>();
+  constexpr int kFusedThr = fused_threads<W>();
+  static_assert(kStages >= 3, "ring needs >= 3 stages");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  auto* stage = reinterpret_cast<FusedStage<W>*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages];
+  const int tid = threadIdx.x;
+  const int64_t n_tiles = shard / kFusedTile;
+  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  constexpr uint32_t kLoadBytes = kFusedTile * (3 * sizeof(float) + W * sizeof(uint16_t));
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  int load_st = 0;
+  auto issue_load = [&](int64_t k) {
+    const int st = load_st;
+    load_st = load_st + 1 == kStages ? 0 : load_st + 1;
+    const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
+    FusedStage<W>& S = stage[st];
+    mbar_expect_tx(&full[st], kLoadBytes);
+    bulk_load(S.master, master + e, kFusedTile * 4, &full[st]);
+    bulk_load(S.m, exp_avg + e, kFusedTile * 4, &full[st]);
+    bulk_load(S.v, exp_avg_sq + e, kFusedTile * 4, &full[st]);
+#pragma unroll
+    for (int r = 0; r < W; ++r)
+      bulk_load(S.grad[r], peers.grad[r] + offset + e, kFusedTile * 2, &full[st]);
+  };
+  constexpr int kAhead = kStages - 2;
+  if (tid == 0)
+    for (int64_t k = 0; k < kAhead && k < my_tiles; ++k) issue_load(k);
+
+  double sq = 0.0;
+  unsigned bad = 0;
+  int st = 0;
+  uint32_t phase = 0;
+  for (int64_t k = 0; k < my_tiles; ++k) {
+    if (tid == 0 && k + kAhead < my_tiles) {
+      bulk_wait_read<1>();
+      issue_load(k + kAhead);
+    }
+    mbar_wait(&full[st], phase);
+    FusedStage<W>& S = stage[st];
+    const int e = tid * 4;
+    float4 p = *reinterpret_cast<float4*>(&S.master[e]);
+    float4 m = *reinterpret_cast<float4*>(&S.m[e]);
+    float4 v = *reinterpret_cast<float4*>(&S.v[e]);
+    uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[0][e]);
+    float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
+#pragma unroll
+    for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
+      g2 = *reinterpret_cast<const uint2*>(&S.grad[r][e]);
+      g[0] = __fadd_rn(g[0], bf_lo(g2.x));
+      g[1] = __fadd_rn(g[1], bf_hi(g2.x));
+      g[2] = __fadd_rn(g[2], bf_lo(g2.y));
+      g[3] = __fadd_rn(g[3], bf_hi(g2.y));
+    }
+    float* pp = &p.x;
+    float* mm = &m.x;
+    float* vv = &v.x;
+    float usq = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float gk = __fmul_rn(g[q], s.gscale);
+      accum_stats(gk, usq, bad);
+      adam_elem(s, gk, pp[q], mm[q], vv[q]);
+    }
+    sq += usq;
+    *reinterpret_cast<float4*>(&S.master[e]) = p;
+    *reinterpret_cast<float4*>(&S.m[e]) = m;
+    *reinterpret_cast<float4*>(&S.v[e]) = v;
+    *reinterpret_cast<uint2*>(&S.param[e]) = make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t ge = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
+      bulk_store(master + ge, S.master, kFusedTile * 4);
+      bulk_store(exp_avg + ge, S.m, kFusedTile * 4);
+      bulk_store(exp_avg_sq + ge, S.v, kFusedTile * 4);
+#pragma unroll
+      for (int r = 0; r < W; ++r) bulk_store(peers.param[r] + offset + ge, S.param, kFusedTile * 2);
+      bulk_commit();
+    }
+    if (++st == kStages) {
+      st = 0;
+      phase ^= 1u;
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+  // partial tile (< kFusedTile owned elements, a multiple of 8): last CTA
+  if (blockIdx.x == gridDim.x - 1) {
+    float usq = 0.0f;
+    for (int64_t e = n_tiles * kFusedTile + tid; e < shard; e += kFusedThr) {
+      float g = GradBf16::load1(peers.grad[0] + offset + e);
+      for (int r = 1; r < W; ++r) g = __fadd_rn(g, GradBf16::load1(peers.grad[r] + offset + e));
+      const float gk = __fmul_rn(g, s.gscale);
+      accum_stats(gk, usq, bad);
+      float p = master[e], mm = exp_avg[e], vv = exp_avg_sq[e];
+      adam_elem(s, gk, p, mm, vv);
+      master[e] = p;
+      exp_avg[e] = mm;
+      exp_avg_sq[e] = vv;
+      const uint16_t b = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
+      for (int r = 0; r < W; ++r) peers.param[r][offset + e] = b;
+    }
+    sq += usq;
+  }
+  if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
+}
+
 struct SignalTable {
   int32_t* slot[PTK_MAX_PEERS];
 };
@@ -851,13 +1003,41 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
   return check_cuda(cudaGetLastError(), "chunk_adam_kernel launch");
 }
 
+// Fused-kernel variant, once per process from PTK_FUSED_KERNEL ("tma", the
+// default, or "ldg" = the register-staged fused_peer_kernel).
+bool fused_use_tma() {
+  static const bool tma = [] {
+    const char* e = std::getenv("PTK_FUSED_KERNEL");
+    return !(e && std::string(e) == "ldg");
+  }();
+  return tma;
+}
+
 template <int W>
-void launch_fused(const ptk_adam_scalars& s, const PeerTable& t, int64_t off, int64_t shard,
-                  float* p, float* m, float* v, StatsWorkspace* ws, ptk_grad_stats_t* stats,
-                  cudaStream_t st) {
-  auto k = fused_peer_kernel<W>;
-  const int grid = grid_for(k, (shard >> 3) > 0 ? (shard >> 3) : 1);
-  k<<<grid, kThreads, 0, st>>>(s, t, off, shard, p, m, v, ws, stats);
+int launch_fused(const ptk_adam_scalars& s, const PeerTable& t, int64_t off, int64_t shard,
+                 float* p, float* m, float* v, StatsWorkspace* ws, ptk_grad_stats_t* stats,
+                 cudaStream_t st) {
+  if (!fused_use_tma()) {
+    auto k = fused_peer_kernel<W>;
+    const int grid = grid_for(k, (shard >> 3) > 0 ? (shard >> 3) : 1);
+    k<<<grid, kThreads, 0, st>>>(s, t, off, shard, p, m, v, ws, stats);
+    return PTK_OK;
+  }
+  constexpr int kSt = fused_stages<W>();
+  constexpr int kSmem = kSt * static_cast<int>(sizeof(FusedStage<W>));
+  auto k = fused_peer_tma_kernel<W, kSt>;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return check_cuda(e, "fused_peer_tma_kernel smem attribute");
+    configured = true;
+  }
+  int64_t grid = sm_count();
+  if (grid > shard / fused_tile<W>()) grid = shard / fused_tile<W>();
+  if (grid < 1) grid = 1;
+  k<<<static_cast<int>(grid), fused_threads<W>(), kSmem, st>>>(s, t, off, shard, p, m, v, ws,
+                                                                stats);
+  return PTK_OK;
 }
 
 }  // namespace
@@ -880,6 +1060,12 @@ const char* ptk_adam_kernel_name(void) {
 #undef PTK_NAME_CASE
   }
   return "?";
+}
+
+const char* ptk_fused_kernel_name(void) {
+  return fused_use_tma() ? "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3, 1024 for W>=4; "
+                           "threads = tile/4; stages = min(9, 220 KB / stage))"
+                         : "fused_peer_kernel (ldg)";
 }
 
 int ptk_chunk_adam(const ptk_adam_config* cfg, float* master, float* exp_avg, float* exp_avg_sq,
@@ -964,16 +1150,18 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
   const int64_t off = static_cast<int64_t>(rank) * shard;
   auto* ws = static_cast<StatsWorkspace*>(workspace);
   cudaStream_t st = as_stream(stream);
+  int rc = PTK_OK;
   switch (world) {
-    case 1: launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 2: launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 3: launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 4: launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 5: launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 6: launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 7: launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    default: launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 1: rc = launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 2: rc = launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 3: rc = launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 4: rc = launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 5: rc = launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 6: rc = launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 7: rc = launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    default: rc = launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
   }
+  if (rc != PTK_OK) return rc;
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "fused_peer_kernel launch");
 }

@@ -71,7 +71,8 @@ def main():
         ms = e0.elapsed_time(e1) / args.steps
         alg = p * (24 + 4 * w)
         gbs = alg / (ms * 1e-3) / 1e9
-        row = {"kernel": f"fused_peer_kernel<{w}>", "virtual_ranks": w, "chunk_params": p,
+        row = {"kernel": nat.raw.ptk_fused_kernel_name().decode() + f" W={w}",
+               "virtual_ranks": w, "chunk_params": p,
                "ms_per_step": round(ms, 4), "algorithmic_bytes_per_step": alg,
                "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 4),
                "launches_per_step": launches // args.steps,

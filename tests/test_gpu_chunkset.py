@@ -31,10 +31,17 @@ def _bf16_bits(t):
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-def test_fused_virtual_ranks_bit_exact(cuda_device, world):
+@pytest.mark.parametrize("world,numels", [(1, [10_007, 4096]), (2, [10_007, 4096]),
+                                          (3, [10_007, 4096]), (4, [10_007, 4096]),
+                                          (8, [10_007, 4096]),
+                                          # several full TMA tiles per CTA + a partial tile
+                                          (2, [2 * 148 * 1024 * 3 + 4104]),
+                                          (8, [8 * 148 * 1024 * 2 + 8 * 1000 + 40])])
+def test_fused_virtual_ranks_bit_exact(cuda_device, world, numels):
+    """The fused RS -> Adam -> AG kernel (TMA ring by default) over W virtual
+    ranks: every rank's fp32 state and every rank's gathered bf16 chunk
+    equal the oracle's rank-order fp32 reduce-scatter + Adam + all-gather."""
     nat, ch = _modules()
-    numels = [10_007, 4096]
     sets = [ch.ChunkSet(numels, world=world, rank=r, device=cuda_device, mode="fused")
             for r in range(world)]
     for cs in sets:
@@ -79,6 +86,21 @@ def test_fused_virtual_ranks_bit_exact(cuda_device, world):
         gathered = ol.allgather(params)
         for r in range(world):  # every rank holds the full gathered chunk
             np.testing.assert_array_equal(_bf16_bits(sets[r].chunks[ci].param), gathered)
+
+
+def test_fused_ldg_variant_bit_exact(cuda_device):
+    """The register-staged fused kernel (PTK_FUSED_KERNEL=ldg) passes the same
+    oracle checks (the variant is chosen once per process: child pytest)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PTK_FUSED_KERNEL="ldg")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p",
+                        "no:cacheprovider", "-k", "test_fused_virtual_ranks_bit_exact"],
+                       env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "7 passed" in r.stdout
 
 
 def _world1_comm(nat):
