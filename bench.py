@@ -573,8 +573,11 @@ def run_e2e(cs, hyper, args, world):
         cfg = hyper.config(cs.step_count, world)
         nat.lib.ptk_stats_reset(vp(cs.stats), sc)
         for c, hg, hp in zip(cs.chunks, host_g, host_p):
-            for lo in range(0, c.shard, piece):
-                n = min(piece, c.shard - lo)
+            # at least ~8 pieces per chunk so copies overlap the update even
+            # for small chunks (multiple of 12288 elements: whole TMA tiles)
+            pc = min(piece, max(1 << 20, -(-c.shard // 8 // 12288) * 12288))
+            for lo in range(0, c.shard, pc):
+                n = min(pc, c.shard - lo)
                 g_dev = c.grad_shard()[lo:lo + n]
                 p_dev = c.param_shard()[lo:lo + n]
                 e_in, e_up = torch.cuda.Event(), torch.cuda.Event()
@@ -623,7 +626,8 @@ def run_e2e(cs, hyper, args, world):
                 max(h2d_bytes / link["h2d_gbs_concurrent"],
                     d2h_bytes / link["d2h_gbs_concurrent"]) / 1e6 / ms, 3),
             "path": ("C-ABI ptk_memcpy_h2d_async -> ptk_chunk_adam -> ptk_memcpy_d2h_async, "
-                     f"pinned host buffers, {piece}-element pieces on 3 streams") if world == 1 else
+                     f"pinned host buffers, pieces of min({piece}, max(1 Mi, chunk/8)) elements "
+                     "on 3 streams") if world == 1 else
                     ("C-ABI: H2D local grad chunks -> ptk_peer_barrier -> ptk_fused_rs_adam_ag "
                      "-> ptk_peer_barrier -> D2H gathered params") if cs.mode == "fused" else
                     ("C-ABI per chunk: H2D local grad chunk -> ptk_chunk_reduce_scatter -> "
