@@ -9,7 +9,10 @@
 #include <omp.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
+#include <vector>
 
 #include "ptk_common.h"
 
@@ -88,20 +91,46 @@ extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* ex
   const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
   const bool stats = sumsq_out != nullptr || nonfinite_out != nullptr;
   const int64_t blocks = (n + kBlock - 1) / kBlock;
-  double sq = 0.0;
-  int64_t bad = 0;
-#pragma omp parallel for num_threads(threads) schedule(static) reduction(+ : sq, bad)
-  for (int64_t b = 0; b < blocks; ++b) {
+  // Per-block statistics summed in block order afterwards: the result does
+  // not depend on which thread ran which block.
+  std::vector<double> part_sq(stats ? blocks : 0);
+  std::vector<int64_t> part_bad(stats ? blocks : 0);
+  // Dynamic scheduling by default: the host Adam shares the cores with the
+  // launching threads and the copy engines' host traffic, and under that
+  // oversubscription a static split waits for its slowest (preempted) thread.
+  // PTK_CPU_ADAM_SCHEDULE=static restores the static split.
+  static const bool kStatic = [] {
+    const char* e = std::getenv("PTK_CPU_ADAM_SCHEDULE");
+    return e && std::string(e) == "static";
+  }();
+  auto body = [&](int64_t b) {
     const int64_t lo = b * kBlock, len = std::min(kBlock, n - lo);
     if (stats) {  // statistics of this block's scaled gradient (still in cache after)
+      double sq = 0.0;
+      int64_t bad = 0;
       for (int64_t i = lo; i < lo + len; ++i) {
         const float g = bf16_to_f32(grad[i]) * s.gscale;
         sq += static_cast<double>(g) * static_cast<double>(g);
         bad += std::isfinite(g) ? 0 : 1;
       }
+      part_sq[b] = sq;
+      part_bad[b] = bad;
     }
     update_block(s, master + lo, exp_avg + lo, exp_avg_sq + lo, grad + lo,
                  param_out ? param_out + lo : nullptr, len);
+  };
+  if (kStatic) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t b = 0; b < blocks; ++b) body(b);
+  } else {
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 2)
+    for (int64_t b = 0; b < blocks; ++b) body(b);
+  }
+  double sq = 0.0;
+  int64_t bad = 0;
+  for (int64_t b = 0; b < static_cast<int64_t>(part_sq.size()); ++b) {
+    sq += part_sq[b];
+    bad += part_bad[b];
   }
   if (sumsq_out) *sumsq_out = sq;
   if (nonfinite_out) *nonfinite_out = bad;

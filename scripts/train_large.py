@@ -122,8 +122,36 @@ def measured_full_trace(full: dict, shape, batch: int, k_blocks: int, dev, work:
     return {"meta": meta, "m_fwd": meas["m_fwd"], "n_blocks": full["n_blocks"], "ops": ops}
 
 
+def phase_split(model, cs, pool, x, y, hyper, iters: int) -> dict:
+    """Diagnosis only (synchronised, after the timed run): forward, backward
+    and persistent-chunk step of train_step, each bracketed by a device sync,
+    plus the host wait for pending host Adam inside forward."""
+    acc = {"fwd": 0.0, "bwd": 0.0, "step": 0.0, "host_drain_wait": 0.0}
+    for _ in range(iters):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        ev[0].record()
+        if pool is not None:
+            pool.begin_step(cs.step_count + 1, hyper, model.pool_uses())
+        loss = model.loss(x, y)
+        ev[1].record()
+        loss.backward()
+        ev[2].record()
+        cs.step(hyper)
+        ev[3].record()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if pool is not None:
+            pool.finish_step()   # host Adam still running after the device work
+        acc["host_drain_wait"] += (time.perf_counter() - t0) * 1e3 / iters
+        acc["fwd"] += ev[0].elapsed_time(ev[1]) / iters
+        acc["bwd"] += ev[1].elapsed_time(ev[2]) / iters
+        acc["step"] += ev[2].elapsed_time(ev[3]) / iters
+    return {k: round(v, 2) for k, v in acc.items()}
+
+
 def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters: int,
-                    warmup: int) -> dict:
+                    warmup: int, phases: int = 0) -> dict:
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
     from paper_2406_08334_b200.offload import ChunkPool
     from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
@@ -178,6 +206,8 @@ def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters
         out["pool"]["per_iter_d2h_GB"] = pool.counters["d2h_bytes"] / iters / 1e9
         out["pinned_host_GB"] = pool.host_bytes / 1e9
         out["buffer_GB"] = pool.device_bytes / 1e9
+    if phases:
+        out["phase_ms_synchronised"] = phase_split(model, cs, pool, x, y, hyper, phases)
     del model, cs, pool
     release_memory()
     return out
@@ -209,19 +239,28 @@ def main():
     ap.add_argument("--oom-retries", type=int, default=2,
                     help="on a device OOM, re-plan with the budget lowered by --oom-step")
     ap.add_argument("--oom-step", type=int, default=4_000_000_000)
+    ap.add_argument("--trace-in", default="", help="use this measured trace instead of profiling")
+    ap.add_argument("--profile-in", default="", help="use this HardwareProfile instead of measuring")
+    ap.add_argument("--tag", default="", help="suffix of the output file names")
+    ap.add_argument("--phases", type=int, default=2,
+                    help="after timing, this many synchronised iterations split into "
+                         "forward / backward / step / host-drain wait (diagnosis)")
     args = ap.parse_args()
     from paper_2406_08334_b200 import planner, runtime
     from paper_2406_08334_b200.train import GPT2Shape
     os.makedirs(OUT, exist_ok=True)
     dev = torch.device("cuda", 0)
-    tag = f"{args.model}_b{args.batch}"
+    tag = f"{args.model}_b{args.batch}{args.tag}"
     work = tempfile.mkdtemp(prefix="train_large_")
     full_path = planner.trace_file(["--model", args.model, "--batch", str(args.batch)],
                                    os.path.join(work, "trace_synth.json"))
     synth = json.load(open(full_path))
     shape = GPT2Shape.from_trace(synth)
     t0 = time.perf_counter()
-    full = measured_full_trace(synth, shape, args.batch, args.profile_blocks, dev, work)
+    if args.trace_in:   # reuse a measured trace (A/B runs of the runtime on one plan)
+        full = json.load(open(args.trace_in))
+    else:
+        full = measured_full_trace(synth, shape, args.batch, args.profile_blocks, dev, work)
     profile_s = time.perf_counter() - t0
     tpath = os.path.join(OUT, f"trace_{tag}_measured.json")
     json.dump(full, open(tpath, "w"), indent=1)
@@ -231,7 +270,11 @@ def main():
                "world_size": 1, "gpu_mem": 180_000_000_000, "cpu_mem": 1_000_000_000_000,
                "cpu_optim_rate": 1e9, "gpu_optim_rate": 1e11}, open(base, "w"))
     prof = os.path.join(OUT, f"profile_{tag}.json")
-    hw = runtime.measure_profile(base, prof)
+    if args.profile_in:
+        hw = json.load(open(args.profile_in))
+        json.dump(hw, open(prof, "w"))
+    else:
+        hw = runtime.measure_profile(base, prof)
     layout = planner.pack(tpath)
     numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
     common = {"model": args.model, "batch": args.batch, "seq": shape.seq, "n_gpus": 1,
@@ -272,7 +315,8 @@ def main():
                 break
             res = None
             try:
-                res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup)
+                res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup,
+                                      args.phases)
             except torch.OutOfMemoryError as e:
                 attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": str(e)[:300]})
             if res is None:   # the failed model is released with the exception
