@@ -98,6 +98,14 @@ def measured_full_trace(full: dict, shape, batch: int, k_blocks: int, dev, work:
     meas = profile_trace(model, x, (x + 1) % shape.vocab, reps=3)
     del model, cs
     torch.cuda.empty_cache()
+    return expand_trace(full, meas, k_blocks, torch.cuda.get_device_name())
+
+
+def expand_trace(full: dict, meas: dict, k_blocks: int, device: str) -> dict:
+    """Full-depth measured trace: `full`'s operators and parameter bytes, the
+    measured t_fwd / t_bwd / act_bytes / d_peak_op of `meas` (a k-block model
+    of the same shape) -- top-level operators one to one, block operators the
+    median over the profiled blocks."""
     by_kind: dict[str, list[dict]] = {}
     top: dict[str, dict] = {}
     for o in meas["ops"]:
@@ -118,7 +126,7 @@ def measured_full_trace(full: dict, shape, batch: int, k_blocks: int, dev, work:
         ops.append(dict(o, **src, d_cur_prior=0, d_peak_prior=0, d_cur_op=0))
     meta = dict(full["meta"], generator=f"profile_trace on a {k_blocks}-block model of the same "
                 "shape, block operators replicated (median over profiled blocks)",
-                timings="measured", device=torch.cuda.get_device_name())
+                timings="measured", device=device)
     return {"meta": meta, "m_fwd": meas["m_fwd"], "n_blocks": full["n_blocks"], "ops": ops}
 
 
