@@ -151,18 +151,27 @@ __device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorks
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (threadIdx.x == 0) {
+  // one warp: lane l sums partials l, l+32, ... then a fixed xor tree, so the
+  // total is the same every run (and not a 148-long serial chain of L2 loads)
+  if (threadIdx.x < 32) {
     double tsq = 0.0;
     unsigned long long tbad = 0;
     const volatile double* vsq = ws->sq;
     const volatile unsigned long long* vbad = ws->bad;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
       tsq += vsq[b];
       tbad += vbad[b];
     }
-    stats->sumsq += tsq;
-    stats->nonfinite += tbad;
-    ws->arrived = 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tsq += __shfl_xor_sync(0xffffffffu, tsq, o);
+      tbad += __shfl_xor_sync(0xffffffffu, tbad, o);
+    }
+    if (threadIdx.x == 0) {
+      stats->sumsq += tsq;
+      stats->nonfinite += tbad;
+      ws->arrived = 0;
+    }
   }
 }
 
@@ -392,10 +401,19 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
   if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
 
   const int tid = threadIdx.x;
-  // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...
-  const int64_t my_tiles =
-      n / kTile > blockIdx.x ? (n / kTile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kLoadBytes = kTile * (3 * sizeof(float) + sizeof(uint16_t));
+  // Ring items of this CTA: its full tiles blockIdx.x, blockIdx.x + gridDim.x,
+  // ...; the last CTA (which has no more full tiles than any other) also
+  // carries the partial tile -- its multiple-of-8 part as one more, shorter
+  // ring item (TMA sizes stay 16-byte multiples), so no CTA finishes with
+  // un-pipelined plain loads. The < 8 trailing elements (n % 8, never the
+  // case for padded shards) are updated with plain loads at the end.
+  const int64_t n_full = n / kTile;
+  const int64_t my_full =
+      n_full > blockIdx.x ? (n_full - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const bool has_part = blockIdx.x == gridDim.x - 1;
+  const int64_t rem = n - n_full * kTile;
+  const int rem8 = has_part ? static_cast<int>(rem & ~int64_t{7}) : 0;
+  const int64_t my_items = my_full + (rem8 > 0 ? 1 : 0);
   const bool has_param = param_out != nullptr;
 
   if (tid == 0) {
@@ -413,41 +431,57 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     if (kHint) bulk_store_hint(dst, src, bytes, policy);
     else bulk_store(dst, src, bytes);
   };
+  // item k -> (first element, length)
+  auto item = [&](int64_t k, int64_t& e, int& len) {
+    if (k < my_full) {
+      e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
+      len = kTile;
+    } else {
+      e = n_full * kTile;
+      len = rem8;
+    }
+  };
   // Ring positions are carried as (stage, phase) counters -- the pipeline
   // state of CUTLASS -- rather than k % kStages: no 64-bit division per tile,
   // and every mbarrier access is a plain [base + 8*stage] address.
   int load_st = 0;
-  auto issue_load = [&](int64_t k) {  // k-th tile of this CTA, into stage load_st
+  auto issue_load = [&](int64_t k) {  // k-th item of this CTA, into stage load_st
     const int st = load_st;
     load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
+    int64_t e;
+    int len;
+    item(k, e, len);
     TmaStage<kTile>& S = stage[st];
-    mbar_expect_tx(&full[st], kLoadBytes);
-    load(S.master, master + e, kTile * 4, &full[st]);
-    load(S.m, exp_avg + e, kTile * 4, &full[st]);
-    load(S.v, exp_avg_sq + e, kTile * 4, &full[st]);
-    load(S.grad, grad + e, kTile * 2, &full[st]);
+    mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + sizeof(uint16_t)));
+    load(S.master, master + e, len * 4, &full[st]);
+    load(S.m, exp_avg + e, len * 4, &full[st]);
+    load(S.v, exp_avg_sq + e, len * 4, &full[st]);
+    load(S.grad, grad + e, len * 2, &full[st]);
   };
 
   constexpr int kAhead = kStages - 2;
   if (tid == 0)
-    for (int64_t k = 0; k < kAhead && k < my_tiles; ++k) issue_load(k);
+    for (int64_t k = 0; k < kAhead && k < my_items; ++k) issue_load(k);
 
   double sq = 0.0;
   unsigned bad = 0;
   int st = 0;
   uint32_t phase = 0;
-  for (int64_t k = 0; k < my_tiles; ++k) {
-    if (tid == 0 && k + kAhead < my_tiles) {
-      bulk_wait_read<1>();  // the store of tile k-2 (same stage) has read its smem
+  for (int64_t k = 0; k < my_items; ++k) {
+    if (tid == 0 && k + kAhead < my_items) {
+      bulk_wait_read<1>();  // the store of item k-2 (same stage) has read its smem
       issue_load(k + kAhead);
     }
+    int64_t ge;
+    int len;
+    item(k, ge, len);
     mbar_wait(&full[st], phase);
     TmaStage<kTile>& S = stage[st];
     float usq = 0.0f;
 #pragma unroll
     for (int j = 0; j < kTile / (kThr * 4); ++j) {
       const int e = (j * kThr + tid) * 4;
+      if (e >= len) break;  // only in the partial item (len is a multiple of 8)
       float4 p = *reinterpret_cast<float4*>(&S.master[e]);
       float4 m = *reinterpret_cast<float4*>(&S.m[e]);
       float4 v = *reinterpret_cast<float4*>(&S.v[e]);
@@ -472,11 +506,10 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     __syncthreads();
     if (tid == 0) {
-      const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
-      store(master + e, S.master, kTile * 4);
-      store(exp_avg + e, S.m, kTile * 4);
-      store(exp_avg_sq + e, S.v, kTile * 4);
-      if (has_param) store(param_out + e, S.param, kTile * 2);
+      store(master + ge, S.master, len * 4);
+      store(exp_avg + ge, S.m, len * 4);
+      store(exp_avg_sq + ge, S.v, len * 4);
+      if (has_param) store(param_out + ge, S.param, len * 2);
       bulk_commit();
     }
     if (++st == kStages) {
@@ -485,11 +518,11 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     }
   }
   if (tid == 0) bulk_wait_all();
-  // The last CTA also updates the partial tile (< kTile elements) with plain
-  // loads, so a chunk is one launch whatever its size.
-  if (blockIdx.x == gridDim.x - 1) {
-    float usq = 0.0f;
-    for (int64_t e = n / kTile * kTile + tid; e < n; e += kThr) {
+  // the < 8 trailing elements of a chunk whose length is not a multiple of 8
+  if (has_part) {
+    const int64_t e = n_full * kTile + rem8 + tid;
+    if (e < n) {
+      float usq = 0.0f;
       const float gk = __fmul_rn(GradBf16::load1(grad + e), gs);
       if (kStats) accum_stats(gk, usq, bad);
       float p = master[e], mm = exp_avg[e], vv = exp_avg_sq[e];
@@ -498,8 +531,8 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
       exp_avg[e] = mm;
       exp_avg_sq[e] = vv;
       if (has_param) param_out[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
+      if (kStats) sq += usq;
     }
-    if (kStats) sq += usq;
   }
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
@@ -650,88 +683,107 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
                       float* __restrict__ exp_avg_sq, StatsWorkspace* ws,
                       ptk_grad_stats_t* stats) {
   constexpr int kFusedTile = fused_tile<W>();
-  constexpr int kFusedThr = fused_threads<W>();
   static_assert(kStages >= 3, "ring needs >= 3 stages");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<FusedStage<W>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
   const int tid = threadIdx.x;
+  // ring items: this CTA's full tiles, plus -- on the last CTA -- the partial
+  // tile (shards are multiples of 8 elements, so its TMA sizes are 16-byte
+  // multiples) as one shorter item: no un-pipelined tail
   const int64_t n_tiles = shard / kFusedTile;
-  const int64_t my_tiles = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  constexpr uint32_t kLoadBytes = kFusedTile * (3 * sizeof(float) + W * sizeof(uint16_t));
+  const int64_t my_full = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int rem = blockIdx.x == gridDim.x - 1 ? static_cast<int>(shard - n_tiles * kFusedTile) : 0;
+  const int64_t my_items = my_full + (rem > 0 ? 1 : 0);
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
+  auto item = [&](int64_t k, int64_t& e, int& len) {
+    if (k < my_full) {
+      e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
+      len = kFusedTile;
+    } else {
+      e = n_tiles * kFusedTile;
+      len = rem;
+    }
+  };
   int load_st = 0;
   auto issue_load = [&](int64_t k) {
     const int st = load_st;
     load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    const int64_t e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
+    int64_t e;
+    int len;
+    item(k, e, len);
     FusedStage<W>& S = stage[st];
-    mbar_expect_tx(&full[st], kLoadBytes);
-    bulk_load(S.master, master + e, kFusedTile * 4, &full[st]);
-    bulk_load(S.m, exp_avg + e, kFusedTile * 4, &full[st]);
-    bulk_load(S.v, exp_avg_sq + e, kFusedTile * 4, &full[st]);
+    mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + W * sizeof(uint16_t)));
+    bulk_load(S.master, master + e, len * 4, &full[st]);
+    bulk_load(S.m, exp_avg + e, len * 4, &full[st]);
+    bulk_load(S.v, exp_avg_sq + e, len * 4, &full[st]);
 #pragma unroll
     for (int r = 0; r < W; ++r)
-      bulk_load(S.grad[r], peers.grad[r] + offset + e, kFusedTile * 2, &full[st]);
+      bulk_load(S.grad[r], peers.grad[r] + offset + e, len * 2, &full[st]);
   };
   constexpr int kAhead = kStages - 2;
   if (tid == 0)
-    for (int64_t k = 0; k < kAhead && k < my_tiles; ++k) issue_load(k);
+    for (int64_t k = 0; k < kAhead && k < my_items; ++k) issue_load(k);
 
   double sq = 0.0;
   unsigned bad = 0;
   int st = 0;
   uint32_t phase = 0;
-  for (int64_t k = 0; k < my_tiles; ++k) {
-    if (tid == 0 && k + kAhead < my_tiles) {
+  for (int64_t k = 0; k < my_items; ++k) {
+    if (tid == 0 && k + kAhead < my_items) {
       bulk_wait_read<1>();
       issue_load(k + kAhead);
     }
+    int64_t ge;
+    int len;
+    item(k, ge, len);
     mbar_wait(&full[st], phase);
     FusedStage<W>& S = stage[st];
     const int e = tid * 4;
-    float4 p = *reinterpret_cast<float4*>(&S.master[e]);
-    float4 m = *reinterpret_cast<float4*>(&S.m[e]);
-    float4 v = *reinterpret_cast<float4*>(&S.v[e]);
-    uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[0][e]);
-    float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
+    if (e < len) {  // always, except in the partial item
+      float4 p = *reinterpret_cast<float4*>(&S.master[e]);
+      float4 m = *reinterpret_cast<float4*>(&S.m[e]);
+      float4 v = *reinterpret_cast<float4*>(&S.v[e]);
+      uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[0][e]);
+      float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
 #pragma unroll
-    for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
-      g2 = *reinterpret_cast<const uint2*>(&S.grad[r][e]);
-      g[0] = __fadd_rn(g[0], bf_lo(g2.x));
-      g[1] = __fadd_rn(g[1], bf_hi(g2.x));
-      g[2] = __fadd_rn(g[2], bf_lo(g2.y));
-      g[3] = __fadd_rn(g[3], bf_hi(g2.y));
-    }
-    float* pp = &p.x;
-    float* mm = &m.x;
-    float* vv = &v.x;
-    float usq = 0.0f;
+      for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
+        g2 = *reinterpret_cast<const uint2*>(&S.grad[r][e]);
+        g[0] = __fadd_rn(g[0], bf_lo(g2.x));
+        g[1] = __fadd_rn(g[1], bf_hi(g2.x));
+        g[2] = __fadd_rn(g[2], bf_lo(g2.y));
+        g[3] = __fadd_rn(g[3], bf_hi(g2.y));
+      }
+      float* pp = &p.x;
+      float* mm = &m.x;
+      float* vv = &v.x;
+      float usq = 0.0f;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float gk = __fmul_rn(g[q], s.gscale);
-      accum_stats(gk, usq, bad);
-      adam_elem(s, gk, pp[q], mm[q], vv[q]);
+      for (int q = 0; q < 4; ++q) {
+        const float gk = __fmul_rn(g[q], s.gscale);
+        accum_stats(gk, usq, bad);
+        adam_elem(s, gk, pp[q], mm[q], vv[q]);
+      }
+      sq += usq;
+      *reinterpret_cast<float4*>(&S.master[e]) = p;
+      *reinterpret_cast<float4*>(&S.m[e]) = m;
+      *reinterpret_cast<float4*>(&S.v[e]) = v;
+      *reinterpret_cast<uint2*>(&S.param[e]) =
+          make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
     }
-    sq += usq;
-    *reinterpret_cast<float4*>(&S.master[e]) = p;
-    *reinterpret_cast<float4*>(&S.m[e]) = m;
-    *reinterpret_cast<float4*>(&S.v[e]) = v;
-    *reinterpret_cast<uint2*>(&S.param[e]) = make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
-      const int64_t ge = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
-      bulk_store(master + ge, S.master, kFusedTile * 4);
-      bulk_store(exp_avg + ge, S.m, kFusedTile * 4);
-      bulk_store(exp_avg_sq + ge, S.v, kFusedTile * 4);
+      bulk_store(master + ge, S.master, len * 4);
+      bulk_store(exp_avg + ge, S.m, len * 4);
+      bulk_store(exp_avg_sq + ge, S.v, len * 4);
 #pragma unroll
-      for (int r = 0; r < W; ++r) bulk_store(peers.param[r] + offset + ge, S.param, kFusedTile * 2);
+      for (int r = 0; r < W; ++r) bulk_store(peers.param[r] + offset + ge, S.param, len * 2);
       bulk_commit();
     }
     if (++st == kStages) {
@@ -740,24 +792,6 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
     }
   }
   if (tid == 0) bulk_wait_all();
-  // partial tile (< kFusedTile owned elements, a multiple of 8): last CTA
-  if (blockIdx.x == gridDim.x - 1) {
-    float usq = 0.0f;
-    for (int64_t e = n_tiles * kFusedTile + tid; e < shard; e += kFusedThr) {
-      float g = GradBf16::load1(peers.grad[0] + offset + e);
-      for (int r = 1; r < W; ++r) g = __fadd_rn(g, GradBf16::load1(peers.grad[r] + offset + e));
-      const float gk = __fmul_rn(g, s.gscale);
-      accum_stats(gk, usq, bad);
-      float p = master[e], mm = exp_avg[e], vv = exp_avg_sq[e];
-      adam_elem(s, gk, p, mm, vv);
-      master[e] = p;
-      exp_avg[e] = mm;
-      exp_avg_sq[e] = vv;
-      const uint16_t b = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
-      for (int r = 0; r < W; ++r) peers.param[r][offset + e] = b;
-    }
-    sq += usq;
-  }
   if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
 }
 
