@@ -63,7 +63,8 @@ class DevState:
            _vp(skip_dev) if skip_dev is not None else None, s)
 
 
-@pytest.mark.parametrize("n", [1, 7, 8, 9, 255, 4096, 1_000_003, (1 << 22) + 5])
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 255, 1536, 4096, 1536 * 148, 1536 * 148 * 3 + 8,
+                               1_000_003, (1 << 22) + 5])
 @pytest.mark.parametrize("mode", ["adam", "adamw", "l2"])
 def test_chunk_adam_bit_exact(cuda_device, n, mode):
     nat = _nat()
