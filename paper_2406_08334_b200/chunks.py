@@ -144,6 +144,7 @@ class ChunkSet:
         self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)
         self.stats = torch.zeros(2, dtype=torch.float64, device=self.device)  # ptk_grad_stats_t
         self.step_count = 0
+        self.timeline = None         # timeline.Timeline: optim_start/end per chunk
         self.peer_grad_ptrs = None   # fused mode: per chunk (c_void_p * world)
         self.peer_param_ptrs = None
         self.signal_ptrs = None      # fused mode: (c_void_p * world) signal slots
@@ -232,7 +233,10 @@ class ChunkSet:
         if self.mode == "fused":
             self._step_fused(cfg, s, stats)
             return
+        tl = self.timeline
         for c in self.chunks:
+            if tl is not None:
+                tl.gpu(stream, "gpu", "optim_start", f"chunk={c.chunk_id + 1}")
             if self.comm is not None:
                 nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
             nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
@@ -240,6 +244,8 @@ class ChunkSet:
                                    c.shard, stats, vp(self.workspace), None, None, s)
             if self.comm is not None:
                 nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
+            if tl is not None:
+                tl.gpu(stream, "gpu", "optim_end", f"chunk={c.chunk_id + 1}")
 
     def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
         if not hasattr(self, "clip_coef"):

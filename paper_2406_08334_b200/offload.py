@@ -95,6 +95,7 @@ class ChunkPool:
         self.hyper = AdamHyper()
         self.step = 0
         self.counters = {"fetch": 0, "evict": 0, "h2d_bytes": 0, "d2h_bytes": 0}
+        self.timeline = None   # timeline.Timeline: events in the simulator's schema
         self._lock = threading.RLock()
         self._slot_ptr = {t.untyped_storage().data_ptr(): k for k, t in enumerate(self.slots)}
 
@@ -148,6 +149,9 @@ class ChunkPool:
             k = self.slot_of.pop(v)
             self.ready.pop(v, None)
             self.counters["evict"] += 1
+            if self.timeline is not None:
+                self.timeline.gpu(torch.cuda.current_stream(self.device), "gpu", "evict",
+                                  f"chunk={v + 1}")
             # the evicted chunk may still be read by compute already issued
             self.h2d.wait_stream(torch.cuda.current_stream(self.device))
         self.slot_of[c] = k
@@ -155,6 +159,8 @@ class ChunkPool:
         dst = self.slots[k][self.rank * s:(self.rank + 1) * s]
         done = self.piece_done.get(c) if fut is not None else None
         waited = 0.0
+        if self.timeline is not None:
+            self.timeline.gpu(self.h2d, "h2d", "upload_start", f"chunk={c + 1}")
         for i, (lo, n) in enumerate(self._pieces(c)):
             if done is not None and not done[i].is_set():
                 t0 = time.perf_counter()
@@ -169,6 +175,8 @@ class ChunkPool:
         self.counters["h2d_bytes"] += 2 * s
         if self.comm is not None:
             nat.lib.ptk_chunk_allgather(self.comm, vp(self.slots[k]), s, 0, _sh(self.h2d))
+        if self.timeline is not None:
+            self.timeline.gpu(self.h2d, "h2d", "upload_end", f"chunk={c + 1}")
         ev = torch.cuda.Event()
         ev.record(self.h2d)
         self.ready[c] = ev
@@ -217,6 +225,8 @@ class ChunkPool:
         self.d2h.wait_stream(cur)
         src = staged[self.rank * s:]
         landed = []
+        if self.timeline is not None:
+            self.timeline.gpu(self.d2h, "d2h", "offload_start", f"chunk={c + 1}")
         for lo, n in self._pieces(c):
             nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c][lo:]), vp(src[lo:]), 2 * n,
                                          _sh(self.d2h))
@@ -224,6 +234,8 @@ class ChunkPool:
             ev.record(self.d2h)
             landed.append(ev)
         staged.record_stream(self.d2h)
+        if self.timeline is not None:
+            self.timeline.gpu(self.d2h, "d2h", "offload_end", f"chunk={c + 1}")
         self.counters["d2h_bytes"] += 2 * s
         cfg = self.hyper.config(self.step, self.world)
         # the device copy is stale once the host update runs: release the slot
@@ -240,8 +252,11 @@ class ChunkPool:
 
     def _host_adam(self, c: int, landed: list, cfg) -> None:
         busy = 0.0
-        for (lo, n), ev, done in zip(self._pieces(c), landed, self.piece_done[c]):
+        tl = self.timeline
+        for i, ((lo, n), ev, done) in enumerate(zip(self._pieces(c), landed, self.piece_done[c])):
             ev.synchronize()   # this piece's gradients are in host memory
+            if i == 0 and tl is not None:
+                tl.host("cpu", "update_start", f"chunk={c + 1}")
             t0 = time.perf_counter()
             rc = nat.raw.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c][lo:]),
                                       vp(self.h_m[c][lo:]), vp(self.h_v[c][lo:]),
@@ -253,6 +268,8 @@ class ChunkPool:
                 for d in self.piece_done[c]:
                     d.set()
                 raise RuntimeError(f"ptk_cpu_adam: {nat.last_error()}")
+        if tl is not None:
+            tl.host("cpu", "update_end", f"chunk={c + 1}")
         self.counters["host_adam_s"] = self.counters.get("host_adam_s", 0.0) + busy
 
     def finish_step(self) -> None:

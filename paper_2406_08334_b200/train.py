@@ -213,6 +213,24 @@ class ChunkedGPT2:
                     (self.params if where is None else self.blocks[where])[pname] = None
         self._init_buf.clear()
 
+    timeline = None   # timeline.Timeline: per-block fwd/bwd events (simulator schema)
+
+    def _block_start(self, b: int, x: torch.Tensor) -> None:
+        tl = getattr(self, "timeline", None)
+        if tl is None:
+            return
+        tl.gpu(None, "gpu", "fwd_start", f"block={b}")
+        if x.requires_grad:  # grad of the block input ready = the block's backward done
+            x.register_hook(lambda g, b=b: tl.gpu(None, "gpu", "bwd_end", f"block={b}"))
+
+    def _block_end(self, b: int, x: torch.Tensor) -> None:
+        tl = getattr(self, "timeline", None)
+        if tl is None:
+            return
+        tl.gpu(None, "gpu", "fwd_end", f"block={b}")
+        if x.requires_grad:  # grad of the block output ready = its backward starts
+            x.register_hook(lambda g, b=b: tl.gpu(None, "gpu", "bwd_start", f"block={b}"))
+
     def _strategies(self) -> list[str]:
         return getattr(self, "strategies", None) or ["none"] * self.shape.blocks
 
@@ -268,16 +286,25 @@ class ChunkedGPT2:
 
         ensure(self.wte_chunk)
         x = embed(sh, params, tokens)
-        for blk_id, strategy in enumerate(self._strategies()):
+        strategies = self._strategies()
+        swap_blocks = [b for b, st in enumerate(strategies) if st == "swap"]
+        for blk_id, strategy in enumerate(strategies):
             if strategy == "checkpoint":
+                self._block_start(blk_id, x)
                 x = torch.utils.checkpoint.checkpoint(checkpointed(blk_id), x, use_reentrant=False)
-                continue
-            ensure(self.block_chunk[blk_id])
-            if strategy == "swap":
-                with torch.autograd.graph.saved_tensors_hooks(self._swap.pack, self._swap.unpack):
-                    x = block_forward(sh, blocks[blk_id], x)
             else:
-                x = block_forward(sh, blocks[blk_id], x)
+                ensure(self.block_chunk[blk_id])
+                self._block_start(blk_id, x)
+                if strategy == "swap":
+                    self._swap.begin_block(blk_id)
+                    with torch.autograd.graph.saved_tensors_hooks(self._swap.pack,
+                                                                  self._swap.unpack):
+                        x = block_forward(sh, blocks[blk_id], x)
+                else:
+                    x = block_forward(sh, blocks[blk_id], x)
+            self._block_end(blk_id, x)
+            if swap_blocks:
+                self._swap.prefetch_hooks(swap_blocks, blk_id, x, blk_id == len(strategies) - 1)
         if sh.tied and self.wte_chunk in self.pool_specs:  # tied head: another use of chunk 0
             gather_into(self.wte_chunk, pool.n_total, None, params, blocks)
         elif not sh.tied:
@@ -304,14 +331,20 @@ class ChunkedGPT2:
         sh = self.shape
         x = embed(sh, self.params, tokens)
         strategies = getattr(self, "strategies", None) or ["none"] * len(self.blocks)
-        for blk, strategy in zip(self.blocks, strategies):
+        swap_blocks = [b for b, st in enumerate(strategies) if st == "swap"]
+        for b, (blk, strategy) in enumerate(zip(self.blocks, strategies)):
+            ChunkedGPT2._block_start(self, b, x)   # (tests call loss on a plain namespace)
             if strategy == "checkpoint":
                 x = torch.utils.checkpoint.checkpoint(block_forward, sh, blk, x, use_reentrant=False)
             elif strategy == "swap":
+                self._swap.begin_block(b)
                 with torch.autograd.graph.saved_tensors_hooks(self._swap.pack, self._swap.unpack):
                     x = block_forward(sh, blk, x)
             else:
                 x = block_forward(sh, blk, x)
+            ChunkedGPT2._block_end(self, b, x)
+            if swap_blocks:
+                self._swap.prefetch_hooks(swap_blocks, b, x, b == len(strategies) - 1)
         return head_loss(sh, self.params, x, targets)
 
 
@@ -397,15 +430,29 @@ class ActivationSwap:
     """saved_tensors_hooks for Swap blocks: each saved activation is copied to
     pinned host memory on a side stream (swap-out overlapping the forward),
     its device memory released to the allocator once that copy is done
-    (record_stream), and copied back on the side stream when backward needs
-    it (swap-in), the compute stream waiting only on that copy. Tensors that
-    live in the chunk buffers (parameters) are never swapped; parameters of
-    non-persistent chunks (pool slots) are handed to the pool's own hooks."""
+    (record_stream). In backward the block's activations come back ahead of
+    need: `prefetch(b)` -- fired by a gradient hook when backward reaches
+    block b + `lead` -- issues all of block b's H2D copies on the side stream,
+    so by the time autograd unpacks them the compute stream only waits on
+    their events (the simulator's swap-in before the block's backward,
+    proj/src/sim.cpp:411-425). A tensor unpacked before its prefetch is copied
+    on demand. Tensors that live in the chunk buffers (parameters) are never
+    swapped; parameters of non-persistent chunks (pool slots) are handed to
+    the pool's own hooks."""
+
+    lead = 2   # prefetch block b when the backward of block b + lead starts
 
     def __init__(self, param_storages: set[int], pool=None):
         self.params = param_storages
         self.pool = pool
         self.side = torch.cuda.Stream()
+        self.block = None
+        self.saved: dict[int, list[dict]] = {}
+        self.timeline = None
+
+    def begin_block(self, b: int) -> None:
+        self.block = b
+        self.saved[b] = []
 
     def pack(self, t: torch.Tensor):
         if self.pool is not None and t.untyped_storage().data_ptr() in self.pool._slot_ptr:
@@ -418,21 +465,55 @@ class ActivationSwap:
             host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             host.copy_(t, non_blocking=True)
         t.record_stream(self.side)
-        return ("swap", host, t.device)
+        entry = {"host": host, "device": t.device, "dev": None, "ev": None}
+        self.saved.setdefault(self.block, []).append(entry)
+        return ("swap", entry)
+
+    def _fetch(self, entry: dict) -> None:
+        with torch.cuda.stream(self.side):
+            entry["dev"] = entry["host"].to(entry["device"], non_blocking=True)
+            entry["ev"] = torch.cuda.Event()
+            entry["ev"].record(self.side)
+
+    def prefetch(self, b: int) -> None:
+        entries = self.saved.pop(b, [])
+        if not entries:
+            return
+        self.side.wait_stream(torch.cuda.current_stream())
+        tl = self.timeline
+        if tl is not None:
+            tl.gpu(self.side, "h2d", "swap_in_start", f"block={b}")
+        for entry in entries:
+            if entry["dev"] is None:
+                self._fetch(entry)
+        if tl is not None:
+            tl.gpu(self.side, "h2d", "swap_in_end", f"block={b}")
 
     def unpack(self, packed):
         if packed[0] == "keep":
             return packed[1]
         if packed[0] == "pool":
             return self.pool.unpack(packed[1])
-        _, host, device = packed
+        entry = packed[1]
         cur = torch.cuda.current_stream()
-        self.side.wait_stream(cur)
-        with torch.cuda.stream(self.side):
-            dev = host.to(device, non_blocking=True)
-        cur.wait_stream(self.side)
+        if entry["dev"] is None:   # not prefetched: copy now
+            self.side.wait_stream(cur)
+            self._fetch(entry)
+        cur.wait_event(entry["ev"])
+        dev = entry["dev"]
         dev.record_stream(cur)
         return dev
+
+    def prefetch_hooks(self, swap_blocks: list[int], j: int, x: torch.Tensor,
+                       last: bool) -> None:
+        """Called with the output x of block j: its gradient hook prefetches
+        every swap block b with b + lead == j (or b + lead beyond the last
+        block, on the last block's output)."""
+        if not x.requires_grad:
+            return
+        due = [b for b in swap_blocks if b + self.lead == j or (last and b + self.lead > j)]
+        if due:
+            x.register_hook(lambda g, due=tuple(due): [self.prefetch(b) for b in due] and None)
 
 
 def _stash_into(slot: torch.Tensor):

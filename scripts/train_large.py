@@ -158,8 +158,33 @@ def phase_split(model, cs, pool, x, y, hyper, iters: int) -> dict:
     return {k: round(v, 2) for k, v in acc.items()}
 
 
+def record_timeline(model, cs, pool, x, y, hyper, path: str) -> dict:
+    """One more iteration with the measured timeline on (simulator schema,
+    paper_2406_08334_b200.timeline), written as CSV; returns its summary."""
+    from paper_2406_08334_b200.timeline import Timeline, summarize, write_csv
+    from paper_2406_08334_b200.train import train_step
+    tl = Timeline()
+    model.timeline = cs.timeline = tl
+    if pool is not None:
+        pool.timeline = tl
+    if getattr(model, "_swap", None) is not None:
+        model._swap.timeline = tl
+    tl.begin()
+    train_step(model, x, y, hyper)
+    if pool is not None:
+        pool.finish_step()
+    rows = tl.end()
+    model.timeline = cs.timeline = None
+    if pool is not None:
+        pool.timeline = None
+    if getattr(model, "_swap", None) is not None:
+        model._swap.timeline = None
+    write_csv(rows, path)
+    return summarize(rows)
+
+
 def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters: int,
-                    warmup: int, phases: int = 0) -> dict:
+                    warmup: int, phases: int = 0, timeline_path: str = "") -> dict:
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
     from paper_2406_08334_b200.offload import ChunkPool
     from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
@@ -216,6 +241,9 @@ def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters
         out["buffer_GB"] = pool.device_bytes / 1e9
     if phases:
         out["phase_ms_synchronised"] = phase_split(model, cs, pool, x, y, hyper, phases)
+    if timeline_path:
+        out["timeline"] = {"csv": os.path.basename(timeline_path),
+                           **record_timeline(model, cs, pool, x, y, hyper, timeline_path)}
     del model, cs, pool
     release_memory()
     return out
@@ -250,6 +278,9 @@ def main():
     ap.add_argument("--trace-in", default="", help="use this measured trace instead of profiling")
     ap.add_argument("--profile-in", default="", help="use this HardwareProfile instead of measuring")
     ap.add_argument("--tag", default="", help="suffix of the output file names")
+    ap.add_argument("--timeline", action="store_true",
+                    help="record one more iteration's measured timeline (simulator schema) and "
+                         "summarise it beside the simulator's timeline of the same plan")
     ap.add_argument("--phases", type=int, default=2,
                     help="after timing, this many synchronised iterations split into "
                          "forward / backward / step / host-drain wait (diagnosis)")
@@ -303,7 +334,9 @@ def main():
             plan = memplan("plan", "--trace", tpath, "--hw", prof, *acct)
             ppath = os.path.join(OUT, f"plan_{tag}_{mode}.json")
             json.dump(plan, open(ppath, "w"), indent=1)
-            sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct)
+            sim_tl = os.path.join(OUT, f"sim_timeline_{tag}_{mode}.csv")
+            sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct,
+                          "--timeline-csv", sim_tl)
             cfg = plan["config"]
             pinned = 16 * sum(numels[cfg["n_persist"]:])
             swap_act = sum(o["act_bytes"] for o in full["ops"] if o["block_id"] is not None
@@ -323,8 +356,9 @@ def main():
                 break
             res = None
             try:
+                tl_path = os.path.join(OUT, f"timeline_{tag}_{mode}.csv") if args.timeline else ""
                 res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup,
-                                      args.phases)
+                                      args.phases, tl_path)
             except torch.OutOfMemoryError as e:
                 attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": str(e)[:300]})
             if res is None:   # the failed model is released with the exception
@@ -332,6 +366,10 @@ def main():
                 budget -= args.oom_step
                 continue
             row.update(res)
+            if args.timeline:
+                from paper_2406_08334_b200.timeline import read_csv, summarize
+                row["simulated_timeline"] = {"csv": os.path.basename(sim_tl),
+                                             **summarize(read_csv(sim_tl))}
             row["rel_err_cost_model"] = abs(res["t_iter_s"] - row["cost_model_t_iter_s"]) / res["t_iter_s"]
             row["rel_err_simulator"] = abs(res["t_iter_s"] - row["simulator_t_iter_s"]) / res["t_iter_s"]
             break

@@ -265,3 +265,52 @@ def test_chunked_parameters_are_chunk_views(tmp_path, cuda_device):
     assert wpe.data_ptr() == c0.param.data_ptr() + 2 * wte.numel()
     blk1 = model.chunks.chunks[2]
     assert model.blocks[1]["ln1_w"].data_ptr() == blk1.param.data_ptr()
+
+
+def test_training_timeline_in_simulator_schema(tmp_path, cuda_device):
+    """The measured timeline of one training iteration (paper_2406_08334_b200
+    .timeline) has the simulator's schema: per block fwd/bwd start/end in
+    order, one upload / offload / host update per pooled chunk, one device
+    optim per persistent chunk; the CSV round-trips and summarises."""
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.timeline import Timeline, read_csv, summarize, write_csv
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    spec = tmp_path / "spec.json"
+    spec.write_text(json.dumps({"hidden_size": 256, "n_blocks": 2, "n_heads": 4,
+                                "vocab_size": 1000, "seq_len": 128}))
+    tpath = planner.trace_file(["--spec", str(spec), "--batch", "4"], str(tmp_path / "t.json"))
+    trace = json.load(open(tpath))
+    layout = planner.pack(tpath, grid="2Mi")
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    cs = ChunkSet(numels[:1], device=cuda_device)
+    pool = ChunkPool(numels, 1, 1, device=cuda_device)
+    model = ChunkedGPT2(GPT2Shape.from_trace(trace), layout, cs, trace["ops"], pool=pool)
+    model.init_weights(0)
+    model.set_block_schedule(["checkpoint", "swap"])
+    x = torch.randint(0, 1000, (4, 128), device=cuda_device)
+    for _ in range(2):
+        train_step(model, x, (x + 1) % 1000, AdamHyper())
+    pool.finish_step()
+    tl = Timeline()
+    model.timeline = cs.timeline = pool.timeline = tl
+    tl.begin()
+    train_step(model, x, (x + 1) % 1000, AdamHyper())
+    pool.finish_step()
+    rows = tl.end()
+    ev = [(r, e, s) for _, r, e, s in rows]
+    for b in range(2):
+        assert ("gpu", "fwd_start", f"block={b}") in ev and ("gpu", "bwd_end", f"block={b}") in ev
+    t = {(e, s): ns for ns, _, e, s in rows}
+    assert t[("fwd_end", "block=1")] <= t[("bwd_start", "block=1")] <= t[("bwd_end", "block=0")]
+    for c in (2, 3):   # pooled chunks (1-based): fetched, drained, updated on the host
+        assert sum(1 for r in ev if r == ("h2d", "upload_start", f"chunk={c}")) >= 1
+        assert ("d2h", "offload_end", f"chunk={c}") in ev
+        assert ("cpu", "update_end", f"chunk={c}") in ev
+    assert ("gpu", "optim_end", "chunk=1") in ev
+    path = str(tmp_path / "tl.csv")
+    write_csv(rows, path)
+    assert read_csv(path) == rows
+    summ = summarize(rows)
+    assert summ["bwd_end_ns"] >= summ["fwd_end_ns"] > 0 and summ["busy_ns"]["cpu"] > 0
