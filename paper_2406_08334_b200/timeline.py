@@ -86,6 +86,36 @@ def read_csv(path: str) -> list[tuple[int, str, str, str]]:
                 for r in csv.DictReader(f)]
 
 
+def last_iteration(rows) -> list[tuple[int, str, str, str]]:
+    """The rows of the last recorded iteration (from its `iter_start` event),
+    re-based to start at 0. Intervals still open from the previous iteration
+    (e.g. its host Adam) are kept from 0 with " prev" appended to the subject."""
+    starts = [ns for ns, _, e, _ in rows if e == "iter_start"]
+    if not starts:
+        return [r for r in rows if r[2] != "iter_start"]
+    last = max(starts)
+    opened = set()
+    for ns, resource, event, subject in rows:
+        if ns >= last:
+            break
+        if event == "iter_start":
+            continue
+        if event.endswith("_start"):
+            opened.add((resource, event[:-6], subject))
+        elif event.endswith("_end"):
+            opened.discard((resource, event[:-4], subject))
+    out = [(0, r, k + "_start", s + " prev") for r, k, s in sorted(opened)]
+    carried = set(opened)
+    for ns, resource, event, subject in rows:
+        if ns < last or event == "iter_start":
+            continue
+        if event.endswith("_end") and (resource, event[:-4], subject) in carried:
+            carried.discard((resource, event[:-4], subject))
+            subject += " prev"
+        out.append((ns - last, resource, event, subject))
+    return out
+
+
 def summarize(rows) -> dict:
     """Per-resource busy time (union of start/end intervals), the end of the
     last forward / backward compute event, and per-chunk start times of

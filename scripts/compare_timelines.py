@@ -53,6 +53,8 @@ def intervals(rows, per_op: bool):
             if mc is None:
                 continue
             key = int(mc.group(1))
+            if subject.endswith(" prev"):
+                kind += "(prev)"
         k = (kind, key)
         if edge == "start":
             if k not in out:
@@ -68,12 +70,17 @@ def intervals(rows, per_op: bool):
 
 
 def main():
-    from paper_2406_08334_b200.timeline import read_csv
+    from paper_2406_08334_b200.timeline import last_iteration, read_csv
     ap = argparse.ArgumentParser()
     ap.add_argument("real")
     ap.add_argument("sim")
     args = ap.parse_args()
     real, sim = read_csv(args.real), read_csv(args.sim)
+    starts = [ns for ns, _, e, _ in real if e == "iter_start"]
+    if starts:   # several recorded iterations: compare the last (steady state)
+        print(f"{len(starts)} recorded iterations, comparing the last "
+              f"(starts at {max(starts) / 1e6:.1f} ms); 'prev' = carried over from the one before")
+    real = last_iteration(real)
     r, s = intervals(real, per_op=False), intervals(sim, per_op=True)
     ms = lambda ns: ns / 1e6  # noqa: E731
     print(f"iteration end: real {ms(max(t for t, *_ in real)):.1f} ms, "
@@ -87,11 +94,11 @@ def main():
                 iv = src.get((kind, b))
                 cells.append(f"{ms(iv[0]):8.1f}-{ms(iv[1]):8.1f}" if iv else " " * 17)
         print(f"{b:5d} | " + " | ".join(cells))
-    chunks = sorted({k for kind, k in list(r) + list(s) if kind in ("upload", "offload",
-                                                                     "update", "optim")})
+    chunks = sorted({k for kind, k in list(r) + list(s) if kind in ("upload", "offload", "update",
+                                                                     "optim", "update(prev)")})
     print("\nchunk | kind    | real (ms)           | simulated")
     for c in chunks:
-        for kind in ("upload", "offload", "update", "optim"):
+        for kind in ("update(prev)", "upload", "offload", "update", "optim"):
             a, b = r.get((kind, c)), s.get((kind, c))
             if a is None and b is None:
                 continue

@@ -158,9 +158,11 @@ def phase_split(model, cs, pool, x, y, hyper, iters: int) -> dict:
     return {k: round(v, 2) for k, v in acc.items()}
 
 
-def record_timeline(model, cs, pool, x, y, hyper, path: str) -> dict:
-    """One more iteration with the measured timeline on (simulator schema,
-    paper_2406_08334_b200.timeline), written as CSV; returns its summary."""
+def record_timeline(model, cs, pool, x, y, hyper, path: str, iters: int = 2) -> dict:
+    """`iters` more back-to-back iterations with the measured timeline on
+    (simulator schema, paper_2406_08334_b200.timeline; an `iter_start` event
+    marks each), written as CSV; returns the summary of the LAST one (steady
+    state: the previous iteration's host Adam overlaps it, as in training)."""
     from paper_2406_08334_b200.timeline import Timeline, summarize, write_csv
     from paper_2406_08334_b200.train import train_step
     tl = Timeline()
@@ -170,7 +172,9 @@ def record_timeline(model, cs, pool, x, y, hyper, path: str) -> dict:
     if getattr(model, "_swap", None) is not None:
         model._swap.timeline = tl
     tl.begin()
-    train_step(model, x, y, hyper)
+    for i in range(iters):
+        tl.gpu(None, "gpu", "iter_start", f"iter={i}")
+        train_step(model, x, y, hyper)
     if pool is not None:
         pool.finish_step()
     rows = tl.end()
@@ -180,7 +184,8 @@ def record_timeline(model, cs, pool, x, y, hyper, path: str) -> dict:
     if getattr(model, "_swap", None) is not None:
         model._swap.timeline = None
     write_csv(rows, path)
-    return summarize(rows)
+    from paper_2406_08334_b200.timeline import last_iteration
+    return {"iterations": iters, "last_iteration": summarize(last_iteration(rows))}
 
 
 def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters: int,
