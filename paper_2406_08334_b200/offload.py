@@ -205,7 +205,8 @@ class ChunkPool:
         self.partial.clear()
 
     def add_grad(self, c: int, flat: torch.Tensor) -> None:
-        """Gradient of one use of chunk c (flat bf16, numel[c] elements)."""
+        """Gradient of one use of chunk c (flat bf16, shard*world elements:
+        the chunk's parameters first, zero padding after)."""
         with self._lock:
             if c in self.partial:
                 self.partial[c] += flat
@@ -218,8 +219,7 @@ class ChunkPool:
     def _drain(self, c: int, grad: torch.Tensor) -> None:
         s = self.shard[c]
         cur = torch.cuda.current_stream(self.device)
-        staged = torch.zeros(s * self.world, dtype=BF16, device=self.device)
-        staged[: grad.numel()] = grad
+        staged = grad   # already padded to shard*world: reduce-scatter / D2H in place
         if self.comm is not None:
             nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
         self.d2h.wait_stream(cur)
@@ -313,7 +313,7 @@ class ChunkGather(torch.autograd.Function):
     @staticmethod
     def backward(ctx, *grads):
         pool, c = ctx.pool, ctx.c
-        flat = torch.zeros(pool.numel[c], dtype=BF16, device=pool.device)
+        flat = torch.zeros(pool.shard[c] * pool.world, dtype=BF16, device=pool.device)
         for (lo, shape), g in zip(ctx.specs, grads):
             if g is not None:
                 flat[lo:lo + g.numel()] = g.reshape(-1)

@@ -528,9 +528,17 @@ def train_step(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
     """One iteration; returns the (device) loss. Gradient slots of the chunk
     buffers are fully overwritten by the hooks each step (padding stays 0)."""
     pool = getattr(model, "pool", None)
+    tl = model.timeline
     if pool is not None:
         pool.begin_step(model.chunks.step_count + 1, hyper, model.pool_uses())
+    if tl is not None:
+        tl.host("host", "forward_call_start", "")
     loss = model.loss(tokens, targets)
+    if tl is not None:
+        tl.host("host", "forward_call_end", "")
+        tl.gpu(None, "gpu", "loss_ready", "")
     loss.backward()
+    if tl is not None:
+        tl.host("host", "backward_call_end", "")
     model.chunks.step(hyper)  # persistent chunks; pooled chunks drained during backward
     return loss.detach()

@@ -274,6 +274,9 @@ def main():
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")
     ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
+    ap.add_argument("--gpu-mem-margin", type=int, default=6_000_000_000,
+                    help="bytes kept free below the allocatable device memory for the "
+                         "caching allocator's slack (ignored with --gpu-mem)")
     ap.add_argument("--chunk-bytes", default="used,reference",
                     help="comma list of planner chunk-state accountings to plan + train with "
                          "(reference = 8*s_chunk per persistent chunk; used = 8*used bytes)")
@@ -331,7 +334,10 @@ def main():
         # profile's gpu_mem is the device total, incl. context + workspaces)
         release_memory()
         free_now = torch.cuda.mem_get_info()[0] + torch.cuda.memory_reserved()
-        budget = args.gpu_mem or min(hw["gpu_mem"], free_now)
+        # minus the caching allocator's slack: plans that fill HBM to the last
+        # GB made it flush its cache mid-iteration (alloc retries, ~1 s stalls
+        # seen in the measured timeline)
+        budget = args.gpu_mem or min(hw["gpu_mem"], free_now) - args.gpu_mem_margin
         attempts = []
         for attempt in range(args.oom_retries + 1):
             row = dict(common, chunk_bytes=mode, gpu_mem_budget=budget)
