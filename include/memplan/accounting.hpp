@@ -44,3 +44,31 @@ class ScopedUsedBytesAccounting {
 };
 
 }  // namespace memplan
+
+namespace memplan {
+
+// B200 extension: host-memory bandwidth shared by the host optimizer and the
+// PCIe copies (opt-in; `memplan simulate|plan|validate --host-mem-bw B`).
+// The reference's simulator gives the host Adam its own rate and the h2d/d2h
+// links their own bandwidth (proj/src/sim.cpp:25-81,552-562); on a real host
+// all three stream through the same DRAM. With bw > 0 every consumer that is
+// active at a moment demands its nominal rate -- the host Adam
+// cpu_bytes_per_param * cpu_optim_rate, an active h2d link h2d_bw, an active
+// d2h link d2h_bw -- and when the sum exceeds bw all of them are slowed by the
+// same factor bw / demand. bw == 0 (the default) is the reference model.
+struct HostMemoryModel {
+  double bw = 0.0;                  // bytes/s; 0 = off
+  double cpu_bytes_per_param = 28;  // host Adam: fp32 master/m/v read+write, bf16 grad in, param out
+};
+
+const HostMemoryModel& host_memory_model();
+
+class ScopedHostMemoryModel {
+ public:
+  explicit ScopedHostMemoryModel(double bw, double cpu_bytes_per_param = 28.0);
+  ~ScopedHostMemoryModel();
+  ScopedHostMemoryModel(const ScopedHostMemoryModel&) = delete;
+  ScopedHostMemoryModel& operator=(const ScopedHostMemoryModel&) = delete;
+};
+
+}  // namespace memplan

@@ -241,6 +241,12 @@ int ptk_profile_collective(ptk_comm* comm, int32_t world, int64_t chunk_bytes, d
                            double* bw);
 int ptk_profile_gpu_adam_rate(int64_t n, double* params_per_s);
 int ptk_profile_cpu_adam_rate(int64_t n, double* params_per_s);
+/* Host-memory bandwidth shared by the host Adam and PCIe copies (the
+ * simulator extension's --host-mem-bw): the host Adam over n params on
+ * `threads` threads (<= 0: cores - 2, the ChunkPool default) runs for about
+ * `seconds` while pinned H2D + D2H copies loop; returns
+ * (28 * params updated + bytes copied) / elapsed. Host-synchronising. */
+int ptk_profile_host_memory_bw(int64_t n, int32_t threads, double seconds, double* bytes_per_s);
 
 /* ---- streams / events / timing helpers used by the host runtime ------- */
 int ptk_stream_create(void** out, int32_t high_priority);

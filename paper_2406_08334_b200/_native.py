@@ -54,6 +54,7 @@ _SIGNATURES = {
     "ptk_stats_workspace_bytes": (c_int64, []),
     "ptk_adam_kernel_name": (c_char_p, []),
     "ptk_fused_kernel_name": (c_char_p, []),
+    "ptk_profile_host_memory_bw": (c_int32, [c_int64, c_int32, c_double, POINTER(c_double)]),
     "ptk_chunk_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),

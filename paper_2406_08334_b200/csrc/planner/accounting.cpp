@@ -73,3 +73,25 @@ ScopedUsedBytesAccounting::~ScopedUsedBytesAccounting() {
 }
 
 }  // namespace memplan
+
+namespace memplan {
+
+namespace {
+HostMemoryModel& host_model() {
+  static HostMemoryModel m;
+  return m;
+}
+}  // namespace
+
+const HostMemoryModel& host_memory_model() { return host_model(); }
+
+ScopedHostMemoryModel::ScopedHostMemoryModel(double bw, double cpu_bytes_per_param) {
+  if (!(bw > 0.0) || !(cpu_bytes_per_param > 0.0))
+    throw InvariantViolation("host memory model needs bw > 0 and bytes per param > 0");
+  if (host_model().bw > 0.0) throw InvariantViolation("host memory model is already active");
+  host_model() = HostMemoryModel{bw, cpu_bytes_per_param};
+}
+
+ScopedHostMemoryModel::~ScopedHostMemoryModel() { host_model() = HostMemoryModel{}; }
+
+}  // namespace memplan

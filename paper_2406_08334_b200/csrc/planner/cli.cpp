@@ -217,6 +217,16 @@ std::optional<ScopedUsedBytesAccounting> chunk_accounting(const Args& a, const C
   return std::optional<ScopedUsedBytesAccounting>(std::in_place, layout);
 }
 
+// B200 extension: `--host-mem-bw B` (bytes/s) makes the simulator share host
+// DRAM between the host Adam and the PCIe copies (include/memplan/accounting.hpp);
+// absent, the simulation is the reference's.
+std::optional<ScopedHostMemoryModel> host_memory(const Args& a) {
+  if (!a.has("--host-mem-bw")) return std::nullopt;
+  const double bw = a.num<double>("--host-mem-bw", 0.0);
+  if (!(bw > 0.0)) throw UsageError("--host-mem-bw must be > 0");
+  return std::optional<ScopedHostMemoryModel>(std::in_place, bw);
+}
+
 struct Workspace {
   ModelTrace trace;
   ChunkLayout layout;
@@ -313,6 +323,7 @@ int verb_plan(const Args& a, std::ostream& out) {
   const Workspace w = open_trace(a.str("--trace"), a.num<std::int64_t>("--s-chunk", 0));
   const HardwareProfile hw = hardware_from(a);
   const auto accounting = chunk_accounting(a, w.layout);
+  const auto hostmem = host_memory(a);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
   SearchOutcome res = find_optimal(w.trace, w.layout, hw, opts);
@@ -382,6 +393,7 @@ int verb_estimate_or_simulate(const Args& a, bool simulate_it, std::ostream& out
   const BlockSchedule sched =
       build_block_schedule(config.n_block, config.n_swap, config.n_checkpoint, config.n_interval);
   const auto accounting = chunk_accounting(a, layout);
+  const auto hostmem = simulate_it ? host_memory(a) : std::nullopt;
   if (!simulate_it) {
     CostOptions opts;
     opts.alpha = a.num<double>("--alpha", 1.05);
@@ -410,6 +422,7 @@ int verb_validate(const Args& a, std::ostream& out, std::ostream& err) {
   const Workspace w = open_trace(a.str("--trace"), a.num<std::int64_t>("--s-chunk", 0));
   const HardwareProfile hw = hardware_from(a);
   const auto accounting = chunk_accounting(a, w.layout);
+  const auto hostmem = host_memory(a);
   CostOptions opts;
   opts.alpha = a.num<double>("--alpha", 1.05);
   const auto configs = sample_feasible_configs(w.trace, w.layout, hw, a.num<int>("--samples", 50),
@@ -523,6 +536,7 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
                                                {{"-o", "--out"}}});
   std::vector<Spec> sim_flags = est_flags;
   sim_flags.push_back({{"--timeline"}});
+  sim_flags.push_back({{"--host-mem-bw"}});
   sim_flags.push_back({{"--timeline-csv"}});
   sim_flags.push_back({{"--mem-trace"}});
   const std::map<std::string, std::vector<Spec>> verbs = {
@@ -531,12 +545,13 @@ int run_cli(const std::vector<std::string>& args, std::ostream& out, std::ostrea
         {{"--act-coeff"}}, {{"--spike-frac"}}, {{"--residual"}}, {{"-o", "--out"}}}},
       {"pack", {{{"--trace"}, true}, {{"--grid"}}, {{"-o", "--out"}}}},
       {"plan", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--alpha"}}, {{"--s-chunk"}},
-                        {{"--refine-sim"}}, {{"--chunk-bytes"}}, {{"-o", "--out"}}})},
+                        {{"--refine-sim"}}, {{"--chunk-bytes"}}, {{"--host-mem-bw"}},
+                        {{"-o", "--out"}}})},
       {"estimate", est_flags},
       {"simulate", sim_flags},
       {"validate", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--samples"}}, {{"--seed"}},
                             {{"--alpha"}}, {{"--s-chunk"}}, {{"--chunk-bytes"}},
-                            {{"-o", "--out"}}})},
+                            {{"--host-mem-bw"}}, {{"-o", "--out"}}})},
       {"sweep", with_hw({{{"--trace"}, true}, {{"--hw"}, true}, {{"--n-persist"}},
                          {{"--n-buffer"}}, {{"--n-swap"}}, {{"--n-checkpoint"}}, {{"--alpha"}},
                          {{"--s-chunk"}}, {{"--chunk-bytes"}}, {{"-o", "--out"}}})},

@@ -9,12 +9,16 @@
 //   gpu_optim_rate       ptk_profile_gpu_adam_rate fused chunk Adam (params/s)
 //   cpu_optim_rate       ptk_profile_cpu_adam_rate host Adam, all threads (params/s)
 //   gpu_mem / cpu_mem    cudaMemGetInfo total / physical host pages
+// and, outside the reference's HardwareProfile schema, the host-memory
+// bandwidth of the simulator extension (ptk_profile_host_memory_bw).
 // measure_profile composes them; the C-ABI also runs the executor.
 #include <cuda_runtime.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -155,6 +159,56 @@ double cpu_adam_rate(std::int64_t n) {
   return n / best;
 }
 
+// Host-memory bandwidth (the --host-mem-bw of the simulator extension): the
+// host Adam on `threads` threads runs while pinned H2D and D2H copies of
+// 256 MiB loop on two streams; bw = (cpu_bytes_per_param * params updated +
+// bytes copied) / elapsed, over about `seconds` of wall time.
+double host_memory_bw(std::int64_t n, int threads, double seconds, double cpu_bytes_per_param) {
+  const std::size_t bytes = 256ull << 20;
+  PinnedBuf up(bytes), down(bytes);
+  DeviceBuf dev(bytes);
+  Stream s1, s2;
+  std::memset(up.p, 1, bytes);
+  std::atomic<bool> stop{false};
+  std::atomic<long long> copied{0};
+  std::atomic<int> errors{0};
+  std::thread dma([&] {
+    while (!stop.load()) {
+      if (ptk_memcpy_h2d_async(dev.p, up.p, bytes, s1.s) != PTK_OK ||
+          ptk_memcpy_d2h_async(down.p, dev.p, bytes, s2.s) != PTK_OK ||
+          ptk_stream_synchronize(s1.s) != PTK_OK || ptk_stream_synchronize(s2.s) != PTK_OK) {
+        errors.fetch_add(1);
+        return;
+      }
+      copied.fetch_add(2ll * static_cast<long long>(bytes));
+    }
+  });
+  std::vector<float> master(n, 0.01f), m(n, 0.0f), v(n, 0.0f);
+  std::vector<uint16_t> g(n, 0x3a83), p(n, 0);
+  std::this_thread::sleep_for(std::chrono::milliseconds(50));
+  const long long c0 = copied.load();
+  const auto t0 = std::chrono::steady_clock::now();
+  long long params = 0;
+  double el = 0.0;
+  for (int r = 1; el < seconds; ++r) {
+    const ptk_adam_config cfg{1e-3, 0.9, 0.999, 1e-8, 0.0, 0, r, 1.0};
+    const int rc = ptk_cpu_adam(&cfg, master.data(), m.data(), v.data(), g.data(), p.data(), n,
+                                threads, nullptr, nullptr);
+    if (rc != PTK_OK) {
+      stop.store(true);
+      dma.join();
+      check(rc, "cpu_adam");
+    }
+    params += n;
+    el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  const long long moved = copied.load() - c0;   // whole copies finished in the window
+  stop.store(true);
+  dma.join();
+  if (errors.load() != 0) throw std::runtime_error("host memory probe: copy failed");
+  return (cpu_bytes_per_param * static_cast<double>(params) + static_cast<double>(moved)) / el;
+}
+
 }  // namespace
 
 namespace memplan {
@@ -284,6 +338,19 @@ int ptk_profile_gpu_adam_rate(int64_t n, double* params_per_s) {
   if (n <= 0 || !params_per_s) return ptk::fail(PTK_EINVAL, "ptk_profile_gpu_adam_rate: bad argument");
   try {
     *params_per_s = gpu_adam_rate(n);
+    return PTK_OK;
+  } catch (const std::exception& e) {
+    return report(e);
+  }
+}
+
+int ptk_profile_host_memory_bw(int64_t n, int32_t threads, double seconds, double* bytes_per_s) {
+  if (n <= 0 || seconds <= 0.0 || !bytes_per_s)
+    return ptk::fail(PTK_EINVAL, "ptk_profile_host_memory_bw: bad argument");
+  try {
+    const long hc = sysconf(_SC_NPROCESSORS_ONLN);
+    const int t = threads > 0 ? threads : static_cast<int>(std::max(1L, hc - 2));
+    *bytes_per_s = host_memory_bw(n, t, seconds, 28.0);
     return PTK_OK;
   } catch (const std::exception& e) {
     return report(e);

@@ -38,3 +38,12 @@ def measure_profile(base_profile_path: str, out_path: str, comm=None, world: int
     nat.lib.ptk_measure_profile(base_profile_path.encode(), comm, world, out_path.encode())
     with open(out_path) as f:
         return json.load(f)
+
+
+def host_memory_bw(n: int = 32 << 20, threads: int = 0, seconds: float = 1.0) -> float:
+    """Host-memory bandwidth shared by the host Adam and pinned PCIe copies
+    (bytes/s), for `memplan simulate --host-mem-bw` (ptk_profile_host_memory_bw)."""
+    import ctypes
+    out = ctypes.c_double()
+    nat.lib.ptk_profile_host_memory_bw(n, threads, seconds, ctypes.byref(out))
+    return out.value

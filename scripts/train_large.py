@@ -322,6 +322,7 @@ def main():
         json.dump(hw, open(prof, "w"))
     else:
         hw = runtime.measure_profile(base, prof)
+    host_bw = runtime.host_memory_bw()   # for the simulator's host-memory extension
     layout = planner.pack(tpath)
     numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
     common = {"model": args.model, "batch": args.batch, "seq": shape.seq, "n_gpus": 1,
@@ -348,6 +349,8 @@ def main():
             sim_tl = os.path.join(OUT, f"sim_timeline_{tag}_{mode}.csv")
             sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct,
                           "--timeline-csv", sim_tl)
+            sim_hm = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct,
+                             "--host-mem-bw", host_bw)
             cfg = plan["config"]
             pinned = 16 * sum(numels[cfg["n_persist"]:])
             swap_act = sum(o["act_bytes"] for o in full["ops"] if o["block_id"] is not None
@@ -358,6 +361,8 @@ def main():
                         "cost_model_m_peak_GB": plan["estimate"]["m_peak"] / 1e9,
                         "simulator_t_iter_s": sim["t_iter"],
                         "simulator_m_peak_GB": sim["m_peak"] / 1e9,
+                        "host_mem_bw_GBs": host_bw / 1e9,
+                        "simulator_host_mem_t_iter_s": sim_hm["t_iter"],
                         "pinned_host_needed_GB": (pinned + swap_act) / 1e9,
                         "host_available_GB": avail / 1e9})
             print(json.dumps(row), flush=True)
@@ -383,6 +388,8 @@ def main():
                                              **summarize(read_csv(sim_tl))}
             row["rel_err_cost_model"] = abs(res["t_iter_s"] - row["cost_model_t_iter_s"]) / res["t_iter_s"]
             row["rel_err_simulator"] = abs(res["t_iter_s"] - row["simulator_t_iter_s"]) / res["t_iter_s"]
+            row["rel_err_simulator_host_mem"] = (abs(res["t_iter_s"] - row["simulator_host_mem_t_iter_s"])
+                                                 / res["t_iter_s"])
             break
         row["oom_attempts"] = attempts
         rows.append(row)

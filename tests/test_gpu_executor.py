@@ -121,3 +121,17 @@ def test_measured_profile_is_sane(tmp_path, cuda_device):
     nat.lib.ptk_profile_gpu_adam_rate(64 << 20, ctypes.byref(rate))
     assert rate.value > 5e10
     subprocess.run([MEMPLAN, "list-presets"], check=True, capture_output=True)
+
+
+def test_host_memory_bandwidth_probe():
+    """ptk_profile_host_memory_bw (the simulator's --host-mem-bw input): host
+    Adam + concurrent pinned copies, a positive bandwidth of a plausible size,
+    and argument checks that fail loudly."""
+    import ctypes
+    from paper_2406_08334_b200 import _native as nat
+    from paper_2406_08334_b200 import runtime
+    bw = runtime.host_memory_bw(n=4 << 20, seconds=0.3)
+    assert 1e9 < bw < 5e12
+    out = ctypes.c_double()
+    assert nat.raw.ptk_profile_host_memory_bw(0, 0, 0.3, ctypes.byref(out)) != nat.PTK_OK
+    assert "ptk_profile_host_memory_bw" in nat.last_error()
