@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--oom-retries", type=int, default=2,
                     help="on a device OOM, re-plan with the budget lowered by --oom-step")
     ap.add_argument("--oom-step", type=int, default=4_000_000_000)
+    ap.add_argument("--refine-k", type=int, default=16,
+                    help="candidates simulated for a ':refine' accounting (memplan --refine-sim)")
     ap.add_argument("--trace-in", default="", help="use this measured trace instead of profiling")
     ap.add_argument("--profile-in", default="", help="use this HardwareProfile instead of measuring")
     ap.add_argument("--tag", default="", help="suffix of the output file names")
@@ -330,7 +332,11 @@ def main():
               "trace_bwd_s": sum(o["t_bwd"] for o in full["ops"]),
               "profile_s": round(profile_s, 1), "measured_profile": hw}
     rows = []
-    for mode in args.chunk_bytes.split(","):
+    for spec in args.chunk_bytes.split(","):
+        # "used" / "reference", optionally ":refine" = plan with --refine-sim
+        # under the measured host-memory bandwidth (the simulator picks)
+        mode, _, refine = spec.partition(":")
+        label = spec.replace(":", "_")
         # the device budget is what this process can still allocate (the
         # profile's gpu_mem is the device total, incl. context + workspaces)
         release_memory()
@@ -341,12 +347,14 @@ def main():
         budget = args.gpu_mem or min(hw["gpu_mem"], free_now) - args.gpu_mem_margin
         attempts = []
         for attempt in range(args.oom_retries + 1):
-            row = dict(common, chunk_bytes=mode, gpu_mem_budget=budget)
+            row = dict(common, chunk_bytes=spec, gpu_mem_budget=budget)
             acct = ["--chunk-bytes", mode, "--gpu-mem", budget]
-            plan = memplan("plan", "--trace", tpath, "--hw", prof, *acct)
-            ppath = os.path.join(OUT, f"plan_{tag}_{mode}.json")
+            extra = (["--refine-sim", args.refine_k, "--host-mem-bw", host_bw]
+                     if refine == "refine" else [])
+            plan = memplan("plan", "--trace", tpath, "--hw", prof, *acct, *extra)
+            ppath = os.path.join(OUT, f"plan_{tag}_{label}.json")
             json.dump(plan, open(ppath, "w"), indent=1)
-            sim_tl = os.path.join(OUT, f"sim_timeline_{tag}_{mode}.csv")
+            sim_tl = os.path.join(OUT, f"sim_timeline_{tag}_{label}.csv")
             sim = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct,
                           "--timeline-csv", sim_tl)
             sim_hm = memplan("simulate", "--trace", tpath, "--hw", prof, "--plan", ppath, *acct,
@@ -372,7 +380,7 @@ def main():
                 break
             res = None
             try:
-                tl_path = os.path.join(OUT, f"timeline_{tag}_{mode}.csv") if args.timeline else ""
+                tl_path = os.path.join(OUT, f"timeline_{tag}_{label}.csv") if args.timeline else ""
                 res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup,
                                       args.phases, tl_path)
             except torch.OutOfMemoryError as e:
