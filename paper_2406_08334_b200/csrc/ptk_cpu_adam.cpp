@@ -6,6 +6,7 @@
 // is real work: OpenMP across all host cores, the same fp32 update rule and
 // the same scalars (ptk::derive_scalars) as the GPU kernel, so a chunk
 // updated on the CPU is bit-identical to one updated on the GPU.
+#include <immintrin.h>
 #include <omp.h>
 
 #include <cmath>
@@ -76,6 +77,80 @@ __attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
   }
 }
 
+// AVX-512 variant with the bf16 parameter output written by non-temporal
+// stores: the output is write-only, so streaming it saves the read-for-
+// ownership of its cache lines (2 of ~30 host DRAM bytes per parameter --
+// host DRAM is what the offloaded iteration is bound by). The arithmetic is
+// the same sequence of IEEE single operations as update_run (no FMA), so the
+// result is bit-identical; the rounding to bf16 is f32_to_bf16's.
+template <bool kL2, bool kDecay>
+__attribute__((target("avx512f,avx512bw"))) void update_run_nt(
+    const ptk_adam_scalars& s, float* __restrict__ pm, float* __restrict__ mm,
+    float* __restrict__ vm, const uint16_t* __restrict__ gr, uint16_t* __restrict__ out,
+    int64_t n) {
+  int64_t i = 0;
+  // scalar head until the output is 32-byte aligned (stream stores need it)
+  while (i < n && (reinterpret_cast<uintptr_t>(out + i) & 31u) != 0) {
+    update_run<kL2, kDecay, true>(s, pm + i, mm + i, vm + i, gr + i, out + i, 1);
+    ++i;
+  }
+  const __m512 gscale = _mm512_set1_ps(s.gscale), wd = _mm512_set1_ps(s.wd),
+               decay = _mm512_set1_ps(s.decay), w1 = _mm512_set1_ps(s.w1),
+               b2 = _mm512_set1_ps(s.b2), w2 = _mm512_set1_ps(s.w2),
+               bc2 = _mm512_set1_ps(s.bc2_sqrt), eps = _mm512_set1_ps(s.eps),
+               step = _mm512_set1_ps(s.neg_step_size);
+  const __m512i abs_mask = _mm512_set1_epi32(0x7fffffff), inf = _mm512_set1_epi32(0x7f800000),
+                round = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1),
+                qnan = _mm512_set1_epi32(0x7fff);
+  for (; i + 16 <= n; i += 16) {
+    const __m256i gb = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(gr + i));
+    __m512 g = _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(gb), 16));
+    g = _mm512_mul_ps(g, gscale);
+    __m512 p = _mm512_loadu_ps(pm + i);
+    if (kL2) g = _mm512_add_ps(g, _mm512_mul_ps(wd, p));
+    if (kDecay) p = _mm512_mul_ps(p, decay);
+    __m512 m = _mm512_loadu_ps(mm + i);
+    m = _mm512_add_ps(m, _mm512_mul_ps(w1, _mm512_sub_ps(g, m)));
+    __m512 v = _mm512_loadu_ps(vm + i);
+    v = _mm512_add_ps(_mm512_mul_ps(v, b2), _mm512_mul_ps(w2, _mm512_mul_ps(g, g)));
+    const __m512 d = _mm512_add_ps(_mm512_div_ps(_mm512_sqrt_ps(v), bc2), eps);
+    p = _mm512_add_ps(p, _mm512_mul_ps(step, _mm512_div_ps(m, d)));
+    _mm512_storeu_ps(pm + i, p);
+    _mm512_storeu_ps(mm + i, m);
+    _mm512_storeu_ps(vm + i, v);
+    const __m512i u = _mm512_castps_si512(p);
+    __m512i r = _mm512_add_epi32(_mm512_add_epi32(u, round),
+                                 _mm512_and_si512(_mm512_srli_epi32(u, 16), one));
+    r = _mm512_srli_epi32(r, 16);
+    const __mmask16 nan = _mm512_cmpgt_epu32_mask(_mm512_and_si512(u, abs_mask), inf);
+    r = _mm512_mask_mov_epi32(r, nan, qnan);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i), _mm512_cvtepi32_epi16(r));
+  }
+  if (i < n) update_run<kL2, kDecay, true>(s, pm + i, mm + i, vm + i, gr + i, out + i, n - i);
+  _mm_sfence();  // the streamed output is visible before the caller publishes it
+}
+
+bool use_nt_path() {
+  static const bool ok = [] {
+    const char* e = std::getenv("PTK_CPU_ADAM_NT");
+    if (e && std::string(e) == "0") return false;
+    __builtin_cpu_init();
+    return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+  }();
+  return ok;
+}
+
+void update_block_dispatch(const ptk_adam_scalars& s, float* pm, float* mm, float* vm,
+                           const uint16_t* gr, uint16_t* out, int64_t n) {
+  if (out != nullptr && use_nt_path()) {
+    if (s.wd != 0.0f) update_run_nt<true, false>(s, pm, mm, vm, gr, out, n);
+    else if (s.adamw != 0) update_run_nt<false, true>(s, pm, mm, vm, gr, out, n);
+    else update_run_nt<false, false>(s, pm, mm, vm, gr, out, n);
+    return;
+  }
+  update_block(s, pm, mm, vm, gr, out, n);
+}
+
 constexpr int64_t kBlock = 1 << 16;
 
 }  // namespace
@@ -116,8 +191,8 @@ extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* ex
       part_sq[b] = sq;
       part_bad[b] = bad;
     }
-    update_block(s, master + lo, exp_avg + lo, exp_avg_sq + lo, grad + lo,
-                 param_out ? param_out + lo : nullptr, len);
+    update_block_dispatch(s, master + lo, exp_avg + lo, exp_avg_sq + lo, grad + lo,
+                          param_out ? param_out + lo : nullptr, len);
   };
   if (kStatic) {
 #pragma omp parallel for num_threads(threads) schedule(static)

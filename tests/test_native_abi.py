@@ -76,6 +76,37 @@ def test_host_adam_k6_bit_exact():
     np.testing.assert_array_equal(pa, pb)
 
 
+@pytest.mark.parametrize("mode", ["adam", "adamw", "l2"])
+@pytest.mark.parametrize("offset", [0, 1, 5])
+def test_host_adam_all_modes_unaligned_bit_exact(mode, offset):
+    """Every update rule of the host Adam (incl. the AVX-512 non-temporal
+    output path) at unaligned output addresses, with a NaN and infinities in
+    the gradients: bit-identical to the oracle, bf16 rounding included."""
+    from paper_2406_08334_b200 import _native as nat
+    n = 70_001
+    wd, adamw = {"adam": (0.0, False), "adamw": (0.01, True), "l2": (0.01, False)}[mode]
+    master = ol.fill_f32(n, 3, 0.05)
+    g = ol.fill_bf16(n, 4, 1e-3)
+    g[17] = 0x7fc0   # NaN
+    g[18] = 0x7f80   # +inf
+    g[n - 3] = 0xff80  # -inf
+    a = [master.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    b = [master.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    buf = np.zeros(n + 8, np.uint16)
+    pa = buf[offset:offset + n]
+    pb = np.zeros(n, np.uint16)
+    for step in (1, 2):
+        cfg = nat.adam_config(step=step, weight_decay=wd, adamw=adamw, grad_scale=0.5)
+        nat.lib.ptk_cpu_adam(ctypes.byref(cfg), *[ctypes.c_void_p(x.ctypes.data) for x in a],
+                             ctypes.c_void_p(g.ctypes.data), ctypes.c_void_p(pa.ctypes.data), n,
+                             3, None, None)
+        ol.adam_step(ol.scalars(step=step, weight_decay=wd, adamw=adamw, grad_scale=0.5), *b, g,
+                     pb)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x.view(np.uint32), y.view(np.uint32))
+    np.testing.assert_array_equal(pa, pb)
+
+
 def test_errors_are_reported():
     from paper_2406_08334_b200 import _native as nat
     rc = nat.raw.ptk_cpu_adam(None, None, None, None, None, None, 0, 0, None, None)
