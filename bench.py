@@ -273,7 +273,7 @@ def run_gpu(args):
     del cs
     torch.cuda.empty_cache()
     train = train_offload = None
-    if args.train_steps > 0 and args.workload == "cfg2":
+    if args.train_steps > 0 and args.workload in TRAIN_MODELS:
         train = run_train(args, world, rank, dev, comm)
         if args.offload_persist >= 0:
             train_offload = run_train(args, world, rank, dev, comm,
@@ -440,9 +440,13 @@ def live_copy_peak():
     return round(2 * 2 * (1 << 30) / (best * 1e-3) / 1e9, 1)
 
 
+TRAIN_MODELS = {"cfg2": "gpt2-1.5b_b8", "cfg1": "gpt2-1b_b2"}
+
+
 def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
-    """tokens/s of a full training iteration of the cfg2 model (GPT-2 1.5B,
-    b8, seq 1024) whose parameters live in the planner's chunk buffers:
+    """tokens/s of a full training iteration of the workload's model (cfg2:
+    GPT-2 1.5B b8; cfg1: the reference's test model gpt2-1b b2; seq 1024)
+    whose parameters live in the planner's chunk buffers:
     forward + backward in PyTorch (bf16 GEMMs / SDPA), then the chunk step
     (RS -> fused Adam -> AG) through the C-ABI. With n_persist < n_chunk the
     remaining chunks are non-persistent: pinned host shards fetched into
@@ -454,8 +458,9 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
     from paper_2406_08334_b200.offload import ChunkPool
     from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
-    trace = planner.trace_for("gpt2-1.5b_b8")
-    layout = planner.layout_for("gpt2-1.5b_b8")
+    name = TRAIN_MODELS[args.workload]
+    trace = planner.trace_for(name)
+    layout = planner.layout_for(name)
     numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
     np_ = len(numels) if n_persist is None else n_persist
     cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode="nccl", comm=comm)
@@ -490,8 +495,9 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     loss_vals = [float(x) for x in losses]
     out = {"tokens_per_s": round(batch * shape.seq * world / (ms * 1e-3), 1),
            "ms_per_iter": round(ms, 3), "iters": args.train_steps,
-           "model": "GPT-2 1.5B (h1600 L48 25 heads, tied, parameter-free final LN: the trace has no ln_f), "
-                    f"b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
+           "model": f"{name}: GPT-2 h{shape.hidden} L{shape.blocks} {shape.heads} heads, "
+                    f"{sum(numels) / 1e9:.2f} B params (tied, parameter-free final LN: the trace has "
+                    f"no ln_f), b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
            "plan": {"n_chunk": len(numels), "n_persist": np_, "n_buffer": n_buffer if pool else 0},
            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
