@@ -478,14 +478,15 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     hyper = AdamHyper(lr=1e-4, weight_decay=0.01, adamw=True)
     stream = torch.cuda.current_stream()
     losses = []
+    overlap = args.train_overlap
     for i in range(args.warmup):
-        losses.append(train_step(model, tokens[i], targets[i], hyper))
+        losses.append(train_step(model, tokens[i], targets[i], hyper, overlap=overlap))
     torch.cuda.synchronize()
     barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(args.warmup, n_iter):
-        losses.append(train_step(model, tokens[i], targets[i], hyper))
+        losses.append(train_step(model, tokens[i], targets[i], hyper, overlap=overlap))
     if pool is not None:
         pool.finish_step()  # the last host updates belong to the timed iterations
     t1.record(stream)
@@ -500,6 +501,8 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
                     f"no ln_f), b{batch} s{shape.seq} per rank, bf16 compute, fp32 master/m/v in chunks",
            "plan": {"n_chunk": len(numels), "n_persist": np_, "n_buffer": n_buffer if pool else 0},
            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
+           "chunk_step": ("per chunk on a side stream as its gradients complete (overlapping "
+                          "the backward)" if overlap else "after the backward"),
            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
     if pool is not None:
         out["offload"] = {"pinned_host_GB": round(pool.host_bytes / 1e9, 3),
@@ -758,6 +761,9 @@ def main():
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train-overlap", action=argparse.BooleanOptionalAction, default=False,
+                    help="training: issue each persistent chunk's step on a side stream as soon "
+                         "as its gradients are complete")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
                     help="N=1: time the K steps as one replay of a CUDA graph holding them "
                          "(default); --no-graph: host-launched steps")

@@ -247,6 +247,53 @@ class ChunkSet:
             if tl is not None:
                 tl.gpu(stream, "gpu", "optim_end", f"chunk={c.chunk_id + 1}")
 
+    # ----------------------------------------------- overlapped (per chunk) --
+    def begin_overlapped_step(self, hyper: AdamHyper, side: torch.cuda.Stream) -> None:
+        """Start a step whose chunks are updated one by one, each as soon as
+        its gradients are complete (ChunkedGPT2's backward hooks), on the
+        side stream `side` while the backward continues on the compute
+        stream. Same kernels and inputs as step(): bit-identical results."""
+        if self.mode != "nccl":
+            raise ValueError("overlapped step needs mode='nccl' (the fused exchange brackets "
+                             "all chunks with peer barriers)")
+        self.step_count += 1
+        self._ov_cfg = hyper.config(self.step_count, self.world)
+        self._ov_side = side
+        self._ov_done = [False] * len(self.chunks)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        nat.lib.ptk_stats_reset(vp(self.stats), stream_handle(side))
+
+    def step_chunk_overlapped(self, ci: int) -> None:
+        """RS -> Adam -> AG of chunk ci on the side stream, after everything
+        issued so far on the compute stream (its gradient copies)."""
+        if self._ov_done[ci]:
+            return
+        self._ov_done[ci] = True
+        side = self._ov_side
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        s = stream_handle(side)
+        c = self.chunks[ci]
+        tl = self.timeline
+        if tl is not None:
+            tl.gpu(side, "gpu", "optim_start", f"chunk={c.chunk_id + 1}")
+        if self.comm is not None:
+            nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
+        nat.lib.ptk_chunk_adam(ctypes.byref(self._ov_cfg), vp(c.master), vp(c.exp_avg),
+                               vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                               c.shard, vp(self.stats), vp(self.workspace), None, None, s)
+        if self.comm is not None:
+            nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
+        if tl is not None:
+            tl.gpu(side, "gpu", "optim_end", f"chunk={c.chunk_id + 1}")
+
+    def finish_overlapped_step(self) -> None:
+        """Update the chunks whose hooks never fired (in chunk order), then
+        order the compute stream after the side stream."""
+        for ci in range(len(self.chunks)):
+            self.step_chunk_overlapped(ci)
+        torch.cuda.current_stream(self.device).wait_stream(self._ov_side)
+        self._ov_side = None
+
     def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
         if not hasattr(self, "clip_coef"):
             self.clip_coef = torch.ones(1, dtype=F32, device=self.device)

@@ -141,6 +141,11 @@ class ChunkedGPT2:
         self.params: dict[str, torch.Tensor] = {}
         self.blocks: list[dict[str, torch.Tensor]] = [dict() for _ in range(shape.blocks)]
         self._hooks = []
+        # overlapped step (train_step(..., overlap=True)): per persistent
+        # chunk, how many parameters must report a gradient before its update
+        self._chunk_nparams = [0] * len(chunks.chunks)
+        self._pending: list[int] = []
+        self._overlap = False
         # non-persistent chunks: parameter specs for ChunkGather, where each
         # param goes (None = top level, else block id), and init staging
         first_pooled = pool.first if pool is not None else len(layout["chunks"])
@@ -165,7 +170,9 @@ class ChunkedGPT2:
                     p = cs.param[lo:lo + numel].view(pshape)
                     p.requires_grad_(True)
                     g = cs.grad[lo:lo + numel].view(pshape)
-                    self._hooks.append(p.register_post_accumulate_grad_hook(_stash_into(g)))
+                    self._hooks.append(p.register_post_accumulate_grad_hook(
+                        _stash_into(g, self, ci)))
+                    self._chunk_nparams[ci] += 1
                 else:
                     buf = self._init_buf.setdefault(
                         ci, torch.zeros(pool.shard[ci] * pool.world, dtype=BF16,
@@ -516,21 +523,45 @@ class ActivationSwap:
             x.register_hook(lambda g, due=tuple(due): [self.prefetch(b) for b in due] and None)
 
 
-def _stash_into(slot: torch.Tensor):
+def _stash_into(slot: torch.Tensor, model: "ChunkedGPT2" = None, ci: int = -1):
     def hook(p: torch.Tensor) -> None:
         slot.copy_(p.grad)
         p.grad = None
+        if model is not None and model._overlap:
+            model._pending[ci] -= 1
+            if model._pending[ci] == 0:   # chunk ci's gradients are complete
+                model.chunks.step_chunk_overlapped(ci)
     return hook
 
 
 def train_step(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
-               hyper: AdamHyper) -> torch.Tensor:
+               hyper: AdamHyper, overlap: bool = False) -> torch.Tensor:
     """One iteration; returns the (device) loss. Gradient slots of the chunk
-    buffers are fully overwritten by the hooks each step (padding stays 0)."""
+    buffers are fully overwritten by the hooks each step (padding stays 0).
+
+    overlap=True: each persistent chunk's step (RS -> Adam -> AG) is issued
+    on a side stream the moment its last gradient lands, while the backward
+    of the earlier blocks continues (a chunk's parameters are used only by
+    its own operators, all of which have run backward by then); the results
+    are bit-identical to the step after the whole backward."""
+    step_no = model.chunks.step_count + 1   # of this iteration, for every chunk
+    if overlap:
+        if not hasattr(model, "_side"):
+            model._side = torch.cuda.Stream(model.chunks.device)
+        model._pending = list(model._chunk_nparams)
+        model._overlap = True
+        model.chunks.begin_overlapped_step(hyper, model._side)
+    try:
+        return _train_step(model, tokens, targets, hyper, overlap, step_no)
+    finally:
+        model._overlap = False
+
+
+def _train_step(model, tokens, targets, hyper, overlap, step_no):
     pool = getattr(model, "pool", None)
     tl = model.timeline
     if pool is not None:
-        pool.begin_step(model.chunks.step_count + 1, hyper, model.pool_uses())
+        pool.begin_step(step_no, hyper, model.pool_uses())
     if tl is not None:
         tl.host("host", "forward_call_start", "")
     loss = model.loss(tokens, targets)
@@ -540,5 +571,8 @@ def train_step(model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
     loss.backward()
     if tl is not None:
         tl.host("host", "backward_call_end", "")
-    model.chunks.step(hyper)  # persistent chunks; pooled chunks drained during backward
+    if overlap:
+        model.chunks.finish_overlapped_step()
+    else:
+        model.chunks.step(hyper)  # persistent chunks; pooled chunks drained during backward
     return loss.detach()

@@ -314,3 +314,52 @@ def test_training_timeline_in_simulator_schema(tmp_path, cuda_device):
     assert read_csv(path) == rows
     summ = summarize(rows)
     assert summ["bwd_end_ns"] >= summ["fwd_end_ns"] > 0 and summ["busy_ns"]["cpu"] > 0
+
+
+@pytest.mark.parametrize("n_persist", [3, 1])
+def test_overlapped_chunk_step_is_bit_identical(tmp_path, cuda_device, n_persist):
+    """train_step(overlap=True): each persistent chunk's update runs on a side
+    stream as soon as its gradients are complete, during the rest of the
+    backward. Losses, fp32 masters and bf16 parameters must equal the
+    step-after-backward run bit for bit (also with non-persistent chunks,
+    whose host Adam must see the same step numbers)."""
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    spec = tmp_path / "spec.json"
+    spec.write_text(json.dumps({"hidden_size": 256, "n_blocks": 2, "n_heads": 4,
+                                "vocab_size": 1000, "seq_len": 128}))
+    tpath = planner.trace_file(["--spec", str(spec), "--batch", "4"], str(tmp_path / "t.json"))
+    trace = json.load(open(tpath))
+    layout = planner.pack(tpath, grid="2Mi")
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+
+    def run(overlap):
+        cs = ChunkSet(numels[:n_persist], device=cuda_device)
+        pool = (ChunkPool(numels, n_persist, 1, device=cuda_device)
+                if n_persist < len(numels) else None)
+        model = ChunkedGPT2(GPT2Shape.from_trace(trace), layout, cs, trace["ops"], pool=pool)
+        model.init_weights(0)
+        g = torch.Generator(device=cuda_device).manual_seed(0)
+        losses = []
+        for _ in range(4):
+            x = torch.randint(0, 1000, (4, 128), device=cuda_device, generator=g)
+            losses.append(float(train_step(model, x, (x + 1) % 1000,
+                                           AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True),
+                                           overlap=overlap)))
+        torch.cuda.synchronize()
+        if pool is not None:
+            pool.finish_step()
+        state = [t.clone() for c in cs.chunks for t in (c.master, c.exp_avg, c.param)]
+        if pool is not None:
+            state += [pool.h_master[c].clone() for c in sorted(pool.numel)]
+        return losses, state, cs.grad_stats()
+
+    ref_l, ref_s, ref_stats = run(False)
+    l, s, stats = run(True)
+    assert l == ref_l
+    for a, b in zip(s, ref_s):
+        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
+                           b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
+    assert stats[1] == ref_stats[1] and abs(stats[0] - ref_stats[0]) <= 1e-9 * ref_stats[0]
