@@ -329,6 +329,7 @@ class ChunkedGPT2:
         self.strategies = list(strategies)
         self._swap = ActivationSwap({c.param.untyped_storage().data_ptr()
                                      for c in self.chunks.chunks}, getattr(self, "pool", None))
+        self._swap.set_lead([b for b, st in enumerate(self.strategies) if st == "swap"])
 
     def loss(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         pool = getattr(self, "pool", None)
@@ -447,7 +448,7 @@ class ActivationSwap:
     swapped; parameters of non-persistent chunks (pool slots) are handed to
     the pool's own hooks."""
 
-    lead = 2   # prefetch block b when the backward of block b + lead starts
+    lead = 2   # prefetch block b when the backward of block b + lead starts (see set_lead)
 
     def __init__(self, param_storages: set[int], pool=None):
         self.params = param_storages
@@ -456,6 +457,20 @@ class ActivationSwap:
         self.block = None
         self.saved: dict[int, list[dict]] = {}
         self.timeline = None
+
+    def set_lead(self, swap_blocks: list[int]) -> None:
+        """Prefetch as early as the schedule allows without two swap blocks'
+        activations coming back at once: swap blocks sit N_int + 1 apart
+        (proj/src/layout.cpp:218-249), so up to spacing - 1 (capped at 4)
+        blocks ahead; a swap-in competes with the host Adam for host DRAM
+        and took up to ~40 ms, several blocks' backward."""
+        import os
+        if os.environ.get("PTK_SWAP_LEAD"):   # measurement override
+            self.lead = max(1, int(os.environ["PTK_SWAP_LEAD"]))
+            return
+        gaps = [b - a for a, b in zip(swap_blocks, swap_blocks[1:])]
+        spacing = min(gaps) if gaps else 5
+        self.lead = max(2, min(4, spacing - 1))
 
     def begin_block(self, b: int) -> None:
         self.block = b
