@@ -363,3 +363,53 @@ def test_overlapped_chunk_step_is_bit_identical(tmp_path, cuda_device, n_persist
         assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
                            b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
     assert stats[1] == ref_stats[1] and abs(stats[0] - ref_stats[0]) <= 1e-9 * ref_stats[0]
+
+
+def test_pool_decisions_match_the_simulator(tmp_path, cuda_device):
+    """Buffer-pool semantics: the real iteration's chunk
+    uploads (h2d stream), drains (d2h stream) and evictions happen in the
+    same per-stream order, for the same chunks, as in `memplan simulate` of
+    the same plan (one fetch in flight, farthest-next-use eviction, drain
+    after the chunk's last backward use)."""
+    import subprocess
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
+    from paper_2406_08334_b200.offload import ChunkPool
+    from paper_2406_08334_b200.timeline import Timeline, read_csv
+    from paper_2406_08334_b200.train import ChunkedGPT2, GPT2Shape, train_step
+    spec = tmp_path / "spec.json"
+    spec.write_text(json.dumps({"hidden_size": 256, "n_blocks": 5, "n_heads": 4,
+                                "vocab_size": 1000, "seq_len": 128}))
+    tpath = planner.trace_file(["--spec", str(spec), "--batch", "4"], str(tmp_path / "t.json"))
+    trace = json.load(open(tpath))
+    layout = planner.pack(tpath, grid="2Mi")
+    numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
+    n_persist, n_buffer = 1, 2
+    cs = ChunkSet(numels[:n_persist], device=cuda_device)
+    pool = ChunkPool(numels, n_persist, n_buffer, device=cuda_device)
+    model = ChunkedGPT2(GPT2Shape.from_trace(trace), layout, cs, trace["ops"], pool=pool)
+    model.init_weights(0)
+    x = torch.randint(0, 1000, (4, 128), device=cuda_device)
+    train_step(model, x, (x + 1) % 1000, AdamHyper())
+    pool.finish_step()
+    tl = Timeline()
+    model.timeline = cs.timeline = pool.timeline = tl
+    tl.begin()
+    train_step(model, x, (x + 1) % 1000, AdamHyper())
+    pool.finish_step()
+    real = tl.end()
+    memplan = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "build", "memplan")
+    sim_csv = str(tmp_path / "sim.csv")
+    subprocess.run([memplan, "simulate", "--trace", tpath, "--hw", "a100x1", "--s-chunk",
+                    str(layout["s_chunk"]), "--n-persist", str(n_persist), "--n-buffer",
+                    str(n_buffer), "--timeline-csv", sim_csv], check=True, capture_output=True)
+    sim = read_csv(sim_csv)
+
+    def per_stream(rows, event):
+        return [s for _, _, e, s in rows if e == event]
+
+    assert len(numels) - n_persist >= 3   # several pooled chunks, so evictions happen
+    for event in ("upload_start", "offload_start", "evict"):
+        assert per_stream(real, event) == per_stream(sim, event), event
+    assert per_stream(real, "evict")
