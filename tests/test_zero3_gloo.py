@@ -1,4 +1,4 @@
-"""World-size-2 coverage of the sharded (N>1) path on CPU with gloo.
+"""World-size-2 and -3 coverage of the sharded (N>1) path on CPU with gloo.
 
 Two processes each own half of a chunk (ptk_shard_elems mapping, padded to
 8*w elements). Each produces its local gradients of the FULL chunk, the
@@ -54,7 +54,18 @@ def _worker(rank, world, port, outdir):
         g_local[N:] = 0
         g32 = torch.from_numpy(ol.bf16_to_f32(g_local).copy())
         out = torch.zeros(shard, dtype=torch.float32)
-        dist.reduce_scatter(out, list(g32.split(shard)), op=dist.ReduceOp.SUM)
+        if world == 2:
+            dist.reduce_scatter(out, list(g32.split(shard)), op=dist.ReduceOp.SUM)
+        else:
+            # w > 2: gloo's ring sums in its own order; gather every rank's
+            # owned slice and sum in rank order, the fused kernel's order
+            parts = [torch.zeros(shard, dtype=torch.float32) for _ in range(world)]
+            for r in range(world):
+                slice_r = g32[r * shard:(r + 1) * shard].contiguous()
+                dist.gather(slice_r, parts if r == rank else None, dst=r)
+            out = parts[0].clone()
+            for r in range(1, world):
+                out += parts[r]
         # product host Adam takes bf16 grads: round the fp32 sum once (RS in bf16)
         g_shard = ol.f32_to_bf16(out.numpy())
         cfg = nat.adam_config(step=step, weight_decay=0.01, adamw=True, grad_scale=1.0 / world)
@@ -72,9 +83,9 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_two_rank_sharded_step_equals_single_rank(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_step_equals_single_rank(tmp_path, world):
     import oracle_lib as ol
-    world = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
                        join=True, start_method="spawn")
     shard = ol.shard_elems(N, world)
