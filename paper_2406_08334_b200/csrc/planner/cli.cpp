@@ -517,7 +517,11 @@ const char* kHelp =
     "  simulate      event-driven simulation (+ --timeline, --timeline-csv, --mem-trace)\n"
     "  validate      estimate vs. simulation sweep (--samples, --seed)\n"
     "  sweep         estimate over config ranges (--n-persist lo:hi, ...)\n"
-    "  list-presets  list model and hardware presets\n";
+    "  list-presets  list model and hardware presets\n"
+    "B200 extensions (opt-in; without them every output is the reference's):\n"
+    "  plan --refine-sim K                rank the K best candidates by simulation\n"
+    "  --chunk-bytes reference|used       charge chunk states by s_chunk or by used bytes\n"
+    "  --host-mem-bw B                    simulate host Adam + PCIe copies sharing B bytes/s\n";
 
 }  // namespace
 
