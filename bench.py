@@ -479,14 +479,24 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     stream = torch.cuda.current_stream()
     losses = []
     overlap = args.train_overlap
+    graphed = None
+    if args.train_graph and pool is None:
+        from paper_2406_08334_b200.train import GraphedTrainStep
+        graphed = GraphedTrainStep(model, tokens[0], targets[0])
+
+    def one(i):
+        if graphed is not None:
+            return graphed(tokens[i], targets[i], hyper)
+        return train_step(model, tokens[i], targets[i], hyper, overlap=overlap)
+
     for i in range(args.warmup):
-        losses.append(train_step(model, tokens[i], targets[i], hyper, overlap=overlap))
+        losses.append(one(i))
     torch.cuda.synchronize()
     barrier(world)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(args.warmup, n_iter):
-        losses.append(train_step(model, tokens[i], targets[i], hyper, overlap=overlap))
+        losses.append(one(i))
     if pool is not None:
         pool.finish_step()  # the last host updates belong to the timed iterations
     t1.record(stream)
@@ -503,6 +513,8 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
            "loss_first": round(loss_vals[0], 4), "loss_last": round(loss_vals[-1], 4),
            "chunk_step": ("per chunk on a side stream as its gradients complete (overlapping "
                           "the backward)" if overlap else "after the backward"),
+           "forward_backward": ("one CUDA-graph replay (GraphedTrainStep)" if graphed is not None
+                                else "host-launched"),
            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
     if pool is not None:
         out["offload"] = {"pinned_host_GB": round(pool.host_bytes / 1e9, 3),
@@ -761,6 +773,9 @@ def main():
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--train-graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="training (all chunks persistent): forward + backward as one CUDA-graph "
+                         "replay, chunk step eager (default; --no-train-graph: host-launched)")
     ap.add_argument("--train-overlap", action=argparse.BooleanOptionalAction, default=False,
                     help="training: issue each persistent chunk's step on a side stream as soon "
                          "as its gradients are complete")

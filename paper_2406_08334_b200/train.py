@@ -591,3 +591,44 @@ def _train_step(model, tokens, targets, hyper, overlap, step_no):
     else:
         model.chunks.step(hyper)  # persistent chunks; pooled chunks drained during backward
     return loss.detach()
+
+
+class GraphedTrainStep:
+    """The forward + backward of an all-persistent ChunkedGPT2 captured once
+    into a CUDA graph and replayed every iteration (the model's ~40 kernels
+    per block no longer pay host launch latency); the chunk step (RS -> Adam
+    -> AG through the C-ABI) runs after it, eagerly, with the step's own
+    Adam scalars. Parameters and gradient slots are the chunk buffers, so
+    the graph's addresses stay valid; tokens / targets are copied into static
+    inputs. Bit-identical to train_step (same kernels, same order).
+
+    Requires: no non-persistent chunks (the pool's fetches and host Adam are
+    host-synchronising) and no swap blocks (pinned-memory saved-tensor
+    hooks); checkpoint blocks are captured as recompute."""
+
+    def __init__(self, model: ChunkedGPT2, tokens: torch.Tensor, targets: torch.Tensor,
+                 warmup: int = 2):
+        if getattr(model, "pool", None) is not None:
+            raise ValueError("graphed step needs every chunk persistent")
+        if "swap" in model._strategies():
+            raise ValueError("graphed step does not capture activation swap")
+        self.model = model
+        self.x = tokens.clone()
+        self.y = targets.clone()
+        side = torch.cuda.Stream(model.chunks.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):   # warm-up outside capture (allocator, cuBLAS handles)
+            for _ in range(warmup):
+                model.loss(self.x, self.y).backward()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss = model.loss(self.x, self.y)
+            self.loss.backward()
+
+    def __call__(self, tokens: torch.Tensor, targets: torch.Tensor, hyper: AdamHyper) -> torch.Tensor:
+        self.x.copy_(tokens, non_blocking=True)
+        self.y.copy_(targets, non_blocking=True)
+        self.graph.replay()
+        self.model.chunks.step(hyper)
+        return self.loss.detach().clone()

@@ -413,3 +413,37 @@ def test_pool_decisions_match_the_simulator(tmp_path, cuda_device):
     for event in ("upload_start", "offload_start", "evict"):
         assert per_stream(real, event) == per_stream(sim, event), event
     assert per_stream(real, "evict")
+
+
+@pytest.mark.parametrize("checkpoint", [False, True])
+def test_graphed_train_step_is_bit_identical(tmp_path, cuda_device, checkpoint):
+    """GraphedTrainStep (forward + backward captured in a CUDA graph, chunk
+    step eager) trains exactly like train_step: losses, masters and params
+    bit for bit, with and without a checkpointed block."""
+    from paper_2406_08334_b200.chunks import AdamHyper
+    from paper_2406_08334_b200.train import GraphedTrainStep, train_step
+    hyper = AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True)
+
+    def run(graphed):
+        model, shape = _setup(tmp_path / ("g" if graphed else "e"), cuda_device)
+        if checkpoint:
+            model.set_block_schedule(["checkpoint", "none"])
+        g = torch.Generator(device=cuda_device).manual_seed(0)
+        xs = [torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device, generator=g)
+              for _ in range(4)]
+        step = GraphedTrainStep(model, xs[0], (xs[0] + 1) % shape.vocab) if graphed else None
+        losses = []
+        for x in xs:
+            y = (x + 1) % shape.vocab
+            losses.append(float(step(x, y, hyper) if graphed else train_step(model, x, y, hyper)))
+        torch.cuda.synchronize()
+        return losses, [t.clone() for c in model.chunks.chunks for t in (c.master, c.param)]
+
+    (tmp_path / "g").mkdir()
+    (tmp_path / "e").mkdir()
+    ref_l, ref_s = run(False)
+    l, s = run(True)
+    assert l == ref_l
+    for a, b in zip(s, ref_s):
+        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
+                           b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
