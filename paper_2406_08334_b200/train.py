@@ -371,9 +371,20 @@ def head_logits(sh: GPT2Shape, params: dict, x: torch.Tensor) -> torch.Tensor:
     operator (proj/src/trace.cpp:320-340 -- embedding, 8 ops per block,
     lm_head, cross_entropy), so the parameter bytes stay the trace's, while
     the residual stream is still normalised before the vocabulary projection
-    (without it the 48-block stream makes the first Adam steps unstable)."""
+    (without it the 48-block stream makes the first Adam steps unstable).
+
+    GPT-2's vocabulary (50257) is not a multiple of 8, and with that
+    leading dimension cuBLAS falls back to `align1` SM75 mma.sync GEMMs for
+    the projection and both its gradients (28 of 136 ms of a GPT-2 1.5B
+    iteration, scripts/train_breakdown.py). The weight is therefore padded
+    with zero rows to a multiple of 64 for the GEMM (a 160 MB copy) and the
+    logits sliced back: the same values, aligned kernels."""
     x = _norm(sh, x, None, None)
-    return F.linear(x, params["wte"] if sh.tied else params["head_w"])
+    w = params["wte"] if sh.tied else params["head_w"]
+    pad = (-w.shape[0]) % 64
+    if pad == 0:
+        return F.linear(x, w)
+    return F.linear(x, F.pad(w, (0, 0, 0, pad)))[..., : w.shape[0]]
 
 
 def head_loss(sh: GPT2Shape, params: dict, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
