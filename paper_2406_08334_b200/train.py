@@ -480,8 +480,12 @@ class ActivationSwap:
             self.lead = max(1, int(os.environ["PTK_SWAP_LEAD"]))
             return
         gaps = [b - a for a, b in zip(swap_blocks, swap_blocks[1:])]
-        spacing = min(gaps) if gaps else 5
-        self.lead = max(2, min(4, spacing - 1))
+        spacing = min(gaps) if gaps else 4
+        # capped at 3: the planner reserves one block of swap-in headroom, and a
+        # block prefetched much earlier than its backward overlaps more live
+        # activations than the memory model charges (a lead of 4 pushed a plan
+        # sized to the last GB over the edge)
+        self.lead = max(2, min(3, spacing - 1))
 
     def begin_block(self, b: int) -> None:
         self.block = b

@@ -188,6 +188,17 @@ def record_timeline(model, cs, pool, x, y, hyper, path: str, iters: int = 2) -> 
     return {"iterations": iters, "last_iteration": summarize(last_iteration(rows))}
 
 
+def _train_child(full, layout, plan, batch, iters, warmup, phases, timeline_path) -> dict:
+    """One training attempt (run in a spawned child with --isolate)."""
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    try:
+        return train_with_plan(full, layout, plan, batch, dev, iters, warmup, phases,
+                               timeline_path)
+    except torch.OutOfMemoryError as e:
+        return {"oom": str(e)[:300]}
+
+
 def train_with_plan(full: dict, layout: dict, plan: dict, batch: int, dev, iters: int,
                     warmup: int, phases: int = 0, timeline_path: str = "") -> dict:
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
@@ -274,7 +285,7 @@ def main():
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")
     ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
-    ap.add_argument("--gpu-mem-margin", type=int, default=6_000_000_000,
+    ap.add_argument("--gpu-mem-margin", type=int, default=10_000_000_000,
                     help="bytes kept free below the allocatable device memory for the "
                          "caching allocator's slack (ignored with --gpu-mem)")
     ap.add_argument("--chunk-bytes", default="used,reference",
@@ -283,6 +294,9 @@ def main():
     ap.add_argument("--oom-retries", type=int, default=2,
                     help="on a device OOM, re-plan with the budget lowered by --oom-step")
     ap.add_argument("--oom-step", type=int, default=4_000_000_000)
+    ap.add_argument("--isolate", action=argparse.BooleanOptionalAction, default=True,
+                    help="train each attempt in a spawned child process (default), so a failed "
+                         "attempt releases all device and pinned host memory")
     ap.add_argument("--refine-k", type=int, default=16,
                     help="candidates simulated for a ':refine' accounting (memplan --refine-sim)")
     ap.add_argument("--trace-in", default="", help="use this measured trace instead of profiling")
@@ -378,14 +392,19 @@ def main():
                 row["skipped"] = (f"plan needs {(pinned + swap_act) / 1e9:.1f} GB pinned host "
                                   f"memory, more than {args.host_frac} x {avail / 1e9:.1f} GB")
                 break
-            res = None
-            try:
-                tl_path = os.path.join(OUT, f"timeline_{tag}_{label}.csv") if args.timeline else ""
-                res = train_with_plan(full, layout, plan, args.batch, dev, args.iters, args.warmup,
-                                      args.phases, tl_path)
-            except torch.OutOfMemoryError as e:
-                attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": str(e)[:300]})
-            if res is None:   # the failed model is released with the exception
+            tl_path = os.path.join(OUT, f"timeline_{tag}_{label}.csv") if args.timeline else ""
+            job = (full, layout, plan, args.batch, args.iters, args.warmup, args.phases, tl_path)
+            if args.isolate:
+                # a child process per attempt: an OOM (or any failure) gives
+                # every device and pinned host byte back when the child exits
+                release_memory()
+                import multiprocessing as mp
+                with mp.get_context("spawn").Pool(1) as workers:
+                    res = workers.apply(_train_child, job)
+            else:
+                res = _train_child(*job)
+            if "oom" in res:
+                attempts.append({"gpu_mem_budget": budget, "plan": cfg, "oom": res["oom"]})
                 release_memory()
                 budget -= args.oom_step
                 continue
