@@ -470,22 +470,13 @@ class ActivationSwap:
         self.timeline = None
 
     def set_lead(self, swap_blocks: list[int]) -> None:
-        """Prefetch as early as the schedule allows without two swap blocks'
-        activations coming back at once: swap blocks sit N_int + 1 apart
-        (proj/src/layout.cpp:218-249), so up to spacing - 1 (capped at 4)
-        blocks ahead; a swap-in competes with the host Adam for host DRAM
-        and took up to ~40 ms, several blocks' backward."""
+        """Prefetch distance in blocks (default 2; PTK_SWAP_LEAD overrides).
+        Measured both ways: a longer lead helped a GPT-2 10B plan (lead 4:
+        -3..5 %) and hurt a Llama-2 13B plan sized to the last GB (lead 3:
+        +14 %, the prefetched block competes for memory and host DRAM), so
+        the default stays 2 (profiles/README.md)."""
         import os
-        if os.environ.get("PTK_SWAP_LEAD"):   # measurement override
-            self.lead = max(1, int(os.environ["PTK_SWAP_LEAD"]))
-            return
-        gaps = [b - a for a, b in zip(swap_blocks, swap_blocks[1:])]
-        spacing = min(gaps) if gaps else 4
-        # capped at 3: the planner reserves one block of swap-in headroom, and a
-        # block prefetched much earlier than its backward overlaps more live
-        # activations than the memory model charges (a lead of 4 pushed a plan
-        # sized to the last GB over the edge)
-        self.lead = max(2, min(3, spacing - 1))
+        self.lead = max(1, int(os.environ.get("PTK_SWAP_LEAD", "2")))
 
     def begin_block(self, b: int) -> None:
         self.block = b
