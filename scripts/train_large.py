@@ -285,7 +285,7 @@ def main():
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")
     ap.add_argument("--gpu-mem", type=int, default=0, help="device budget override (bytes)")
-    ap.add_argument("--gpu-mem-margin", type=int, default=6_000_000_000,
+    ap.add_argument("--gpu-mem-margin", type=int, default=10_000_000_000,
                     help="bytes kept free below the allocatable device memory for the "
                          "caching allocator's slack (ignored with --gpu-mem)")
     ap.add_argument("--chunk-bytes", default="used,reference",
