@@ -24,6 +24,7 @@ One iteration (ZeRO-3 chunk semantics):
 from __future__ import annotations
 
 import math
+import weakref
 from dataclasses import dataclass
 
 import torch
@@ -171,7 +172,7 @@ class ChunkedGPT2:
                     p.requires_grad_(True)
                     g = cs.grad[lo:lo + numel].view(pshape)
                     self._hooks.append(p.register_post_accumulate_grad_hook(
-                        _stash_into(g, self, ci)))
+                        _stash_into(g, weakref.ref(self), ci)))
                     self._chunk_nparams[ci] += 1
                 else:
                     buf = self._init_buf.setdefault(
@@ -544,10 +545,15 @@ class ActivationSwap:
             x.register_hook(lambda g, due=tuple(due): [self.prefetch(b) for b in due] and None)
 
 
-def _stash_into(slot: torch.Tensor, model: "ChunkedGPT2" = None, ci: int = -1):
+def _stash_into(slot: torch.Tensor, model_ref=None, ci: int = -1):
+    # The model is held WEAKLY: the hook lives in the parameter's C++ autograd
+    # metadata, invisible to Python's cycle collector, so a strong reference
+    # back to the model would keep the model -- and its chunk buffers -- alive
+    # forever (measured: a 26 GB profiling model never freed).
     def hook(p: torch.Tensor) -> None:
         slot.copy_(p.grad)
         p.grad = None
+        model = model_ref() if model_ref is not None else None
         if model is not None and model._overlap:
             model._pending[ci] -= 1
             if model._pending[ci] == 0:   # chunk ci's gradients are complete

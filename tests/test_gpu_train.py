@@ -447,3 +447,24 @@ def test_graphed_train_step_is_bit_identical(tmp_path, cuda_device, checkpoint):
     for a, b in zip(s, ref_s):
         assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
                            b.view(torch.int16) if b.dtype == torch.bfloat16 else b)
+
+
+def test_model_and_chunks_are_freed(tmp_path, cuda_device):
+    """A ChunkedGPT2 and its chunk buffers are released once dropped (no
+    reference cycle through the gradient hooks, which live in C++ autograd
+    metadata where Python's collector cannot see them)."""
+    import gc
+    from paper_2406_08334_b200.chunks import AdamHyper
+    from paper_2406_08334_b200.train import train_step
+    gc.collect()
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    model, shape = _setup(tmp_path, cuda_device)
+    x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device)
+    train_step(model, x, (x + 1) % shape.vocab, AdamHyper())
+    held = torch.cuda.memory_allocated()
+    assert held > base
+    del model
+    gc.collect()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= base + (1 << 20)
