@@ -651,12 +651,12 @@ fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t s
 // locally and the bf16 tile into every rank's parameter chunk (push
 // all-gather). Bytes in flight live in shared memory, not registers.
 // Tile shape per W (elements; threads = tile / 4), measured with virtual
-// ranks (profiles/README.md): W = 2 -> 2048, W = 1, 3 -> 1536, W >= 4 -> 1024.
+// ranks (profiles/README.md): W = 2 -> 2048, W = 1, 3, 4 -> 1536, W >= 5 -> 1024.
 // Smaller W means smaller stages; the wider tile keeps ~140-150 KB of loads
 // in flight per SM (tile 1024 at W = 2 reached only 0.66 of HBM).
 constexpr int kFusedSmemBudget = 220 * 1024;
 template <int W>
-__host__ __device__ constexpr int fused_tile() { return W == 1 ? 1536 : W == 2 ? 2048 : W == 3 ? 1536 : 1024; }
+__host__ __device__ constexpr int fused_tile() { return W == 1 ? 1536 : W == 2 ? 2048 : W <= 4 ? 1536 : 1024; }
 template <int W>
 __host__ __device__ constexpr int fused_threads() { return fused_tile<W>() / 4; }
 
@@ -1097,7 +1097,7 @@ const char* ptk_adam_kernel_name(void) {
 }
 
 const char* ptk_fused_kernel_name(void) {
-  return fused_use_tma() ? "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3, 1024 for W>=4; "
+  return fused_use_tma() ? "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for W>=5; "
                            "threads = tile/4; stages = min(9, 220 KB / stage))"
                          : "fused_peer_kernel (ldg)";
 }
