@@ -19,7 +19,14 @@ with exactly the plan the cost-model search picks from MEASURED inputs.
      estimate and the simulation, and the device peak against the model's.
 
     python scripts/train_large.py --model llama-13b --batch 8
+        [--chunk-bytes used,reference,used:refine] [--timeline] [--no-isolate]
 Writes gpurun_out/train_large_<model>_b<batch>.json (one row per --chunk-bytes mode).
+Each row also carries the simulation under the measured host-memory bandwidth
+(`memplan simulate --host-mem-bw`); ":refine" plans with --refine-sim under
+it; --timeline records a measured iteration in the simulator's event schema;
+every training attempt runs in its own child process (a failed attempt gives
+all device and pinned host memory back) and an OOM re-plans with a smaller
+device budget.
 """
 from __future__ import annotations
 
