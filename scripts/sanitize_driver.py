@@ -3,7 +3,7 @@
 compute-sanitizer racecheck / synccheck / initcheck, scripts/sanitize.sh):
 each chunk-Adam shape (TMA ring variants incl. the partial last tile, LDG),
 the f32-grad variant, grad stats / prep, clip coefficient, the fused
-RS->Adam->AG kernel (TMA ring) over 2 and 8 virtual ranks, the peer barrier, fills."""
+RS->Adam->AG kernel (TMA ring) over 2, 4 and 8 virtual ranks, the peer barrier, fills."""
 import ctypes
 import os
 import sys
@@ -53,15 +53,17 @@ def main():
         cs.attach_virtual_peers(sets)
     for cs in sets:
         cs.step(AdamHyper(lr=1e-3))
-    # the TMA fused kernel at W = 8: several full tiles per rank + a partial tile
-    sets8 = [ChunkSet([8 * 1024 * 3 + 80], world=8, rank=r, device=dev, mode="fused")
-             for r in range(8)]
-    for cs in sets8:
-        cs.init_synthetic()
-        cs.fill_grads(0)
-        cs.attach_virtual_peers(sets8)
-    for cs in sets8:
-        cs.step(AdamHyper(lr=1e-3))
+    # the TMA fused kernel at W = 4 (1536-element tiles) and W = 8 (1024):
+    # several full tiles per rank + a partial tile
+    for w, tile in ((4, 1536), (8, 1024)):
+        sets_w = [ChunkSet([w * tile * 3 + 8 * w * 5], world=w, rank=r, device=dev, mode="fused")
+                  for r in range(w)]
+        for cs in sets_w:
+            cs.init_synthetic()
+            cs.fill_grads(0)
+            cs.attach_virtual_peers(sets_w)
+        for cs in sets_w:
+            cs.step(AdamHyper(lr=1e-3))
     print("fused kernel in use:", nat.raw.ptk_fused_kernel_name().decode())
     sig = torch.zeros(nat.PTK_MAX_PEERS, dtype=torch.int32, device=dev)
     arr = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(sig.data_ptr())
