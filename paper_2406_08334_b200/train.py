@@ -416,6 +416,37 @@ def _norm(sh: GPT2Shape, x, w, b):
     return F.rms_norm(x, (sh.hidden,), w)
 
 
+class _BiasLinear(torch.autograd.Function):
+    """y = x W^T + b with the bias gradient as a GEMV (ones^T dY on cuBLAS)
+    instead of a column-sum reduction kernel over the (tokens x out) output
+    gradient: the reductions took 5.9 ms of a GPT-2 1.5B iteration
+    (scripts/train_breakdown.py). Forward and the x / W gradients are the
+    same GEMMs F.linear runs."""
+
+    @staticmethod
+    def forward(ctx, x, w, b):
+        ctx.save_for_backward(x, w)
+        return F.linear(x, w, b)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        gy2 = gy.reshape(-1, gy.shape[-1])
+        gx = gw = gb = None
+        if ctx.needs_input_grad[0]:
+            gx = (gy2 @ w).view(x.shape)
+        if ctx.needs_input_grad[1]:
+            gw = gy2.t() @ x.reshape(-1, x.shape[-1])
+        if ctx.needs_input_grad[2]:
+            ones = torch.ones(1, gy2.shape[0], dtype=gy2.dtype, device=gy2.device)
+            gb = (ones @ gy2).view(-1)
+        return gx, gw, gb
+
+
+def _linear(x, w, b):
+    return F.linear(x, w) if b is None else _BiasLinear.apply(x, w, b)
+
+
 def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor, mark=None) -> torch.Tensor:
     """One transformer block: the trace's attn_norm .. mlp_down operators.
     GPT-2: LayerNorm, fused QKV with bias, GELU MLP. Llama: RMSNorm, rotary
@@ -426,7 +457,7 @@ def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor, mark=None) -> torch
     hd = sh.hidden // sh.heads
     kvh = sh.kv_heads or sh.heads
     y = mark(0, _norm(sh, x, blk["ln1_w"], blk.get("ln1_b")))
-    qkv = mark(1, F.linear(y, blk["qkv_w"], blk.get("qkv_b")))
+    qkv = mark(1, _linear(y, blk["qkv_w"], blk.get("qkv_b")))
     q, k, v = qkv.split([sh.hidden, sh.kv_dim, sh.kv_dim], dim=-1)
     q, k, v = q.view(b, s, sh.heads, hd), k.view(b, s, kvh, hd), v.view(b, s, kvh, hd)
     if not sh.learned_pos:
@@ -434,16 +465,16 @@ def block_forward(sh: GPT2Shape, blk: dict, x: torch.Tensor, mark=None) -> torch
     a = mark(2, F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
                                                v.transpose(1, 2), is_causal=True,
                                                enable_gqa=kvh != sh.heads))
-    x = mark(3, x + F.linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"],
+    x = mark(3, x + _linear(a.transpose(1, 2).reshape(b, s, sh.hidden), blk["out_w"],
                              blk.get("out_b")))
     y = mark(4, _norm(sh, x, blk["ln2_w"], blk.get("ln2_b")))
-    y = mark(5, F.linear(y, blk["up_w"], blk.get("up_b")))
+    y = mark(5, _linear(y, blk["up_w"], blk.get("up_b")))
     if sh.gated:
         gate, up = y.chunk(2, dim=-1)
         y = mark(6, F.silu(gate) * up)
     else:
         y = mark(6, F.gelu(y, approximate="tanh"))
-    return mark(7, x + F.linear(y, blk["down_w"], blk.get("down_b")))
+    return mark(7, x + _linear(y, blk["down_w"], blk.get("down_b")))
 
 
 class ActivationSwap:

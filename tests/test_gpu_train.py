@@ -468,3 +468,24 @@ def test_model_and_chunks_are_freed(tmp_path, cuda_device):
     gc.collect()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() <= base + (1 << 20)
+
+
+def test_bias_linear_matches_f_linear(cuda_device):
+    """_BiasLinear (bias gradient as a GEMV) gives F.linear's output exactly
+    and its gradients within bf16 rounding of the reduction order."""
+    from paper_2406_08334_b200.train import _BiasLinear
+    g = torch.Generator(device=cuda_device).manual_seed(0)
+    x = torch.randn(4, 256, 320, device=cuda_device, dtype=torch.bfloat16, generator=g)
+    w = torch.randn(480, 320, device=cuda_device, dtype=torch.bfloat16, generator=g) * 0.05
+    b = torch.randn(480, device=cuda_device, dtype=torch.bfloat16, generator=g)
+    gy = torch.randn(4, 256, 480, device=cuda_device, dtype=torch.bfloat16, generator=g)
+    outs = []
+    for fn in (lambda x, w, b: torch.nn.functional.linear(x, w, b), _BiasLinear.apply):
+        xx, ww, bb = (t.detach().clone().requires_grad_(True) for t in (x, w, b))
+        y = fn(xx, ww, bb)
+        y.backward(gy)
+        outs.append((y.detach(), xx.grad, ww.grad, bb.grad))
+    (y0, gx0, gw0, gb0), (y1, gx1, gw1, gb1) = outs
+    assert torch.equal(y0, y1)
+    for a, c in ((gx0, gx1), (gw0, gw1), (gb0, gb1)):
+        torch.testing.assert_close(a.float(), c.float(), rtol=2e-2, atol=2e-2)
