@@ -456,17 +456,22 @@ def test_model_and_chunks_are_freed(tmp_path, cuda_device):
     import gc
     from paper_2406_08334_b200.chunks import AdamHyper
     from paper_2406_08334_b200.train import train_step
+    def one_model():
+        model, shape = _setup(tmp_path, cuda_device)
+        x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device)
+        train_step(model, x, (x + 1) % shape.vocab, AdamHyper())
+        held = torch.cuda.memory_allocated()
+        del model
+        gc.collect()
+        torch.cuda.synchronize()
+        return held
+
+    one_model()   # first use of cuBLAS etc. allocates process-lifetime workspaces
     gc.collect()
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated()
-    model, shape = _setup(tmp_path, cuda_device)
-    x = torch.randint(0, shape.vocab, (4, shape.seq), device=cuda_device)
-    train_step(model, x, (x + 1) % shape.vocab, AdamHyper())
-    held = torch.cuda.memory_allocated()
+    held = one_model()
     assert held > base
-    del model
-    gc.collect()
-    torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() <= base + (1 << 20)
 
 
