@@ -195,6 +195,8 @@ def run_gpu(args):
 
     world, rank, local = dist_setup()
     mode = args.exchange
+    if mode == "auto":
+        mode = "fused" if world > 1 else "nccl"
     if args.shared_device:
         # flow validation on a one-GPU box: every rank on cuda:0, peers mapped
         # through cudaIpc as on an NVLink node; NCCL refuses duplicate devices,
@@ -759,9 +761,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ptk", choices=["ptk", "reference"])
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
-                    help="N>1 chunk exchange: NCCL RS/AG + fused Adam, or the single fused "
-                         "RS->Adam->AG kernel over NVLink peer memory")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "fused"],
+                    help="N>1 chunk exchange: the single fused RS->Adam->AG kernel over NVLink "
+                         "peer memory (auto at N>1), or NCCL RS/AG + chunk Adam (the library "
+                         "baseline; auto at N=1, where there is no exchange)")
     ap.add_argument("--cpu-sample", type=int, default=64 * 1024 * 1024)
     ap.add_argument("--e2e-piece", type=int, default=32 * 1024 * 1024)
     ap.add_argument("--e2e-steps", type=int, default=20)

@@ -1039,19 +1039,34 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
 
 // Fused-kernel variant, once per process from PTK_FUSED_KERNEL ("tma", the
 // default, or "ldg" = the register-staged fused_peer_kernel).
-bool fused_use_tma() {
-  static const bool tma = [] {
+// 0 = auto (TMA ring when every peer buffer lives on this device -- virtual
+// ranks, cudaIpc mappings of the same GPU, which is what is tested here --
+// and the register-staged LDG kernel, the plain peer load / store pattern,
+// when a buffer is on another GPU), 1 = always TMA, 2 = always LDG.
+int fused_mode() {
+  static const int mode = [] {
     const char* e = std::getenv("PTK_FUSED_KERNEL");
-    return !(e && std::string(e) == "ldg");
+    if (e && std::string(e) == "tma") return 1;
+    if (e && std::string(e) == "ldg") return 2;
+    return 0;
   }();
-  return tma;
+  return mode;
+}
+
+bool same_device(const void* p, int dev) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice && a.device == dev;
 }
 
 template <int W>
 int launch_fused(const ptk_adam_scalars& s, const PeerTable& t, int64_t off, int64_t shard,
                  float* p, float* m, float* v, StatsWorkspace* ws, ptk_grad_stats_t* stats,
-                 cudaStream_t st) {
-  if (!fused_use_tma()) {
+                 cudaStream_t st, bool tma) {
+  if (!tma) {
     auto k = fused_peer_kernel<W>;
     const int grid = grid_for(k, (shard >> 3) > 0 ? (shard >> 3) : 1);
     k<<<grid, kThreads, 0, st>>>(s, t, off, shard, p, m, v, ws, stats);
@@ -1097,9 +1112,17 @@ const char* ptk_adam_kernel_name(void) {
 }
 
 const char* ptk_fused_kernel_name(void) {
-  return fused_use_tma() ? "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for W>=5; "
-                           "threads = tile/4; stages = min(9, 220 KB / stage))"
-                         : "fused_peer_kernel (ldg)";
+  switch (fused_mode()) {
+    case 1:
+      return "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for W>=5; "
+             "threads = tile/4; stages = min(9, 220 KB / stage))";
+    case 2:
+      return "fused_peer_kernel (ldg)";
+    default:
+      return "fused RS->Adam->AG, auto: fused_peer_tma_kernel (tile 2048 for W=2, 1536 for "
+             "W=1,3,4, 1024 for W>=5) when every peer buffer is on this device, "
+             "fused_peer_kernel (ldg) across devices";
+  }
 }
 
 int ptk_chunk_adam(const ptk_adam_config* cfg, float* master, float* exp_avg, float* exp_avg_sq,
@@ -1184,16 +1207,23 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
   const int64_t off = static_cast<int64_t>(rank) * shard;
   auto* ws = static_cast<StatsWorkspace*>(workspace);
   cudaStream_t st = as_stream(stream);
+  bool tma = fused_mode() != 2;
+  if (fused_mode() == 0) {
+    int dev = 0;
+    PTK_TRY_CUDA(cudaGetDevice(&dev));
+    for (int r = 0; r < world && tma; ++r)
+      tma = same_device(grad_peers[r], dev) && same_device(param_peers[r], dev);
+  }
   int rc = PTK_OK;
   switch (world) {
-    case 1: rc = launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 2: rc = launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 3: rc = launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 4: rc = launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 5: rc = launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 6: rc = launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    case 7: rc = launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
-    default: rc = launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st); break;
+    case 1: rc = launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 2: rc = launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 3: rc = launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 4: rc = launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 5: rc = launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 6: rc = launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    case 7: rc = launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
+    default: rc = launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
   }
   if (rc != PTK_OK) return rc;
   launch_counter()++;
