@@ -136,9 +136,11 @@ int ptk_clip_coef(const ptk_grad_stats_t* stats, double max_norm,
  * GPU optimizer task (proj/src/cost.cpp:206-219) and gather
  * (proj/src/hardware.cpp:29-34) of one chunk with ONE kernel: by default a
  * TMA ring (cp.async.bulk of the local state and of every rank's gradient
- * tile into shared memory, bulk stores of the bf16 tile into every rank);
- * PTK_FUSED_KERNEL=ldg selects the register-staged variant. Both are
- * bit-identical. shard must be a multiple of 8 elements. */
+ * tile into shared memory, bulk stores of the bf16 tile into every rank)
+ * when every peer buffer is on the calling device, the register-staged
+ * variant (128-bit peer loads / stores) when one is on another GPU;
+ * PTK_FUSED_KERNEL=tma|ldg forces one. Both are bit-identical. shard must be
+ * a multiple of 8 elements. */
 int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad_peers,
                          uint16_t* const* param_peers, int32_t world, int32_t rank,
                          int64_t shard, float* master, float* exp_avg,
