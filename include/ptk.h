@@ -83,7 +83,7 @@ int ptk_adam_derive(const ptk_adam_config* cfg, ptk_adam_scalars* out);
 int64_t ptk_shard_elems(int64_t n, int32_t world);
 /* name of the chunk-Adam kernel shape in use (PTK_ADAM_VARIANT or default) */
 const char* ptk_adam_kernel_name(void);
-/* name of the fused RS->Adam->AG kernel in use (PTK_FUSED_KERNEL=tma|ldg, default tma) */
+/* how the fused RS->Adam->AG kernel is chosen (PTK_FUSED_KERNEL=tma|ldg, or per table) */
 const char* ptk_fused_kernel_name(void);
 /* scratch: CTA partial buffer the reducing kernels need (bytes) */
 int64_t ptk_stats_workspace_bytes(void);
@@ -107,6 +107,31 @@ int ptk_chunk_adam_f32grad(const ptk_adam_config* cfg, float* master,
                            ptk_grad_stats_t* stats, void* workspace,
                            const float* gscale_dev, const int32_t* skip_dev,
                            void* stream);
+
+/* ---- K1 + K2 over a chunk TABLE: one launch per step --------------------
+ * The persistent TMA kernel walks every chunk of the table in one launch, so
+ * its shared-memory ring is filled and drained once per step instead of once
+ * per chunk (small chunks: ProTrain's 32-128 MiB chunk sizes). The table is
+ * built once (device copy owned by the handle) and may be used inside CUDA
+ * graph capture. Same per-element rule, statistics and device-side
+ * gscale/skip semantics as ptk_chunk_adam, bit-identical results. Replaces
+ * the per-chunk GpuOptim tasks of one iteration (proj/src/sim.cpp:245-250,
+ * 470-471) with one kernel. */
+typedef struct ptk_chunk_desc {
+  float* master;
+  float* exp_avg;
+  float* exp_avg_sq;
+  const uint16_t* grad;
+  uint16_t* param_out; /* nullable */
+  int64_t n;
+} ptk_chunk_desc;
+typedef struct ptk_chunk_table ptk_chunk_table;
+int ptk_chunk_table_create(const ptk_chunk_desc* descs, int32_t n_chunks, ptk_chunk_table** out);
+int ptk_chunk_table_destroy(ptk_chunk_table* table);
+int64_t ptk_chunk_table_params(const ptk_chunk_table* table);
+int ptk_chunk_adam_table(const ptk_adam_config* cfg, const ptk_chunk_table* table,
+                         ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                         const int32_t* skip_dev, void* stream);
 
 /* ---- K2 standalone: gradient statistics (+ optional fp32 scaled copy) --- */
 int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale,
@@ -147,6 +172,54 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
                          float* exp_avg_sq, ptk_grad_stats_t* stats,
                          void* workspace, void* stream);
 
+/* Table form of the fused step: every chunk of a rank in ONE launch (the
+ * ring stays full across chunks). kernel: PTK_FUSED_AUTO (PTK_FUSED_KERNEL
+ * env if set, else TMA when every peer buffer is on the calling device and
+ * the register-staged kernel otherwise -- decided once, here), PTK_FUSED_TMA
+ * or PTK_FUSED_LDG. gscale_dev / skip_dev as for ptk_chunk_adam (a device
+ * clip coefficient / overflow flag from ptk_stats_collect).
+ * ptk_fused_grad_stats_table is phase 1 of a clipped or overflow-checked
+ * step: the statistics of this rank's reduced, scaled gradient shards (the
+ * same fp32 rank-order sums), ADDED to *stats, no update. */
+#define PTK_FUSED_AUTO 0
+#define PTK_FUSED_TMA 1
+#define PTK_FUSED_LDG 2
+typedef struct ptk_fused_desc {
+  const uint16_t* grad_peers[PTK_MAX_PEERS];
+  uint16_t* param_peers[PTK_MAX_PEERS];
+  float* master;
+  float* exp_avg;
+  float* exp_avg_sq;
+  int64_t shard;
+} ptk_fused_desc;
+typedef struct ptk_fused_table ptk_fused_table;
+int ptk_fused_table_create(const ptk_fused_desc* descs, int32_t n_chunks, int32_t world,
+                           int32_t rank, int32_t kernel, ptk_fused_table** out);
+int ptk_fused_table_destroy(ptk_fused_table* table);
+/* the resolved kernel of a table: PTK_FUSED_TMA or PTK_FUSED_LDG */
+int32_t ptk_fused_table_kernel(const ptk_fused_table* table);
+int ptk_fused_step_table(const ptk_adam_config* cfg, const ptk_fused_table* table,
+                         ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                         const int32_t* skip_dev, void* stream);
+int ptk_fused_grad_stats_table(const ptk_adam_config* cfg, const ptk_fused_table* table,
+                               ptk_grad_stats_t* stats, void* workspace, void* stream);
+
+/* Statistics exchange over peer memory (global grad norm / overflow of the
+ * fused path, no NCCL): a mailbox is ptk_stats_mailbox_bytes() of device
+ * memory per rank (zeroed once, 32-byte aligned, peer-mapped like the
+ * signal slots). ptk_stats_publish stores this rank's *stats into slot
+ * [rank] of every rank's mailbox with a release-stored epoch;
+ * ptk_stats_collect waits (device-side, PTK_PEER_BARRIER_TIMEOUT_MS) for
+ * all `world` slots of the local mailbox to reach `epoch`, sums them in
+ * rank order (identical bits on every rank) into *global_out (nullable) and
+ * writes coef_out / skip_out (nullable) like ptk_clip_coef. */
+int64_t ptk_stats_mailbox_bytes(void);
+int ptk_stats_publish(const ptk_grad_stats_t* stats, void* const* mailbox_peers, int32_t world,
+                      int32_t rank, int32_t epoch, void* stream);
+int ptk_stats_collect(const void* mailbox, int32_t world, int32_t epoch, double max_norm,
+                      ptk_grad_stats_t* global_out, float* coef_out, int32_t* skip_out,
+                      void* stream);
+
 /* ---- synthetic inputs (SURVEY §8(d) counter-based generator) ----------- */
 /* out[i] = scale * u(seed, index0 + i), u in [-1, 1) exact in fp32 */
 int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, float scale,
@@ -178,6 +251,17 @@ int ptk_chunk_reduce_scatter(ptk_comm* comm, void* buf, int64_t shard_elems,
 int ptk_stats_allreduce(ptk_comm* comm, ptk_grad_stats_t* stats, void* stream);
 /* Device-side barrier over the communicator (an 1-element all-reduce). */
 int ptk_comm_barrier(ptk_comm* comm, void* stream);
+/* Failure detection (the reference simulator's DeadlockDetected,
+ * proj/src/sim.cpp:640-647, for the real exchange): ptk_comm_wait blocks the
+ * host until `stream` has drained, polling ncclCommGetAsyncError; on an
+ * asynchronous NCCL error, or when timeout_ms (> 0) elapses first (a hung or
+ * dead peer), it aborts the communicator (ncclCommAbort) and returns
+ * PTK_ENCCL. ptk_comm_async_error returns PTK_ENCCL if NCCL reported an
+ * asynchronous error. After ptk_comm_abort every collective call on the
+ * communicator fails with PTK_ENCCL; ptk_comm_destroy still frees it. */
+int ptk_comm_wait(ptk_comm* comm, void* stream, int64_t timeout_ms);
+int ptk_comm_async_error(ptk_comm* comm);
+int ptk_comm_abort(ptk_comm* comm);
 
 /* ---- NVLink peer memory for the fused path ---------------------------- */
 #define PTK_IPC_HANDLE_BYTES 64

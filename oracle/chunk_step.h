@@ -80,6 +80,7 @@ void oracle_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index
 void oracle_fill_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, int64_t index0,
                               float scale);
 int oracle_num_threads(void);
+void oracle_set_num_threads(int n);
 
 #ifdef __cplusplus
 }

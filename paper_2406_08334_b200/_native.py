@@ -45,6 +45,22 @@ class GradStats(Structure):
     _fields_ = [("sumsq", c_double), ("nonfinite", c_ulonglong)]
 
 
+class ChunkDesc(Structure):
+    """ptk_chunk_desc: one chunk shard of a ptk_chunk_table."""
+    _fields_ = [("master", c_void_p), ("exp_avg", c_void_p), ("exp_avg_sq", c_void_p),
+                ("grad", c_void_p), ("param_out", c_void_p), ("n", c_int64)]
+
+
+class FusedDesc(Structure):
+    """ptk_fused_desc: one chunk of a ptk_fused_table (every rank's buffers)."""
+    _fields_ = [("grad_peers", c_void_p * PTK_MAX_PEERS), ("param_peers", c_void_p * PTK_MAX_PEERS),
+                ("master", c_void_p), ("exp_avg", c_void_p), ("exp_avg_sq", c_void_p),
+                ("shard", c_int64)]
+
+
+PTK_FUSED_AUTO, PTK_FUSED_TMA, PTK_FUSED_LDG = 0, 1, 2
+
+
 # name -> (restype, argtypes); int-returning functions are status-checked.
 _SIGNATURES = {
     "ptk_last_error": (c_char_p, []),
@@ -70,6 +86,24 @@ _SIGNATURES = {
     "ptk_fused_rs_adam_ag": (c_int32, [POINTER(AdamConfig), POINTER(c_void_p), POINTER(c_void_p),
                                        c_int32, c_int32, c_int64, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p, c_void_p]),
+    "ptk_chunk_table_create": (c_int32, [POINTER(ChunkDesc), c_int32, POINTER(c_void_p)]),
+    "ptk_chunk_table_destroy": (c_int32, [c_void_p]),
+    "ptk_chunk_table_params": (c_int64, [c_void_p]),
+    "ptk_chunk_adam_table": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p]),
+    "ptk_fused_table_create": (c_int32, [POINTER(FusedDesc), c_int32, c_int32, c_int32, c_int32,
+                                         POINTER(c_void_p)]),
+    "ptk_fused_table_destroy": (c_int32, [c_void_p]),
+    "ptk_fused_table_kernel": (c_int32, [c_void_p]),
+    "ptk_fused_step_table": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p]),
+    "ptk_fused_grad_stats_table": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p,
+                                             c_void_p]),
+    "ptk_stats_mailbox_bytes": (c_int64, []),
+    "ptk_stats_publish": (c_int32, [c_void_p, POINTER(c_void_p), c_int32, c_int32, c_int32,
+                                    c_void_p]),
+    "ptk_stats_collect": (c_int32, [c_void_p, c_int32, c_int32, c_double, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
     "ptk_fill_uniform_f32": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
     "ptk_fill_uniform_bf16": (c_int32, [c_void_p, c_int64, c_uint64, c_int64, c_float, c_void_p]),
     "ptk_busy_wait": (c_int32, [c_int64, c_void_p]),
@@ -80,6 +114,9 @@ _SIGNATURES = {
     "ptk_chunk_reduce_scatter": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "ptk_comm_barrier": (c_int32, [c_void_p, c_void_p]),
     "ptk_stats_allreduce": (c_int32, [c_void_p, c_void_p, c_void_p]),
+    "ptk_comm_wait": (c_int32, [c_void_p, c_void_p, c_int64]),
+    "ptk_comm_async_error": (c_int32, [c_void_p]),
+    "ptk_comm_abort": (c_int32, [c_void_p]),
     "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8), POINTER(c_int64)]),
     "ptk_ipc_open_handle": (c_int32, [POINTER(c_uint8), POINTER(c_void_p)]),
     "ptk_ipc_close_handle": (c_int32, [c_void_p]),

@@ -22,14 +22,19 @@ What this executes is what the reference only models:
   proj/src/hardware.cpp:29-34).
 
 Two exchange modes:
-  "nccl"  — ptk_chunk_reduce_scatter / ptk_chunk_adam / ptk_chunk_allgather
-  "fused" — ptk_fused_rs_adam_ag, one kernel doing RS -> Adam -> AG over
-            peer pointers (NVLink P2P on a multi-GPU box), bracketed by
-            ptk_peer_barrier.
+  "nccl"  — ptk_chunk_reduce_scatter per chunk, ONE ptk_chunk_adam_table
+            launch over every chunk shard, ptk_chunk_allgather per chunk
+  "fused" — ptk_fused_step_table: ONE kernel doing RS -> Adam -> AG over
+            peer pointers (NVLink P2P on a multi-GPU box) for every chunk,
+            bracketed by ptk_peer_barrier. Global-norm clipping / overflow
+            skip add a statistics pass (ptk_fused_grad_stats_table) and a
+            peer-memory exchange of the 16-byte statistics
+            (ptk_stats_publish / ptk_stats_collect) before the update.
 """
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -143,12 +148,43 @@ class ChunkSet:
         ws_bytes = int(nat.raw.ptk_stats_workspace_bytes())
         self.workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device)
         self.stats = torch.zeros(2, dtype=torch.float64, device=self.device)  # ptk_grad_stats_t
+        self.clip_coef = torch.ones(1, dtype=F32, device=self.device)
+        self.skip_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.step_count = 0
         self.timeline = None         # timeline.Timeline: optim_start/end per chunk
         self.peer_grad_ptrs = None   # fused mode: per chunk (c_void_p * world)
         self.peer_param_ptrs = None
         self.signal_ptrs = None      # fused mode: (c_void_p * world) signal slots
+        self.mailbox_ptrs = None     # fused mode: (c_void_p * world) statistics mailboxes
+        self.fused_table = None      # ptk_fused_table over every chunk (peers attached)
         self.epoch = 0
+        self.stats_epoch = 0
+        self.mailbox = (torch.zeros(int(nat.raw.ptk_stats_mailbox_bytes()), dtype=torch.uint8,
+                                    device=self.device) if mode == "fused" else None)
+        # one ptk_chunk_table over this rank's shards: the step's Adam is ONE launch
+        descs = (nat.ChunkDesc * len(self.chunks))()
+        for d, c in zip(descs, self.chunks):
+            d.master, d.exp_avg, d.exp_avg_sq = (c.master.data_ptr(), c.exp_avg.data_ptr(),
+                                                 c.exp_avg_sq.data_ptr())
+            d.grad, d.param_out, d.n = c.grad_shard().data_ptr(), c.param_shard().data_ptr(), c.shard
+        self.table = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            nat.lib.ptk_chunk_table_create(descs, len(self.chunks), ctypes.byref(self.table))
+
+    def close(self) -> None:
+        """Releases the native chunk tables (also done on garbage collection)."""
+        for name, fn in (("table", "ptk_chunk_table_destroy"),
+                         ("fused_table", "ptk_fused_table_destroy")):
+            t = getattr(self, name, None)
+            if t is not None and t.value:
+                getattr(nat.raw, fn)(t)
+            setattr(self, name, None)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
     # ------------------------------------------------------------ sizes --
     @property
@@ -212,40 +248,50 @@ class ChunkSet:
         """One optimizer step over every chunk: RS -> Adam -> AG.
 
         With `max_grad_norm > 0` or `skip_nonfinite`, the global statistics
-        of the scaled gradient are needed BEFORE any update: all chunks are
-        reduce-scattered, ptk_grad_stats sums squares / counts non-finite
-        elements of every owned shard (warp-shuffle + CTA reductions), the
-        partial statistics are all-reduced over the ranks, ptk_clip_coef
-        turns them into a device-side clip coefficient and skip flag, and
-        every chunk's fused Adam reads both from device memory (no host
-        synchronisation anywhere)."""
+        of the scaled gradient are needed BEFORE any update. NCCL mode: all
+        chunks are reduce-scattered, ptk_grad_stats sums squares / counts
+        non-finite elements of every owned shard, the partial statistics are
+        all-reduced over the ranks and ptk_clip_coef turns them into a
+        device-side clip coefficient and skip flag. Fused mode: a statistics
+        pass over the reduced gradient of the owned shards
+        (ptk_fused_grad_stats_table), the partials exchanged through the
+        peer mailboxes (ptk_stats_publish / ptk_stats_collect, rank-order
+        sum: identical on every rank). Either way the update reads both from
+        device memory (no host synchronisation anywhere)."""
         self.step_count += 1
         cfg = hyper.config(self.step_count, self.world)
         s = stream_handle(stream)
         stats = vp(self.stats) if with_stats else ctypes.c_void_p(None)
-        if with_stats or max_grad_norm > 0 or skip_nonfinite:
+        clip = max_grad_norm > 0 or skip_nonfinite
+        if with_stats or clip:
             nat.lib.ptk_stats_reset(vp(self.stats), s)
-        if max_grad_norm > 0 or skip_nonfinite:
-            if self.mode == "fused":
-                raise ValueError("clipping needs the global norm before the update: use mode='nccl'")
+        if self.mode == "fused":
+            self._step_fused(cfg, s, stats, max_grad_norm, skip_nonfinite)
+            return
+        if clip:
             self._step_clipped(cfg, s, max_grad_norm, skip_nonfinite)
             return
-        if self.mode == "fused":
-            self._step_fused(cfg, s, stats)
-            return
         tl = self.timeline
-        for c in self.chunks:
-            if tl is not None:
+        if tl is not None:  # per-chunk launches so every chunk's optim span is timed
+            for c in self.chunks:
                 tl.gpu(stream, "gpu", "optim_start", f"chunk={c.chunk_id + 1}")
-            if self.comm is not None:
-                nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
-            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
-                                   vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
-                                   c.shard, stats, vp(self.workspace), None, None, s)
-            if self.comm is not None:
-                nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
-            if tl is not None:
+                if self.comm is not None:
+                    nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
+                nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg),
+                                       vp(c.exp_avg_sq), vp(c.grad_shard()), vp(c.param_shard()),
+                                       c.shard, stats, vp(self.workspace), None, None, s)
+                if self.comm is not None:
+                    nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
                 tl.gpu(stream, "gpu", "optim_end", f"chunk={c.chunk_id + 1}")
+            return
+        if self.comm is not None:
+            for c in self.chunks:
+                nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
+        nat.lib.ptk_chunk_adam_table(ctypes.byref(cfg), self.table, stats, vp(self.workspace),
+                                     None, None, s)
+        if self.comm is not None:
+            for c in self.chunks:
+                nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
 
     # ----------------------------------------------- overlapped (per chunk) --
     def begin_overlapped_step(self, hyper: AdamHyper, side: torch.cuda.Stream) -> None:
@@ -295,9 +341,6 @@ class ChunkSet:
         self._ov_side = None
 
     def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
-        if not hasattr(self, "clip_coef"):
-            self.clip_coef = torch.ones(1, dtype=F32, device=self.device)
-            self.skip_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         for c in self.chunks:
             if self.comm is not None:
                 nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(c.grad), c.shard, 0, s)
@@ -307,27 +350,75 @@ class ChunkSet:
             nat.lib.ptk_stats_allreduce(self.comm, vp(self.stats), s)
         nat.lib.ptk_clip_coef(vp(self.stats), max_grad_norm, vp(self.clip_coef),
                               vp(self.skip_flag) if skip_nonfinite else None, s)
-        for c in self.chunks:
-            nat.lib.ptk_chunk_adam(ctypes.byref(cfg), vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq),
-                                   vp(c.grad_shard()), vp(c.param_shard()), c.shard, None, None,
-                                   vp(self.clip_coef), vp(self.skip_flag) if skip_nonfinite else None,
-                                   s)
-            if self.comm is not None:
+        nat.lib.ptk_chunk_adam_table(ctypes.byref(cfg), self.table, None, None, vp(self.clip_coef),
+                                     vp(self.skip_flag) if skip_nonfinite else None, s)
+        if self.comm is not None:
+            for c in self.chunks:
                 nat.lib.ptk_chunk_allgather(self.comm, vp(c.param), c.shard, 0, s)
 
-    def _step_fused(self, cfg, s, stats) -> None:
-        if self.peer_grad_ptrs is None:
+    def _step_fused(self, cfg, s, stats, max_grad_norm: float = 0.0,
+                    skip_nonfinite: bool = False) -> None:
+        if self.fused_table is None:
             raise RuntimeError("fused mode needs peer pointers (attach_virtual_peers / attach_ipc_peers)")
+        clip = max_grad_norm > 0 or skip_nonfinite
+        if clip and self.signal_ptrs is None and self.world > 1:
+            raise ValueError("virtual ranks share one stream: a clipped fused step must be issued "
+                             "for all of them together (fused_group_step)")
         if self.signal_ptrs is not None:
             self.epoch += 1
             nat.lib.ptk_peer_barrier(self.signal_ptrs, self.world, self.rank, self.epoch, s)
-        for c, gp, pp in zip(self.chunks, self.peer_grad_ptrs, self.peer_param_ptrs):
-            nat.lib.ptk_fused_rs_adam_ag(ctypes.byref(cfg), gp, pp, self.world, self.rank, c.shard,
-                                         vp(c.master), vp(c.exp_avg), vp(c.exp_avg_sq), stats,
-                                         vp(self.workspace), s)
+        if clip:
+            self._fused_stats_phase(cfg, s)
+            self._fused_publish(s)
+            self._fused_collect(s, max_grad_norm, skip_nonfinite)
+            self._fused_update(cfg, s, None, clip=True, skip=skip_nonfinite)
+        else:
+            self._fused_update(cfg, s, stats)
         if self.signal_ptrs is not None:
             self.epoch += 1
             nat.lib.ptk_peer_barrier(self.signal_ptrs, self.world, self.rank, self.epoch, s)
+
+    # The phases of a fused step (fused_group_step issues them rank by rank
+    # for virtual ranks sharing one stream).
+    def _fused_stats_phase(self, cfg, s) -> None:
+        nat.lib.ptk_fused_grad_stats_table(ctypes.byref(cfg), self.fused_table, vp(self.stats),
+                                           vp(self.workspace), s)
+
+    def _fused_publish(self, s) -> None:
+        self.stats_epoch += 1
+        nat.lib.ptk_stats_publish(vp(self.stats), self.mailbox_ptrs, self.world, self.rank,
+                                  self.stats_epoch, s)
+
+    def _fused_collect(self, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
+        nat.lib.ptk_stats_collect(vp(self.mailbox), self.world, self.stats_epoch, max_grad_norm,
+                                  vp(self.stats), vp(self.clip_coef),
+                                  vp(self.skip_flag) if skip_nonfinite else None, s)
+
+    def _fused_update(self, cfg, s, stats, clip: bool = False, skip: bool = False) -> None:
+        nat.lib.ptk_fused_step_table(ctypes.byref(cfg), self.fused_table, stats,
+                                     vp(self.workspace), vp(self.clip_coef) if clip else None,
+                                     vp(self.skip_flag) if skip else None, s)
+
+    def _build_fused_table(self, kernel: int) -> None:
+        if self.fused_table is not None:
+            nat.raw.ptk_fused_table_destroy(self.fused_table)
+        descs = (nat.FusedDesc * len(self.chunks))()
+        for d, c, gp, pp in zip(descs, self.chunks, self.peer_grad_ptrs, self.peer_param_ptrs):
+            for r in range(self.world):
+                d.grad_peers[r], d.param_peers[r] = gp[r], pp[r]
+            d.master, d.exp_avg, d.exp_avg_sq = (c.master.data_ptr(), c.exp_avg.data_ptr(),
+                                                 c.exp_avg_sq.data_ptr())
+            d.shard = c.shard
+        self.fused_table = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            nat.lib.ptk_fused_table_create(descs, len(self.chunks), self.world, self.rank, kernel,
+                                           ctypes.byref(self.fused_table))
+
+    @property
+    def fused_kernel(self) -> str:
+        """'tma' or 'ldg': the fused kernel this rank's table runs."""
+        k = int(nat.raw.ptk_fused_table_kernel(self.fused_table)) if self.fused_table else -1
+        return {nat.PTK_FUSED_TMA: "tma", nat.PTK_FUSED_LDG: "ldg"}.get(k, "none")
 
     def attach_virtual_peers(self, sets: list["ChunkSet"]) -> None:
         """Single-GPU validation of the fused path: `sets[r]` plays rank r.
@@ -340,6 +431,9 @@ class ChunkSet:
             p = arr(*[sets[r].chunks[ci].param.data_ptr() for r in range(self.world)])
             self.peer_grad_ptrs.append(g)
             self.peer_param_ptrs.append(p)
+        self.mailbox_ptrs = arr(*[sets[r].mailbox.data_ptr() for r in range(self.world)])
+        # every buffer is on this device: the TMA ring (PTK_FUSED_KERNEL may force one)
+        self._build_fused_table(fused_kernel_choice(same_device=True))
 
     def attach_ipc_peers(self, group=None) -> None:
         """Multi-GPU fused mode: map every peer's gradient / parameter chunk
@@ -349,24 +443,29 @@ class ChunkSet:
         import torch.distributed as dist
         arr = ctypes.c_void_p * PTK_MAX
         self.signal = torch.zeros(PTK_MAX, dtype=torch.int32, device=self.device)
+        bufs = ([c.grad for c in self.chunks] + [c.param for c in self.chunks] +
+                [self.signal, self.mailbox])
         mine = []
-        for t in [c.grad for c in self.chunks] + [c.param for c in self.chunks] + [self.signal]:
+        for t in bufs:
             h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
             off = ctypes.c_int64()
             nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
             mine.append((bytes(h), off.value))
         torch.cuda.synchronize(self.device)
+        # the physical GPU of every rank (UUID, not an ordinal: ranks may be
+        # isolated with CUDA_VISIBLE_DEVICES) decides the fused kernel once
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
         everyone = [None] * self.world
-        dist.all_gather_object(everyone, mine, group=group)
+        dist.all_gather_object(everyone, (uuid, mine), group=group)
+        same_device = all(u == uuid for u, _ in everyone)
+        everyone = [m for _, m in everyone]
         self._opened = []
         ptrs = []  # ptrs[r][k]: rank r's k-th buffer as mapped here
         for r in range(self.world):
             row = []
             for k, (hb, off) in enumerate(everyone[r]):
                 if r == self.rank:
-                    own = ([c.grad for c in self.chunks] + [c.param for c in self.chunks] +
-                           [self.signal])[k]
-                    row.append(own.data_ptr())
+                    row.append(bufs[k].data_ptr())
                     continue
                 base = ctypes.c_void_p()
                 nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
@@ -379,7 +478,10 @@ class ChunkSet:
         self.peer_param_ptrs = [arr(*[ptrs[r][n + ci] for r in range(self.world)])
                                 for ci in range(n)]
         self.signal_ptrs = arr(*[ptrs[r][2 * n] for r in range(self.world)])
+        self.mailbox_ptrs = arr(*[ptrs[r][2 * n + 1] for r in range(self.world)])
         self.epoch = 0
+        self.stats_epoch = 0
+        self._build_fused_table(fused_kernel_choice(same_device))
         dist.barrier(group=group)
 
     def close_ipc_peers(self) -> None:
@@ -395,3 +497,46 @@ class ChunkSet:
 
 
 PTK_MAX = nat.PTK_MAX_PEERS
+
+
+def fused_kernel_choice(same_device: bool) -> int:
+    """The fused kernel for a peer table: PTK_FUSED_KERNEL=tma|ldg if set,
+    else the TMA ring when every rank's buffers are on this GPU (virtual
+    ranks, same-device cudaIpc) and the register-staged kernel (plain
+    128-bit peer loads / stores) across GPUs. Chosen once per table."""
+    env = os.environ.get("PTK_FUSED_KERNEL", "")
+    if env == "tma":
+        return nat.PTK_FUSED_TMA
+    if env == "ldg":
+        return nat.PTK_FUSED_LDG
+    return nat.PTK_FUSED_TMA if same_device else nat.PTK_FUSED_LDG
+
+
+def fused_group_step(sets: list[ChunkSet], hyper: AdamHyper, stream=None, with_stats: bool = True,
+                     max_grad_norm: float = 0.0, skip_nonfinite: bool = False) -> None:
+    """One fused step of W VIRTUAL ranks sharing a device and a stream
+    (single-GPU validation of the N>1 path): without clipping, each rank's
+    fused launch in turn; with clipping / overflow skip, every rank's
+    statistics pass, then every publish, every collect, every update -- the
+    order the peer mailboxes need when the ranks cannot run concurrently."""
+    clip = max_grad_norm > 0 or skip_nonfinite
+    if not clip:
+        for cs in sets:
+            cs.step(hyper, stream=stream, with_stats=with_stats)
+        return
+    s = stream_handle(stream)
+    cfgs = []
+    for cs in sets:
+        if cs.fused_table is None or cs.signal_ptrs is not None:
+            raise ValueError("fused_group_step drives virtual ranks (attach_virtual_peers)")
+        cs.step_count += 1
+        cfgs.append(hyper.config(cs.step_count, cs.world))
+        nat.lib.ptk_stats_reset(vp(cs.stats), s)
+    for cs, cfg in zip(sets, cfgs):
+        cs._fused_stats_phase(cfg, s)
+    for cs in sets:
+        cs._fused_publish(s)
+    for cs in sets:
+        cs._fused_collect(s, max_grad_norm, skip_nonfinite)
+    for cs, cfg in zip(sets, cfgs):
+        cs._fused_update(cfg, s, None, clip=True, skip=skip_nonfinite)

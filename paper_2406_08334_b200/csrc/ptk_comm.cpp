@@ -9,8 +9,10 @@
 // (proj/src/sim.cpp:335-350,428-436).
 #include <nccl.h>
 
+#include <chrono>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "ptk_common.h"
 
@@ -19,6 +21,7 @@ struct ptk_comm {
   int world = 1;
   int rank = 0;
   void* scratch = nullptr;  // 1 float for the barrier all-reduce
+  bool aborted = false;     // after ptk_comm_abort / a failed ptk_comm_wait
 };
 
 namespace {
@@ -31,7 +34,21 @@ int check_nccl(ncclResult_t r, const char* what) {
 ncclDataType_t to_nccl(int32_t dtype) { return dtype == 1 ? ncclFloat32 : ncclBfloat16; }
 size_t elem_bytes(int32_t dtype) { return dtype == 1 ? 4 : 2; }
 
+// Every collective entry point refuses an aborted communicator loudly.
+int usable(const ptk_comm* c, const char* what) {
+  if (!c) return ptk::fail(PTK_EINVAL, std::string(what) + ": null comm");
+  if (c->aborted || !c->comm)
+    return ptk::fail(PTK_ENCCL, std::string(what) + ": communicator was aborted");
+  return PTK_OK;
+}
+
 }  // namespace
+
+#define PTK_TRY_USABLE(c, what)                 \
+  do {                                          \
+    int ptk_rc_ = usable((c), (what));          \
+    if (ptk_rc_ != PTK_OK) return ptk_rc_;      \
+  } while (0)
 
 #define PTK_TRY_NCCL(expr)                                \
   do {                                                    \
@@ -82,9 +99,63 @@ int ptk_comm_destroy(ptk_comm* c) {
   return rc;
 }
 
+// Failure detection of the NCCL path (the analogue of the reference
+// simulator's DeadlockDetected, proj/src/sim.cpp:640-647): a hung or failed
+// peer must not hang the job. ptk_comm_wait polls the stream and the
+// communicator's asynchronous error state; on an async error or after
+// timeout_ms it aborts the communicator (ncclCommAbort releases the NCCL
+// kernels still waiting on the stream) and returns PTK_ENCCL.
+int ptk_comm_abort(ptk_comm* c) {
+  if (!c) return ptk::fail(PTK_EINVAL, "ptk_comm_abort: null comm");
+  if (c->comm) {
+    const ncclResult_t r = ncclCommAbort(c->comm);
+    c->comm = nullptr;
+    c->aborted = true;
+    return check_nccl(r, "ncclCommAbort");
+  }
+  c->aborted = true;
+  return PTK_OK;
+}
+
+int ptk_comm_async_error(ptk_comm* c) {
+  PTK_TRY_USABLE(c, "ptk_comm_async_error");
+  ncclResult_t async = ncclSuccess;
+  PTK_TRY_NCCL(ncclCommGetAsyncError(c->comm, &async));
+  if (async == ncclSuccess || async == ncclInProgress) return PTK_OK;
+  return ptk::fail(PTK_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(async));
+}
+
+int ptk_comm_wait(ptk_comm* c, void* stream, int64_t timeout_ms) {
+  PTK_TRY_USABLE(c, "ptk_comm_wait");
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(ptk::as_stream(stream));
+    if (q == cudaSuccess) return PTK_OK;
+    if (q != cudaErrorNotReady) return ptk::check_cuda(q, "ptk_comm_wait: stream");
+    ncclResult_t async = ncclSuccess;
+    if (ncclCommGetAsyncError(c->comm, &async) != ncclSuccess ||
+        (async != ncclSuccess && async != ncclInProgress)) {
+      const std::string why = ncclGetErrorString(async);
+      ptk_comm_abort(c);
+      return ptk::fail(PTK_ENCCL, "ptk_comm_wait: NCCL asynchronous error (" + why +
+                                      "); communicator aborted");
+    }
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                        std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms > timeout_ms) {
+      ptk_comm_abort(c);
+      return ptk::fail(PTK_ENCCL, "ptk_comm_wait: stream not drained after " +
+                                      std::to_string(timeout_ms) +
+                                      " ms (hung peer?); communicator aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
 int ptk_chunk_allgather(ptk_comm* c, void* buf, int64_t shard_elems, int32_t dtype,
                         void* stream) {
-  if (!c || !buf || shard_elems < 0) return ptk::fail(PTK_EINVAL, "ptk_chunk_allgather: bad arguments");
+  PTK_TRY_USABLE(c, "ptk_chunk_allgather");
+  if (!buf || shard_elems < 0) return ptk::fail(PTK_EINVAL, "ptk_chunk_allgather: bad arguments");
   if (shard_elems == 0) return PTK_OK;  // w = 1 still goes through NCCL (a local copy)
   char* base = static_cast<char*>(buf);
   const void* send = base + static_cast<size_t>(c->rank) * shard_elems * elem_bytes(dtype);
@@ -95,7 +166,8 @@ int ptk_chunk_allgather(ptk_comm* c, void* buf, int64_t shard_elems, int32_t dty
 
 int ptk_chunk_reduce_scatter(ptk_comm* c, void* buf, int64_t shard_elems, int32_t dtype,
                              void* stream) {
-  if (!c || !buf || shard_elems < 0)
+  PTK_TRY_USABLE(c, "ptk_chunk_reduce_scatter");
+  if (!buf || shard_elems < 0)
     return ptk::fail(PTK_EINVAL, "ptk_chunk_reduce_scatter: bad arguments");
   if (shard_elems == 0) return PTK_OK;  // w = 1 still goes through NCCL (a local copy)
   char* base = static_cast<char*>(buf);
@@ -106,7 +178,8 @@ int ptk_chunk_reduce_scatter(ptk_comm* c, void* buf, int64_t shard_elems, int32_
 }
 
 int ptk_stats_allreduce(ptk_comm* c, ptk_grad_stats_t* stats, void* stream) {
-  if (!c || !stats) return ptk::fail(PTK_EINVAL, "ptk_stats_allreduce: null argument");
+  PTK_TRY_USABLE(c, "ptk_stats_allreduce");
+  if (!stats) return ptk::fail(PTK_EINVAL, "ptk_stats_allreduce: null argument");
   PTK_TRY_NCCL(ncclGroupStart());
   PTK_TRY_NCCL(ncclAllReduce(&stats->sumsq, &stats->sumsq, 1, ncclFloat64, ncclSum, c->comm,
                              ptk::as_stream(stream)));
@@ -117,7 +190,7 @@ int ptk_stats_allreduce(ptk_comm* c, ptk_grad_stats_t* stats, void* stream) {
 }
 
 int ptk_comm_barrier(ptk_comm* c, void* stream) {
-  if (!c) return ptk::fail(PTK_EINVAL, "ptk_comm_barrier: null comm");
+  PTK_TRY_USABLE(c, "ptk_comm_barrier");
   PTK_TRY_NCCL(ncclAllReduce(c->scratch, c->scratch, 1, ncclFloat32, ncclSum, c->comm,
                              ptk::as_stream(stream)));
   return PTK_OK;

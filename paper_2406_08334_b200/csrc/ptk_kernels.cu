@@ -1,33 +1,40 @@
 // libptk device kernels for sm_100a: the chunk data plane of ProTrain.
 //
-//   K1+K2  chunk_adam_kernel     fused grad cast/scale + grad-norm/overflow
-//                                statistics + Adam/AdamW over a flat chunk
-//                                shard (28 B/param of HBM traffic, bf16 grad)
-//   K2     grad_stats_kernel     standalone statistics (+ fp32 scaled copy)
-//   K1+K3+K4 fused_peer_kernel   reduce-scatter (fp32 sum over NVLink peer
-//                                loads) -> Adam -> all-gather (peer stores)
-//   aux    fill kernels (counter-based synthetic inputs), clip coefficient,
-//          peer barrier (system-scope release/acquire flags)
+//   K1+K2    chunk_adam_tma_kernel  fused grad cast/scale + grad-norm/overflow
+//                                   statistics + Adam/AdamW over a TABLE of flat
+//                                   chunk shards in ONE launch (28 B/param of
+//                                   HBM traffic, bf16 grad): a TMA bulk ring
+//   K1+K2    chunk_adam_kernel      register-staged variant (fp32 grads, "ldg")
+//   K2       grad_stats_kernel      standalone statistics (+ fp32 scaled copy)
+//   K1+K3+K4 fused_peer_tma_kernel  reduce-scatter (fp32 rank-order sum of every
+//            fused_peer_kernel      rank's gradient tile read over NVLink) ->
+//                                   Adam -> all-gather (push of the bf16 tile
+//                                   into every rank), over a chunk table
+//   K2'      fused_stats_kernel     phase 1 of a clipped fused step: statistics
+//                                   of the reduced gradient, no update
+//   aux      stats mailbox (publish / collect of per-rank statistics over peer
+//            memory), clip coefficient, peer barrier, fill kernels
 //
 // The modeled counterparts in the reference are listed in include/ptk.h.
-// Design notes: every kernel is HBM-streaming integer/fp32
-// element work — no data reuse, so no tensor cores and no shared-memory
-// tiling; the levers are 128-bit coalesced accesses, enough bytes in flight
-// per SM (UNROLL independent 8-element units per thread, all loads issued
-// before any math), a persistent grid sized to the SM count × occupancy,
-// streaming cache hints (.cs) so the once-touched chunk bytes do not thrash
-// L2, and deterministic warp-shuffle → CTA → last-CTA reductions for the
-// statistics. The update arithmetic uses explicit round-to-nearest
-// intrinsics (no FMA contraction) so it matches oracle/chunk_step.c bit for
-// bit.
+// Design notes: every kernel is HBM-streaming element work —
+// no data reuse, so no tensor cores; the levers are 128-bit / TMA bulk
+// accesses, enough bytes in flight per SM (a shared-memory ring, not
+// registers), a persistent grid of one CTA per SM that walks every chunk of
+// the step (the ring stays full across chunk boundaries: one fill and one
+// drain per step, not per chunk), and deterministic warp-shuffle → CTA →
+// last-CTA reductions for the statistics. The update arithmetic uses explicit
+// round-to-nearest intrinsics (no FMA contraction) so it matches
+// oracle/chunk_step.c bit for bit.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cctype>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "ptk_common.h"
 
@@ -36,6 +43,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxGrid = 4096;
+constexpr int kMaxDevices = 64;
 
 struct StatsWorkspace {
   double sq[kMaxGrid];
@@ -108,17 +116,23 @@ __device__ __forceinline__ float adam_elem(const ptk_adam_scalars& s, float g, f
   return p;
 }
 
-// Statistics: squares are summed in fp32 over one 8-element unit, the unit
-// sums in fp64 per thread (keeps the full-chunk sum within ~1e-7 relative).
+// Statistics: squares are summed in fp32 over one 4- or 8-element unit, the
+// unit sums in fp64 per thread (keeps the full-step sum within ~1e-7 relative).
 __device__ __forceinline__ void accum_stats(float g, float& sq, unsigned& bad) {
   sq = __fmaf_rn(g, g, sq);
   bad += isfinite(g) ? 0u : 1u;
 }
 
+// Effective gradient scale of a launch: the host scalar times the optional
+// device multiplier (a clip coefficient); skip_dev != 0 makes it a no-op.
+__device__ __forceinline__ float launch_gscale(const ptk_adam_scalars& s, const float* gscale_dev) {
+  return gscale_dev != nullptr ? __fmul_rn(s.gscale, *gscale_dev) : s.gscale;
+}
+
 // Deterministic grid reduction: warp shuffle -> CTA (fixed order) -> the last
-// CTA to arrive sums the per-CTA partials in index order and ADDS the result
-// to *stats. Safe across back-to-back launches on one stream (the arrival
-// counter is re-armed by the last CTA).
+// CTA to arrive sums the per-CTA partials in a fixed lane-strided order + xor
+// tree and ADDS the result to *stats. Safe across back-to-back launches on
+// one stream (the arrival counter is re-armed by the last CTA).
 __device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorkspace* ws,
                                              ptk_grad_stats_t* stats) {
   __shared__ double s_sq[32];
@@ -151,8 +165,6 @@ __device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorks
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // one warp: lane l sums partials l, l+32, ... then a fixed xor tree, so the
-  // total is the same every run (and not a 148-long serial chain of L2 loads)
   if (threadIdx.x < 32) {
     double tsq = 0.0;
     unsigned long long tbad = 0;
@@ -176,18 +188,18 @@ __device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorks
 }
 
 // ------------------------------------------------------------ K1 + K2 ----
+// Register-staged chunk Adam (one chunk per launch): U independent 8-element
+// units per thread with every load issued before any math. Used for fp32
+// gradients (ptk_chunk_adam_f32grad) and as the "ldg" variant.
 
 template <class G, int U, bool kStats>
-__device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict__ master,
-                                          float* __restrict__ exp_avg,
-                                          float* __restrict__ exp_avg_sq,
-                                          const typename G::T* __restrict__ grad,
-                                          uint16_t* __restrict__ param_out, int64_t n,
-                                          StatsWorkspace* ws, ptk_grad_stats_t* stats,
-                                          const float* gscale_dev, const int32_t* skip_dev) {
+__global__ void __launch_bounds__(kThreads)
+chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
+                  float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
+                  uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
+                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
   if (skip_dev != nullptr && *skip_dev != 0) return;  // grid-uniform
-  float gs = s.gscale;
-  if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
+  const float gs = launch_gscale(s, gscale_dev);
   double sq = 0.0;
   unsigned bad = 0;
 
@@ -195,7 +207,6 @@ __device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict_
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
 
-  // Main loop: U independent 8-element units per thread, loads first.
   for (; i + (U - 1) * stride < nvec; i += U * stride) {
     float p[U][8], m[U][8], v[U][8], g[U][8];
 #pragma unroll
@@ -223,7 +234,6 @@ __device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict_
       if (param_out != nullptr) __stcs(reinterpret_cast<uint4*>(param_out + e), pack8(p[u]));
     }
   }
-  // Remainder units.
   for (; i < nvec; i += stride) {
     const int64_t e = i << 3;
     float p[8], m[8], v[8], g[8];
@@ -244,8 +254,7 @@ __device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict_
     st8f(exp_avg_sq + e, v);
     if (param_out != nullptr) __stcs(reinterpret_cast<uint4*>(param_out + e), pack8(p));
   }
-  // Scalar tail (< 8 elements) on CTA 0.
-  const int64_t t0 = nvec << 3;
+  const int64_t t0 = nvec << 3;  // scalar tail (< 8 elements) on CTA 0
   if (blockIdx.x == 0 && threadIdx.x < n - t0) {
     const int64_t e = t0 + threadIdx.x;
     const float gk = __fmul_rn(G::load1(grad + e), gs);
@@ -262,38 +271,7 @@ __device__ __forceinline__ void adam_body(ptk_adam_scalars s, float* __restrict_
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
 
-template <class G, int U, bool kStats>
-__global__ void __launch_bounds__(kThreads)
-chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
-                  float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
-                  uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
-                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
-  adam_body<G, U, kStats>(s, master, exp_avg, exp_avg_sq, grad, param_out, n, ws, stats,
-                          gscale_dev, skip_dev);
-}
-
-// Same body, higher occupancy (launch bounds force <= 64 registers).
-template <class G, int U, bool kStats, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-chunk_adam_occ_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
-                      float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
-                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
-                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
-  adam_body<G, U, kStats>(s, master, exp_avg, exp_avg_sq, grad, param_out, n, ws, stats,
-                          gscale_dev, skip_dev);
-}
-
-// ------------------------------------------- K1 + K2, TMA bulk pipeline --
-//
-// Persistent CTAs walk whole tiles of kTile elements. One elected thread
-// moves every tile with 1-D bulk copies (cp.async.bulk, the TMA engine):
-// master/m/v/grad global -> shared, completion counted on an mbarrier
-// (complete_tx), and after the update master/m/v/param shared -> global as a
-// bulk_group. kStages tiles of shared memory form a ring; the producer runs
-// kStages-2 tiles ahead of the consumers, and a stage is refilled only after
-// the bulk store that last read it has finished reading shared memory
-// (cp.async.bulk.wait_group.read 1). Register pressure no longer limits the
-// bytes in flight: they live in shared memory.
+// ---------------------------------------------------- TMA bulk primitives --
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -331,8 +309,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-// Variants with an L2 eviction-priority hint (createpolicy evict_first): the
-// chunk bytes are touched once per step, so they need not compete for L2.
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -375,6 +351,95 @@ __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------------------------ chunk tables --
+//
+// A step's chunks are described by a table (device memory, built once by
+// ptk_chunk_table_create / ptk_fused_table_create) or, for the single-chunk
+// entry points, by one descriptor passed in the launch parameters. Every
+// chunk's multiple-of-8 prefix is cut into tiles of the kernel's tile size;
+// tile0 = index of the chunk's first tile in the step's global tile order.
+// CTA b walks global tiles b, b + G, b + 2G, ... across chunk boundaries, so
+// the TMA ring is filled once per step. The < 8 trailing elements of a chunk
+// whose length is not a multiple of 8 (never the case for padded shards) are
+// updated with plain loads by CTA (chunk % G) after the ring drains.
+
+struct ChunkDesc {
+  float* master;
+  float* m;
+  float* v;
+  const uint16_t* grad;
+  uint16_t* param;  // nullable
+  int64_t n;
+  int64_t tile0;
+};
+
+struct ChunkList {
+  const ChunkDesc* table;  // device table of n_chunks descriptors, or nullptr -> `one`
+  ChunkDesc one;
+  int64_t total_tiles;
+  int32_t n_chunks;
+};
+
+__device__ __forceinline__ const ChunkDesc& chunk_at(const ChunkList& l, int c) {
+  return l.table != nullptr ? l.table[c] : l.one;
+}
+
+struct FusedDesc {
+  const uint16_t* grad[PTK_MAX_PEERS];  // rank r's full gradient chunk
+  uint16_t* param[PTK_MAX_PEERS];       // rank r's full parameter chunk
+  float* master;                        // this rank's shard state
+  float* m;
+  float* v;
+  int64_t shard;  // elements per rank (multiple of 8)
+  int64_t tile0;
+};
+
+struct FusedList {
+  const FusedDesc* table;
+  FusedDesc one;
+  int64_t total_tiles;
+  int32_t n_chunks;
+  int32_t rank;
+};
+
+__device__ __forceinline__ const FusedDesc& fused_at(const FusedList& l, int c) {
+  return l.table != nullptr ? l.table[c] : l.one;
+}
+
+// Producer-side cursor over the global tile order (monotone per CTA).
+struct TileCursor {
+  int c = 0;
+  int64_t end = 0;
+};
+
+__device__ __forceinline__ const ChunkDesc& desc_at(const ChunkList& l, int c) { return chunk_at(l, c); }
+__device__ __forceinline__ const FusedDesc& desc_at(const FusedList& l, int c) { return fused_at(l, c); }
+
+template <class L>
+__device__ __forceinline__ int cursor_seek(const L& l, TileCursor& cur, int64_t t) {
+  while (t >= cur.end) {  // skips chunks without tiles (tile0 equal to the next one)
+    ++cur.c;
+    cur.end = cur.c + 1 < l.n_chunks ? desc_at(l, cur.c + 1).tile0 : l.total_tiles;
+  }
+  return cur.c;
+}
+
+struct ItemMeta {
+  int64_t e;  // first element of the tile within its chunk (shard)
+  int32_t c;  // chunk
+  int32_t len;
+};
+
+// ------------------------------------------- K1 + K2, TMA bulk pipeline --
+//
+// Persistent CTAs (one per SM) walk the step's tiles. One elected thread moves
+// every tile with 1-D bulk copies (cp.async.bulk, the TMA engine): master/m/v/
+// grad global -> shared, completion counted on an mbarrier (complete_tx), and
+// after the update master/m/v/param shared -> global as a bulk_group. kStages
+// tiles of shared memory form a ring; the producer runs kStages-2 tiles ahead
+// of the consumers, and a stage is refilled only after the bulk store that
+// last read it has finished reading shared memory (wait_group.read 1).
+
 template <int kTile>
 struct TmaStage {
   float master[kTile];
@@ -386,35 +451,21 @@ struct TmaStage {
 
 template <int kTile, int kStages, int kThr, bool kStats, bool kHint>
 __global__ void __launch_bounds__(kThr, 1)
-chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
-                      float* __restrict__ exp_avg_sq, const uint16_t* __restrict__ grad,
-                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
-                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list,
+                      StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
+                      const int32_t* skip_dev) {
   static_assert(kTile % (kThr * 4) == 0, "tile must be a multiple of 4 elements per thread");
   static_assert(kStages >= 3, "ring needs >= 3 stages");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<TmaStage<kTile>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ ItemMeta meta[kStages];
 
   if (skip_dev != nullptr && *skip_dev != 0) return;
-  float gs = s.gscale;
-  if (gscale_dev != nullptr) gs = __fmul_rn(gs, *gscale_dev);
-
+  const float gs = launch_gscale(s, gscale_dev);
   const int tid = threadIdx.x;
-  // Ring items of this CTA: its full tiles blockIdx.x, blockIdx.x + gridDim.x,
-  // ...; the last CTA (which has no more full tiles than any other) also
-  // carries the partial tile -- its multiple-of-8 part as one more, shorter
-  // ring item (TMA sizes stay 16-byte multiples), so no CTA finishes with
-  // un-pipelined plain loads. The < 8 trailing elements (n % 8, never the
-  // case for padded shards) are updated with plain loads at the end.
-  const int64_t n_full = n / kTile;
-  const int64_t my_full =
-      n_full > blockIdx.x ? (n_full - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const bool has_part = blockIdx.x == gridDim.x - 1;
-  const int64_t rem = n - n_full * kTile;
-  const int rem8 = has_part ? static_cast<int>(rem & ~int64_t{7}) : 0;
-  const int64_t my_items = my_full + (rem8 > 0 ? 1 : 0);
-  const bool has_param = param_out != nullptr;
+  const int64_t T = list.total_tiles;
+  const int64_t my_items = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
@@ -431,32 +482,27 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     if (kHint) bulk_store_hint(dst, src, bytes, policy);
     else bulk_store(dst, src, bytes);
   };
-  // item k -> (first element, length)
-  auto item = [&](int64_t k, int64_t& e, int& len) {
-    if (k < my_full) {
-      e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kTile);
-      len = kTile;
-    } else {
-      e = n_full * kTile;
-      len = rem8;
-    }
-  };
+  TileCursor cur;
+  cur.end = list.n_chunks > 1 ? chunk_at(list, 1).tile0 : T;
   // Ring positions are carried as (stage, phase) counters -- the pipeline
-  // state of CUTLASS -- rather than k % kStages: no 64-bit division per tile,
-  // and every mbarrier access is a plain [base + 8*stage] address.
+  // state of CUTLASS -- rather than k % kStages.
   int load_st = 0;
   auto issue_load = [&](int64_t k) {  // k-th item of this CTA, into stage load_st
     const int st = load_st;
     load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    int64_t e;
-    int len;
-    item(k, e, len);
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int c = cursor_seek(list, cur, t);
+    const ChunkDesc& d = chunk_at(list, c);
+    const int64_t e = (t - d.tile0) * kTile;
+    const int64_t left = (d.n & ~int64_t{7}) - e;
+    const int len = left < kTile ? static_cast<int>(left) : kTile;
+    meta[st] = ItemMeta{e, c, len};  // published to the consumers by the arrive below
     TmaStage<kTile>& S = stage[st];
     mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + sizeof(uint16_t)));
-    load(S.master, master + e, len * 4, &full[st]);
-    load(S.m, exp_avg + e, len * 4, &full[st]);
-    load(S.v, exp_avg_sq + e, len * 4, &full[st]);
-    load(S.grad, grad + e, len * 2, &full[st]);
+    load(S.master, d.master + e, len * 4, &full[st]);
+    load(S.m, d.m + e, len * 4, &full[st]);
+    load(S.v, d.v + e, len * 4, &full[st]);
+    load(S.grad, d.grad + e, len * 2, &full[st]);
   };
 
   constexpr int kAhead = kStages - 2;
@@ -472,16 +518,14 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
       bulk_wait_read<1>();  // the store of item k-2 (same stage) has read its smem
       issue_load(k + kAhead);
     }
-    int64_t ge;
-    int len;
-    item(k, ge, len);
     mbar_wait(&full[st], phase);
+    const int len = meta[st].len;
     TmaStage<kTile>& S = stage[st];
     float usq = 0.0f;
 #pragma unroll
     for (int j = 0; j < kTile / (kThr * 4); ++j) {
       const int e = (j * kThr + tid) * 4;
-      if (e >= len) break;  // only in the partial item (len is a multiple of 8)
+      if (e >= len) break;  // only in a chunk's last tile (len is a multiple of 8)
       float4 p = *reinterpret_cast<float4*>(&S.master[e]);
       float4 m = *reinterpret_cast<float4*>(&S.m[e]);
       float4 v = *reinterpret_cast<float4*>(&S.v[e]);
@@ -506,10 +550,12 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     __syncthreads();
     if (tid == 0) {
-      store(master + ge, S.master, len * 4);
-      store(exp_avg + ge, S.m, len * 4);
-      store(exp_avg_sq + ge, S.v, len * 4);
-      if (has_param) store(param_out + ge, S.param, len * 2);
+      const ItemMeta it = meta[st];
+      const ChunkDesc& d = chunk_at(list, it.c);
+      store(d.master + it.e, S.master, it.len * 4);
+      store(d.m + it.e, S.m, it.len * 4);
+      store(d.v + it.e, S.v, it.len * 4);
+      if (d.param != nullptr) store(d.param + it.e, S.param, it.len * 2);
       bulk_commit();
     }
     if (++st == kStages) {
@@ -518,19 +564,20 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __r
     }
   }
   if (tid == 0) bulk_wait_all();
-  // the < 8 trailing elements of a chunk whose length is not a multiple of 8
-  if (has_part) {
-    const int64_t e = n_full * kTile + rem8 + tid;
-    if (e < n) {
+  // the < 8 trailing elements of chunks whose length is not a multiple of 8
+  for (int c = blockIdx.x; c < list.n_chunks; c += gridDim.x) {
+    const ChunkDesc& d = chunk_at(list, c);
+    const int64_t e = (d.n & ~int64_t{7}) + tid;
+    if (e < d.n) {
       float usq = 0.0f;
-      const float gk = __fmul_rn(GradBf16::load1(grad + e), gs);
+      const float gk = __fmul_rn(GradBf16::load1(d.grad + e), gs);
       if (kStats) accum_stats(gk, usq, bad);
-      float p = master[e], mm = exp_avg[e], vv = exp_avg_sq[e];
+      float p = d.master[e], mm = d.m[e], vv = d.v[e];
       adam_elem(s, gk, p, mm, vv);
-      master[e] = p;
-      exp_avg[e] = mm;
-      exp_avg_sq[e] = vv;
-      if (has_param) param_out[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
+      d.master[e] = p;
+      d.m[e] = mm;
+      d.v[e] = vv;
+      if (d.param != nullptr) d.param[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
       if (kStats) sq += usq;
     }
   }
@@ -577,83 +624,137 @@ __global__ void stats_reset_kernel(ptk_grad_stats_t* stats) {
   stats->nonfinite = 0;
 }
 
-__global__ void clip_coef_kernel(const ptk_grad_stats_t* stats, double max_norm, float* coef,
-                                 int32_t* skip) {
-  const double norm = sqrt(stats->sumsq);
+__device__ __forceinline__ void clip_from_stats(double sumsq, unsigned long long nonfinite,
+                                                double max_norm, float* coef, int32_t* skip) {
+  const double norm = sqrt(sumsq);
   double c = 1.0;
   if (max_norm > 0.0) {
     c = max_norm / (norm + 1e-6);
     if (c > 1.0) c = 1.0;
   }
-  *coef = static_cast<float>(c);
-  if (skip != nullptr) *skip = stats->nonfinite != 0 ? 1 : 0;
+  if (coef != nullptr) *coef = static_cast<float>(c);
+  if (skip != nullptr) *skip = nonfinite != 0 ? 1 : 0;
+}
+
+__global__ void clip_coef_kernel(const ptk_grad_stats_t* stats, double max_norm, float* coef,
+                                 int32_t* skip) {
+  clip_from_stats(stats->sumsq, stats->nonfinite, max_norm, coef, skip);
 }
 
 // ------------------------------------------------ K1+K3+K4 over NVLink ----
 
-struct PeerTable {
-  const uint16_t* grad[PTK_MAX_PEERS];
-  uint16_t* param[PTK_MAX_PEERS];
-};
-
+// Register-staged fused step: per 8-element unit, W 128-bit gradient loads
+// (peer memory), fp32 rank-order sum, Adam on the local state, W 128-bit
+// stores of the bf16 result (push all-gather). Chunks in table order.
 template <int W>
 __global__ void __launch_bounds__(kThreads)
-fused_peer_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t shard,
-                  float* __restrict__ master, float* __restrict__ exp_avg,
-                  float* __restrict__ exp_avg_sq, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
+fused_peer_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, StatsWorkspace* ws,
+                  ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
+  if (skip_dev != nullptr && *skip_dev != 0) return;
+  const float gs = launch_gscale(s, gscale_dev);
   double sq = 0.0;
   unsigned bad = 0;
-  const int64_t nvec = shard >> 3;  // shards are multiples of 8 elements
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < nvec;
-       i += stride) {
-    const int64_t e = i << 3;
-    uint4 raw[W];
+  for (int c = 0; c < list.n_chunks; ++c) {
+    const FusedDesc& d = fused_at(list, c);
+    const int64_t off = static_cast<int64_t>(list.rank) * d.shard;
+    const int64_t nvec = d.shard >> 3;  // shards are multiples of 8 elements
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < nvec;
+         i += stride) {
+      const int64_t e = i << 3;
+      uint4 raw[W];
 #pragma unroll
-    for (int r = 0; r < W; ++r)
-      raw[r] = __ldcs(reinterpret_cast<const uint4*>(peers.grad[r] + offset + e));
-    float p[8], m[8], v[8], g[8], t[8];
-    ld8f(master + e, p);
-    ld8f(exp_avg + e, m);
-    ld8f(exp_avg_sq + e, v);
-    unpack8(raw[0], g);
+      for (int r = 0; r < W; ++r)
+        raw[r] = __ldcs(reinterpret_cast<const uint4*>(d.grad[r] + off + e));
+      float p[8], m[8], v[8], g[8], t[8];
+      ld8f(d.master + e, p);
+      ld8f(d.m + e, m);
+      ld8f(d.v + e, v);
+      unpack8(raw[0], g);
 #pragma unroll
-    for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
-      unpack8(raw[r], t);
+      for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
+        unpack8(raw[r], t);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) g[k] = __fadd_rn(g[k], t[k]);
+        for (int k = 0; k < 8; ++k) g[k] = __fadd_rn(g[k], t[k]);
+      }
+      float usq = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float gk = __fmul_rn(g[k], gs);
+        accum_stats(gk, usq, bad);
+        adam_elem(s, gk, p[k], m[k], v[k]);
+      }
+      sq += usq;
+      st8f(d.master + e, p);
+      st8f(d.m + e, m);
+      st8f(d.v + e, v);
+      const uint4 out = pack8(p);
+#pragma unroll
+      for (int r = 0; r < W; ++r)  // all-gather by push
+        __stcs(reinterpret_cast<uint4*>(d.param[r] + off + e), out);
     }
-    float usq = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float gk = __fmul_rn(g[k], s.gscale);
-      accum_stats(gk, usq, bad);
-      adam_elem(s, gk, p[k], m[k], v[k]);
-    }
-    sq += usq;
-    st8f(master + e, p);
-    st8f(exp_avg + e, m);
-    st8f(exp_avg_sq + e, v);
-    const uint4 out = pack8(p);
-#pragma unroll
-    for (int r = 0; r < W; ++r)  // all-gather by push
-      __stcs(reinterpret_cast<uint4*>(peers.param[r] + offset + e), out);
   }
   if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
 }
 
-// The same K1+K3+K4 step through the TMA ring of chunk_adam_tma_kernel: per
-// tile of kFusedTile owned elements one elected thread bulk-loads the local
-// fp32 master/m/v tiles and the owned tile of EVERY rank's gradient chunk
-// (peer memory, NVLink on a node) into one stage, the CTA sums the W
-// gradients in fp32 in rank order (bit-identical to fused_peer_kernel and
-// the oracle), applies Adam, and the elected thread bulk-stores the state
-// locally and the bf16 tile into every rank's parameter chunk (push
-// all-gather). Bytes in flight live in shared memory, not registers.
-// Tile shape per W (elements; threads = tile / 4), measured with virtual
-// ranks (profiles/README.md): W = 2 -> 2048, W = 1, 3, 4 -> 1536, W >= 5 -> 1024.
-// Smaller W means smaller stages; the wider tile keeps ~140-150 KB of loads
-// in flight per SM (tile 1024 at W = 2 reached only 0.66 of HBM).
+// Phase 1 of a clipped / overflow-checked fused step: the statistics of the
+// reduced, scaled gradient of this rank's shards (the same fp32 rank-order
+// sum and the same per-element values the update kernel then uses), no
+// update. 2 B per chunk parameter of gradient reads per rank.
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+fused_stats_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, StatsWorkspace* ws,
+                   ptk_grad_stats_t* stats) {
+  constexpr int U = W <= 2 ? 4 : W <= 4 ? 2 : 1;  // >= 4 x 16 B loads in flight per thread
+  double sq = 0.0;
+  unsigned bad = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int c = 0; c < list.n_chunks; ++c) {
+    const FusedDesc& d = fused_at(list, c);
+    const int64_t off = static_cast<int64_t>(list.rank) * d.shard;
+    const int64_t nvec = d.shard >> 3;
+    int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    for (; i < nvec; i += U * stride) {
+      uint4 raw[U][W];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < W; ++r)
+          if (i + u * stride < nvec)
+            raw[u][r] = __ldcs(reinterpret_cast<const uint4*>(d.grad[r] + off +
+                                                              ((i + u * stride) << 3)));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (i + u * stride >= nvec) break;
+        float g[8], t[8];
+        unpack8(raw[u][0], g);
+#pragma unroll
+        for (int r = 1; r < W; ++r) {
+          unpack8(raw[u][r], t);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) g[k] = __fadd_rn(g[k], t[k]);
+        }
+        // the update kernels sum squares per 4 elements (TMA tile) or per 8
+        // (LDG): statistics are reproducible per kernel, within 1e-6 across
+        float usq = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) accum_stats(__fmul_rn(g[k], s.gscale), usq, bad);
+        sq += usq;
+      }
+    }
+  }
+  reduce_stats(sq, bad, ws, stats);
+}
+
+// The same K1+K3+K4 step through a TMA ring: per tile of owned elements one
+// elected thread bulk-loads the local fp32 master/m/v tiles and the owned tile
+// of EVERY rank's gradient chunk (peer memory, NVLink on a node) into one
+// stage, the CTA sums the W gradients in fp32 in rank order (bit-identical to
+// fused_peer_kernel and the oracle), applies Adam, and the elected thread
+// bulk-stores the state locally and the bf16 tile into every rank's parameter
+// chunk (push all-gather). Tile shape per W (elements; threads = tile / 4),
+// measured with virtual ranks (profiles/README.md): W = 2 -> 2048,
+// W = 1, 3, 4 -> 1536, W >= 5 -> 1024.
 constexpr int kFusedSmemBudget = 220 * 1024;
 template <int W>
 __host__ __device__ constexpr int fused_tile() { return W == 1 ? 1536 : W == 2 ? 2048 : W <= 4 ? 1536 : 1024; }
@@ -678,53 +779,47 @@ constexpr int fused_stages() {
 
 template <int W, int kStages>
 __global__ void __launch_bounds__(fused_threads<W>(), 1)
-fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64_t shard,
-                      float* __restrict__ master, float* __restrict__ exp_avg,
-                      float* __restrict__ exp_avg_sq, StatsWorkspace* ws,
-                      ptk_grad_stats_t* stats) {
+fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list,
+                      StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
+                      const int32_t* skip_dev) {
   constexpr int kFusedTile = fused_tile<W>();
   static_assert(kStages >= 3, "ring needs >= 3 stages");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<FusedStage<W>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ ItemMeta meta[kStages];
+  if (skip_dev != nullptr && *skip_dev != 0) return;
+  const float gs = launch_gscale(s, gscale_dev);
   const int tid = threadIdx.x;
-  // ring items: this CTA's full tiles, plus -- on the last CTA -- the partial
-  // tile (shards are multiples of 8 elements, so its TMA sizes are 16-byte
-  // multiples) as one shorter item: no un-pipelined tail
-  const int64_t n_tiles = shard / kFusedTile;
-  const int64_t my_full = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int rem = blockIdx.x == gridDim.x - 1 ? static_cast<int>(shard - n_tiles * kFusedTile) : 0;
-  const int64_t my_items = my_full + (rem > 0 ? 1 : 0);
+  const int64_t T = list.total_tiles;
+  const int64_t my_items = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  auto item = [&](int64_t k, int64_t& e, int& len) {
-    if (k < my_full) {
-      e = (blockIdx.x + k * gridDim.x) * static_cast<int64_t>(kFusedTile);
-      len = kFusedTile;
-    } else {
-      e = n_tiles * kFusedTile;
-      len = rem;
-    }
-  };
+  TileCursor cur;
+  cur.end = list.n_chunks > 1 ? fused_at(list, 1).tile0 : T;
   int load_st = 0;
   auto issue_load = [&](int64_t k) {
     const int st = load_st;
     load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    int64_t e;
-    int len;
-    item(k, e, len);
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    const int c = cursor_seek(list, cur, t);
+    const FusedDesc& d = fused_at(list, c);
+    const int64_t e = (t - d.tile0) * kFusedTile;
+    const int64_t left = d.shard - e;
+    const int len = left < kFusedTile ? static_cast<int>(left) : kFusedTile;
+    const int64_t off = static_cast<int64_t>(list.rank) * d.shard + e;
+    meta[st] = ItemMeta{e, c, len};
     FusedStage<W>& S = stage[st];
     mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + W * sizeof(uint16_t)));
-    bulk_load(S.master, master + e, len * 4, &full[st]);
-    bulk_load(S.m, exp_avg + e, len * 4, &full[st]);
-    bulk_load(S.v, exp_avg_sq + e, len * 4, &full[st]);
+    bulk_load(S.master, d.master + e, len * 4, &full[st]);
+    bulk_load(S.m, d.m + e, len * 4, &full[st]);
+    bulk_load(S.v, d.v + e, len * 4, &full[st]);
 #pragma unroll
-    for (int r = 0; r < W; ++r)
-      bulk_load(S.grad[r], peers.grad[r] + offset + e, len * 2, &full[st]);
+    for (int r = 0; r < W; ++r) bulk_load(S.grad[r], d.grad[r] + off, len * 2, &full[st]);
   };
   constexpr int kAhead = kStages - 2;
   if (tid == 0)
@@ -739,13 +834,11 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
       bulk_wait_read<1>();
       issue_load(k + kAhead);
     }
-    int64_t ge;
-    int len;
-    item(k, ge, len);
     mbar_wait(&full[st], phase);
+    const int len = meta[st].len;
     FusedStage<W>& S = stage[st];
     const int e = tid * 4;
-    if (e < len) {  // always, except in the partial item
+    if (e < len) {  // always, except in a chunk's last tile
       float4 p = *reinterpret_cast<float4*>(&S.master[e]);
       float4 m = *reinterpret_cast<float4*>(&S.m[e]);
       float4 v = *reinterpret_cast<float4*>(&S.v[e]);
@@ -765,7 +858,7 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
       float usq = 0.0f;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float gk = __fmul_rn(g[q], s.gscale);
+        const float gk = __fmul_rn(g[q], gs);
         accum_stats(gk, usq, bad);
         adam_elem(s, gk, pp[q], mm[q], vv[q]);
       }
@@ -779,11 +872,14 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
-      bulk_store(master + ge, S.master, len * 4);
-      bulk_store(exp_avg + ge, S.m, len * 4);
-      bulk_store(exp_avg_sq + ge, S.v, len * 4);
+      const ItemMeta it = meta[st];
+      const FusedDesc& d = fused_at(list, it.c);
+      const int64_t off = static_cast<int64_t>(list.rank) * d.shard + it.e;
+      bulk_store(d.master + it.e, S.master, it.len * 4);
+      bulk_store(d.m + it.e, S.m, it.len * 4);
+      bulk_store(d.v + it.e, S.v, it.len * 4);
 #pragma unroll
-      for (int r = 0; r < W; ++r) bulk_store(peers.param[r] + offset + ge, S.param, len * 2);
+      for (int r = 0; r < W; ++r) bulk_store(d.param[r] + off, S.param, it.len * 2);
       bulk_commit();
     }
     if (++st == kStages) {
@@ -795,9 +891,29 @@ fused_peer_tma_kernel(ptk_adam_scalars s, PeerTable peers, int64_t offset, int64
   if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
 }
 
+// ------------------------------------------------- peer synchronisation ----
+
 struct SignalTable {
   int32_t* slot[PTK_MAX_PEERS];
 };
+
+__device__ __forceinline__ void spin_until(const int32_t* flag, int32_t epoch, int64_t timeout_ns,
+                                           const char* what, int rank, int peer) {
+  int32_t seen;
+  uint64_t t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(flag) : "memory");
+    if (seen >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (static_cast<int64_t>(now - t0) > timeout_ns) {
+      printf("%s: rank %d timed out waiting for rank %d (epoch %d, seen %d)\n", what, rank, peer,
+             epoch, seen);
+      __trap();
+    }
+    __nanosleep(64);
+  }
+}
 
 // A peer that never arrives (crashed rank, mismatched epochs) must not hang
 // the device: after timeout_ns of device time the barrier traps, which fails
@@ -809,21 +925,53 @@ __global__ void peer_barrier_kernel(SignalTable sig, int world, int rank, int ep
   __threadfence_system();
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(sig.slot[t] + rank), "r"(epoch)
                : "memory");
-  const int32_t* mine = sig.slot[rank] + t;
-  int32_t seen;
-  uint64_t t0, now;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
-    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(seen) : "l"(mine) : "memory");
-    if (seen >= epoch) break;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (static_cast<int64_t>(now - t0) > timeout_ns) {
-      printf("ptk_peer_barrier: rank %d timed out waiting for rank %d (epoch %d, seen %d)\n",
-             rank, t, epoch, seen);
-      __trap();
-    }
-    __nanosleep(64);
+  spin_until(sig.slot[rank] + t, epoch, timeout_ns, "ptk_peer_barrier", rank, t);
+}
+
+// Statistics mailbox: slot r of every rank's mailbox receives rank r's
+// partial statistics; a release-stored epoch publishes them.
+struct alignas(32) MailSlot {
+  double sumsq;
+  unsigned long long nonfinite;
+  int32_t epoch;
+  int32_t pad[3];
+};
+static_assert(sizeof(MailSlot) == 32, "mailbox slot is 32 bytes");
+
+struct MailTable {
+  MailSlot* box[PTK_MAX_PEERS];
+};
+
+__global__ void stats_publish_kernel(const ptk_grad_stats_t* stats, MailTable peers, int world,
+                                     int rank, int epoch) {
+  const int t = threadIdx.x;
+  if (t >= world) return;
+  MailSlot* slot = peers.box[t] + rank;
+  slot->sumsq = stats->sumsq;
+  slot->nonfinite = stats->nonfinite;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(&slot->epoch), "r"(epoch) : "memory");
+}
+
+// Sums the world's slots in rank order 0..W-1 (the same bits on every rank),
+// writes the global statistics, the clip coefficient and the skip flag.
+__global__ void stats_collect_kernel(const MailSlot* box, int world, int epoch, double max_norm,
+                                     int64_t timeout_ns, ptk_grad_stats_t* global_out, float* coef,
+                                     int32_t* skip) {
+  if (threadIdx.x != 0) return;
+  double sq = 0.0;
+  unsigned long long bad = 0;
+  for (int r = 0; r < world; ++r) {
+    spin_until(&box[r].epoch, epoch, timeout_ns, "ptk_stats_collect", -1, r);
+    const volatile MailSlot* v = box + r;
+    sq += v->sumsq;
+    bad += v->nonfinite;
   }
+  if (global_out != nullptr) {
+    global_out->sumsq = sq;
+    global_out->nonfinite = bad;
+  }
+  clip_from_stats(sq, bad, max_norm, coef, skip);
 }
 
 // Occupies the stream for `ns` nanoseconds of device time (global timer).
@@ -866,15 +1014,38 @@ __global__ void fill_bf16_kernel(uint16_t* out, int64_t n, uint64_t seed, int64_
 }
 
 // --------------------------------------------------------- launch sizing --
+// Per-device caches: a process may launch on several devices (single-process
+// multi-GPU harnesses, the executor), and both the SM count and the opt-in
+// dynamic shared-memory attribute are properties of a device context.
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
 
 int sm_count() {
-  static int count = [] {
-    int dev = 0, c = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[kMaxDevices];
+  const int dev = current_device();
+  int c = cache[dev].load(std::memory_order_relaxed);
+  if (c == 0) {
     cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
-    return c > 0 ? c : 148;
-  }();
-  return count;
+    if (c <= 0) c = 148;
+    cache[dev].store(c, std::memory_order_relaxed);
+  }
+  return c;
+}
+
+// Opt-in dynamic shared memory for kernel `k` on the current device, once per
+// (kernel instantiation, device): `done` is the caller's per-kernel static.
+template <typename K>
+int ensure_smem(K k, int bytes, std::atomic<bool> (&done)[kMaxDevices], const char* what) {
+  const int dev = current_device();
+  if (done[dev].load(std::memory_order_acquire)) return PTK_OK;
+  const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return check_cuda(e, what);
+  done[dev].store(true, std::memory_order_release);
+  return PTK_OK;
 }
 
 template <typename K>
@@ -892,33 +1063,37 @@ int grid_for(K kernel, int64_t work_items) {
 
 constexpr int kUnroll = 2;
 
-// Kernel variant of the bf16-gradient chunk Adam. Selected once per process
-// from PTK_ADAM_VARIANT (benchmarking aid); the default is the measured best.
-// TMA pipeline shapes: (name, tile elements, ring stages, CTAs per SM,
-// threads, L2 evict-first hint).
+// TMA ring shapes of the chunk Adam: (name, tile elements, ring stages, CTAs
+// per SM, threads, L2 evict-first hint). The product build has the measured
+// best only (profiles/README.md, interleaved sweep); the shape sweep is
+// compiled in with -DPTK_BENCH_VARIANTS and selected by PTK_ADAM_VARIANT.
+#ifdef PTK_BENCH_VARIANTS
 #define PTK_TMA_VARIANTS(X)                     \
+  X(Tma1536x9t384, 1536, 9, 1, 384, false)      \
   X(Tma1536x8t384, 1536, 8, 1, 384, false)      \
   X(Tma1536x8t384h, 1536, 8, 1, 384, true)      \
-  X(Tma1536x9t384, 1536, 9, 1, 384, false)      \
   X(Tma1536x9t384h, 1536, 9, 1, 384, true)      \
   X(Tma1536x4x2t384, 1536, 4, 2, 384, false)    \
   X(Tma2048x6, 2048, 6, 1, 256, false)          \
   X(Tma2048x6h, 2048, 6, 1, 256, true)          \
   X(Tma3072x4t384, 3072, 4, 1, 384, false)      \
   X(Tma1792x7t448, 1792, 7, 1, 448, false)
+#else
+#define PTK_TMA_VARIANTS(X) X(Tma1536x9t384, 1536, 9, 1, 384, false)
+#endif
 
 #define PTK_ENUM_ENTRY(V, T, S, P, THR, H) V,
-enum class AdamVariant { Ldg, LdgOcc, PTK_TMA_VARIANTS(PTK_ENUM_ENTRY) };
+enum class AdamVariant { Ldg, PTK_TMA_VARIANTS(PTK_ENUM_ENTRY) };
 #undef PTK_ENUM_ENTRY
 
-// Default: the fastest shape measured on B200 (profiles/README.md).
+// Default: the fastest shape measured on B200; "ldg" selects the register-
+// staged kernel (per-chunk launches) in any build.
 AdamVariant adam_variant() {
-  static AdamVariant v = [] {
+  static const AdamVariant v = [] {
     const char* e = std::getenv("PTK_ADAM_VARIANT");
     std::string name = e ? e : "";
     for (auto& ch : name) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
     if (name == "ldg") return AdamVariant::Ldg;
-    if (name == "ldg_occ") return AdamVariant::LdgOcc;
 #define PTK_NAME_ENTRY(V, T, S, P, THR, H)                                \
     {                                                                     \
       std::string tag = #V;                                               \
@@ -927,17 +1102,22 @@ AdamVariant adam_variant() {
     }
     PTK_TMA_VARIANTS(PTK_NAME_ENTRY)
 #undef PTK_NAME_ENTRY
-    return AdamVariant::Tma1536x9t384;  // profiles/README.md, interleaved sweep
+    return AdamVariant::Tma1536x9t384;
   }();
   return v;
 }
 
-template <class G, int U, bool kStats, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks)
-chunk_adam_occ_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restrict__ exp_avg,
-                      float* __restrict__ exp_avg_sq, const typename G::T* __restrict__ grad,
-                      uint16_t* __restrict__ param_out, int64_t n, StatsWorkspace* ws,
-                      ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev);
+int adam_tile() {
+  switch (adam_variant()) {
+#define PTK_TILE_CASE(V, T, S, P, THR, H) \
+  case AdamVariant::V:                    \
+    return T;
+    PTK_TMA_VARIANTS(PTK_TILE_CASE)
+#undef PTK_TILE_CASE
+    default:
+      return 1536;
+  }
+}
 
 template <class G, bool kStats>
 void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
@@ -952,38 +1132,57 @@ void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
 }
 
 template <int kTile, int kStages, int kPerSm, int kThr, bool kStats, bool kHint>
-int launch_tma(const ptk_adam_scalars& s, float* master, float* m, float* v,
-               const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
+int launch_tma(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                cudaStream_t st) {
   auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint>;
   constexpr int kSmem = kStages * static_cast<int>(sizeof(TmaStage<kTile>));
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return check_cuda(e, "chunk_adam_tma_kernel smem attribute");
-    configured = true;
-  }
+  static std::atomic<bool> configured[kMaxDevices];
+  const int rc = ensure_smem(k, kSmem, configured, "chunk_adam_tma_kernel smem attribute");
+  if (rc != PTK_OK) return rc;
   int64_t grid = static_cast<int64_t>(sm_count()) * kPerSm;
-  if (grid > n / kTile) grid = n / kTile;
-  if (grid < 1) grid = 1;  // partial tile only
-  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, master, m, v, grad, param_out, n, ws, stats,
-                                                 gscale_dev, skip_dev);
+  if (grid > list.total_tiles) grid = list.total_tiles;
+  if (grid < 1) grid = 1;  // tails only
+  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, list, ws, stats, gscale_dev, skip_dev);
   launch_counter()++;
   return PTK_OK;
 }
 
-// One launch per chunk: full tiles through the TMA ring, the partial tile by
-// the last CTA.
 template <int kTile, int kStages, int kPerSm, int kThr, bool kHint>
-int adam_tma_then_tail(const ptk_adam_scalars& s, float* master, float* m, float* v,
-                       const uint16_t* grad, uint16_t* param_out, int64_t n, StatsWorkspace* ws,
-                       ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
-                       cudaStream_t st) {
-  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true, kHint>(
-                     s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st)
-               : launch_tma<kTile, kStages, kPerSm, kThr, false, kHint>(
-                     s, master, m, v, grad, param_out, n, ws, stats, gscale_dev, skip_dev, st);
+int launch_tma_any(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
+                   ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+                   cudaStream_t st) {
+  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true, kHint>(s, list, ws, stats,
+                                                                       gscale_dev, skip_dev, st)
+               : launch_tma<kTile, kStages, kPerSm, kThr, false, kHint>(s, list, ws, stats,
+                                                                        gscale_dev, skip_dev, st);
+}
+
+int64_t tiles_of(int64_t n, int tile) { return ((n & ~int64_t{7}) + tile - 1) / tile; }
+
+// One TMA launch over `list` (tile0 computed for adam_tile()).
+int launch_tma_list(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
+                    ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+                    cudaStream_t st) {
+  switch (adam_variant()) {
+#define PTK_TMA_CASE(V, T, S, P, THR, H) \
+  case AdamVariant::V:                   \
+    return launch_tma_any<T, S, P, THR, H>(s, list, ws, stats, gscale_dev, skip_dev, st);
+    PTK_TMA_VARIANTS(PTK_TMA_CASE)
+#undef PTK_TMA_CASE
+    default:
+      return fail(PTK_EINVAL, "launch_tma_list: not a TMA variant");
+  }
+}
+
+int validate_adam_buffers(const float* master, const float* m, const float* v, const void* grad,
+                          const uint16_t* param_out, int64_t n, const char* what) {
+  if (!master || !m || !v || !grad) return fail(PTK_EINVAL, std::string(what) + ": null buffer");
+  if (n < 0) return fail(PTK_EINVAL, std::string(what) + ": negative n");
+  if (!aligned16(master) || !aligned16(m) || !aligned16(v) || !aligned16(grad) ||
+      (param_out && !aligned16(param_out)))
+    return fail(PTK_EINVAL, std::string(what) + ": buffers must be 16-byte aligned");
+  return PTK_OK;
 }
 
 template <class G>
@@ -991,43 +1190,24 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
                 const typename G::T* grad, uint16_t* param_out, int64_t n,
                 ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
                 const int32_t* skip_dev, void* stream) {
-  if (!cfg || !master || !m || !v || !grad) return fail(PTK_EINVAL, "ptk_chunk_adam: null buffer");
-  if (n < 0) return fail(PTK_EINVAL, "ptk_chunk_adam: negative n");
+  if (!cfg) return fail(PTK_EINVAL, "ptk_chunk_adam: null config");
+  int rc = validate_adam_buffers(master, m, v, grad, param_out, n, "ptk_chunk_adam");
+  if (rc != PTK_OK) return rc;
   if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_chunk_adam: step must be >= 1");
-  if (!aligned16(master) || !aligned16(m) || !aligned16(v) || !aligned16(grad) ||
-      (param_out && !aligned16(param_out)))
-    return fail(PTK_EINVAL, "ptk_chunk_adam: buffers must be 16-byte aligned");
   if (stats && !workspace) return fail(PTK_EINVAL, "ptk_chunk_adam: stats requires workspace");
   if (n == 0) return PTK_OK;
   const ptk_adam_scalars s = derive_scalars(*cfg);
   auto* ws = static_cast<StatsWorkspace*>(workspace);
   cudaStream_t st = as_stream(stream);
-  int rc = PTK_OK;
   if constexpr (std::is_same_v<G, GradBf16>) {
-    switch (adam_variant()) {
-#define PTK_TMA_CASE(V, T, S, P, THR, H)                                                    \
-  case AdamVariant::V:                                                                       \
-    rc = adam_tma_then_tail<T, S, P, THR, H>(s, master, m, v, grad, param_out, n, ws, stats, \
-                                             gscale_dev, skip_dev, st);                      \
-    return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
-      PTK_TMA_VARIANTS(PTK_TMA_CASE)
-#undef PTK_TMA_CASE
-      case AdamVariant::LdgOcc: {
-        const int64_t units = (n >> 3) > 0 ? (n >> 3) : 1;
-        if (stats) {
-          auto k = chunk_adam_occ_kernel<G, 1, true, 4>;
-          k<<<grid_for(k, units), kThreads, 0, st>>>(s, master, m, v, grad, param_out, n, ws,
-                                                     stats, gscale_dev, skip_dev);
-        } else {
-          auto k = chunk_adam_occ_kernel<G, 1, false, 4>;
-          k<<<grid_for(k, units), kThreads, 0, st>>>(s, master, m, v, grad, param_out, n, ws,
-                                                     stats, gscale_dev, skip_dev);
-        }
-        launch_counter()++;
-        return check_cuda(cudaGetLastError(), "chunk_adam_occ_kernel launch");
-      }
-      default:
-        break;
+    if (adam_variant() != AdamVariant::Ldg) {
+      ChunkList list{};
+      list.table = nullptr;
+      list.one = ChunkDesc{master, m, v, grad, param_out, n, 0};
+      list.n_chunks = 1;
+      list.total_tiles = tiles_of(n, adam_tile());
+      rc = launch_tma_list(s, list, ws, stats, gscale_dev, skip_dev, st);
+      return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
     }
   }
   if (stats)
@@ -1037,23 +1217,19 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
   return check_cuda(cudaGetLastError(), "chunk_adam_kernel launch");
 }
 
-// Fused-kernel variant, once per process from PTK_FUSED_KERNEL ("tma", the
-// default, or "ldg" = the register-staged fused_peer_kernel).
-// 0 = auto (TMA ring when every peer buffer lives on this device -- virtual
-// ranks, cudaIpc mappings of the same GPU, which is what is tested here --
-// and the register-staged LDG kernel, the plain peer load / store pattern,
-// when a buffer is on another GPU), 1 = always TMA, 2 = always LDG.
-int fused_mode() {
+// Fused-kernel override from PTK_FUSED_KERNEL ("tma" / "ldg"), read once; the
+// per-table choice (ptk_fused_table_create's `kernel`) applies otherwise.
+int fused_env_override() {
   static const int mode = [] {
     const char* e = std::getenv("PTK_FUSED_KERNEL");
-    if (e && std::string(e) == "tma") return 1;
-    if (e && std::string(e) == "ldg") return 2;
-    return 0;
+    if (e && std::string(e) == "tma") return PTK_FUSED_TMA;
+    if (e && std::string(e) == "ldg") return PTK_FUSED_LDG;
+    return PTK_FUSED_AUTO;
   }();
   return mode;
 }
 
-bool same_device(const void* p, int dev) {
+bool on_device(const void* p, int dev) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -1062,37 +1238,98 @@ bool same_device(const void* p, int dev) {
   return a.type == cudaMemoryTypeDevice && a.device == dev;
 }
 
+int fused_tile_for(int world) {
+  switch (world) {
+    case 1: return fused_tile<1>();
+    case 2: return fused_tile<2>();
+    case 3: return fused_tile<3>();
+    case 4: return fused_tile<4>();
+    case 5: return fused_tile<5>();
+    case 6: return fused_tile<6>();
+    case 7: return fused_tile<7>();
+    default: return fused_tile<8>();
+  }
+}
+
+enum class FusedOp { Step, Stats };
+
 template <int W>
-int launch_fused(const ptk_adam_scalars& s, const PeerTable& t, int64_t off, int64_t shard,
-                 float* p, float* m, float* v, StatsWorkspace* ws, ptk_grad_stats_t* stats,
-                 cudaStream_t st, bool tma) {
+int launch_fused(FusedOp op, const ptk_adam_scalars& s, const FusedList& list, int64_t max_shard,
+                 StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
+                 const int32_t* skip_dev, cudaStream_t st, bool tma) {
+  const int64_t units = (max_shard >> 3) > 0 ? (max_shard >> 3) : 1;
+  if (op == FusedOp::Stats) {
+    auto k = fused_stats_kernel<W>;
+    k<<<grid_for(k, units), kThreads, 0, st>>>(s, list, ws, stats);
+    return PTK_OK;
+  }
   if (!tma) {
     auto k = fused_peer_kernel<W>;
-    const int grid = grid_for(k, (shard >> 3) > 0 ? (shard >> 3) : 1);
-    k<<<grid, kThreads, 0, st>>>(s, t, off, shard, p, m, v, ws, stats);
+    k<<<grid_for(k, units), kThreads, 0, st>>>(s, list, ws, stats, gscale_dev, skip_dev);
     return PTK_OK;
   }
   constexpr int kSt = fused_stages<W>();
   constexpr int kSmem = kSt * static_cast<int>(sizeof(FusedStage<W>));
   auto k = fused_peer_tma_kernel<W, kSt>;
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return check_cuda(e, "fused_peer_tma_kernel smem attribute");
-    configured = true;
-  }
+  static std::atomic<bool> configured[kMaxDevices];
+  const int rc = ensure_smem(k, kSmem, configured, "fused_peer_tma_kernel smem attribute");
+  if (rc != PTK_OK) return rc;
   int64_t grid = sm_count();
-  if (grid > shard / fused_tile<W>()) grid = shard / fused_tile<W>();
+  if (grid > list.total_tiles) grid = list.total_tiles;
   if (grid < 1) grid = 1;
-  k<<<static_cast<int>(grid), fused_threads<W>(), kSmem, st>>>(s, t, off, shard, p, m, v, ws,
-                                                                stats);
+  k<<<static_cast<int>(grid), fused_threads<W>(), kSmem, st>>>(s, list, ws, stats, gscale_dev,
+                                                                skip_dev);
   return PTK_OK;
+}
+
+int dispatch_fused(int world, FusedOp op, const ptk_adam_scalars& s, const FusedList& list,
+                   int64_t max_shard, StatsWorkspace* ws, ptk_grad_stats_t* stats,
+                   const float* gscale_dev, const int32_t* skip_dev, cudaStream_t st, bool tma) {
+  switch (world) {
+    case 1: return launch_fused<1>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 2: return launch_fused<2>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 3: return launch_fused<3>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 4: return launch_fused<4>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 5: return launch_fused<5>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 6: return launch_fused<6>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    case 7: return launch_fused<7>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+    default: return launch_fused<8>(op, s, list, max_shard, ws, stats, gscale_dev, skip_dev, st, tma);
+  }
+}
+
+int64_t peer_timeout_ns() {
+  static const int64_t ns = [] {
+    const char* e = std::getenv("PTK_PEER_BARRIER_TIMEOUT_MS");
+    const long long ms = e ? std::atoll(e) : 60000;
+    return static_cast<int64_t>(ms > 0 ? ms : 60000) * 1000000;
+  }();
+  return ns;
 }
 
 }  // namespace
 }  // namespace ptk
 
 using namespace ptk;
+
+// Opaque table handles of the C-ABI (include/ptk.h).
+struct ptk_chunk_table {
+  std::vector<ChunkDesc> host;  // tile0 for `tile`
+  ChunkDesc* dev = nullptr;
+  int64_t total_tiles = 0;
+  int tile = 0;
+  int device = 0;
+};
+
+struct ptk_fused_table {
+  std::vector<FusedDesc> host;
+  FusedDesc* dev = nullptr;
+  int64_t total_tiles = 0;
+  int64_t max_shard = 0;
+  int32_t world = 1;
+  int32_t rank = 0;
+  int32_t kernel = PTK_FUSED_TMA;  // resolved: PTK_FUSED_TMA or PTK_FUSED_LDG
+  int device = 0;
+};
 
 extern "C" {
 
@@ -1101,7 +1338,6 @@ int64_t ptk_stats_workspace_bytes(void) { return static_cast<int64_t>(sizeof(Sta
 const char* ptk_adam_kernel_name(void) {
   switch (adam_variant()) {
     case AdamVariant::Ldg: return "ldg";
-    case AdamVariant::LdgOcc: return "ldg_occ";
 #define PTK_NAME_CASE(V, T, S, P, THR, H) \
   case AdamVariant::V:                    \
     return "tma tile=" #T " stages=" #S " ctas/sm=" #P " threads=" #THR " l2_evict_first=" #H;
@@ -1112,16 +1348,15 @@ const char* ptk_adam_kernel_name(void) {
 }
 
 const char* ptk_fused_kernel_name(void) {
-  switch (fused_mode()) {
-    case 1:
-      return "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for W>=5; "
-             "threads = tile/4; stages = min(9, 220 KB / stage))";
-    case 2:
-      return "fused_peer_kernel (ldg)";
+  switch (fused_env_override()) {
+    case PTK_FUSED_TMA:
+      return "fused_peer_tma_kernel (forced by PTK_FUSED_KERNEL=tma)";
+    case PTK_FUSED_LDG:
+      return "fused_peer_kernel (ldg, forced by PTK_FUSED_KERNEL=ldg)";
     default:
-      return "fused RS->Adam->AG, auto: fused_peer_tma_kernel (tile 2048 for W=2, 1536 for "
-             "W=1,3,4, 1024 for W>=5) when every peer buffer is on this device, "
-             "fused_peer_kernel (ldg) across devices";
+      return "per table: fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for "
+             "W>=5; threads = tile/4; stages = min(9, 220 KB / stage)) when every peer buffer is "
+             "on this device, fused_peer_kernel (ldg) across devices";
   }
 }
 
@@ -1139,6 +1374,86 @@ int ptk_chunk_adam_f32grad(const ptk_adam_config* cfg, float* master, float* exp
                            const int32_t* skip_dev, void* stream) {
   return launch_adam<GradF32>(cfg, master, exp_avg, exp_avg_sq, grad, param_out, n, stats,
                               workspace, gscale_dev, skip_dev, stream);
+}
+
+// ---- chunk tables: one launch per step over every chunk ----
+
+int ptk_chunk_table_create(const ptk_chunk_desc* descs, int32_t n_chunks, ptk_chunk_table** out) {
+  if (!out || (!descs && n_chunks > 0) || n_chunks < 0)
+    return fail(PTK_EINVAL, "ptk_chunk_table_create: bad arguments");
+  *out = nullptr;
+  auto* t = new ptk_chunk_table;
+  t->tile = adam_tile();
+  t->device = current_device();
+  int64_t tile0 = 0;
+  for (int32_t c = 0; c < n_chunks; ++c) {
+    const ptk_chunk_desc& d = descs[c];
+    const int rc = validate_adam_buffers(d.master, d.exp_avg, d.exp_avg_sq, d.grad, d.param_out,
+                                         d.n, "ptk_chunk_table_create");
+    if (rc != PTK_OK) {
+      delete t;
+      return rc;
+    }
+    t->host.push_back(ChunkDesc{d.master, d.exp_avg, d.exp_avg_sq, d.grad, d.param_out, d.n, tile0});
+    tile0 += tiles_of(d.n, t->tile);
+  }
+  t->total_tiles = tile0;
+  if (n_chunks > 0) {
+    const size_t bytes = sizeof(ChunkDesc) * t->host.size();
+    cudaError_t e = cudaMalloc(&t->dev, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(t->dev, t->host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (t->dev) cudaFree(t->dev);
+      delete t;
+      return check_cuda(e, "ptk_chunk_table_create: device table");
+    }
+  }
+  *out = t;
+  return PTK_OK;
+}
+
+int ptk_chunk_table_destroy(ptk_chunk_table* t) {
+  if (!t) return PTK_OK;
+  const cudaError_t e = t->dev ? cudaFree(t->dev) : cudaSuccess;
+  delete t;
+  return check_cuda(e, "ptk_chunk_table_destroy");
+}
+
+int64_t ptk_chunk_table_params(const ptk_chunk_table* t) {
+  int64_t n = 0;
+  if (t)
+    for (const auto& d : t->host) n += d.n;
+  return n;
+}
+
+int ptk_chunk_adam_table(const ptk_adam_config* cfg, const ptk_chunk_table* t,
+                         ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                         const int32_t* skip_dev, void* stream) {
+  if (!cfg || !t) return fail(PTK_EINVAL, "ptk_chunk_adam_table: null argument");
+  if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_chunk_adam_table: step must be >= 1");
+  if (stats && !workspace) return fail(PTK_EINVAL, "ptk_chunk_adam_table: stats requires workspace");
+  if (t->host.empty()) return PTK_OK;
+  if (t->device != current_device())
+    return fail(PTK_EINVAL, "ptk_chunk_adam_table: table was created on another device");
+  const ptk_adam_scalars s = derive_scalars(*cfg);
+  auto* ws = static_cast<StatsWorkspace*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  if (adam_variant() == AdamVariant::Ldg || t->tile != adam_tile()) {
+    // per-chunk launches (the "ldg" variant, or a table built for another tile)
+    for (const auto& d : t->host) {
+      const int rc = ptk_chunk_adam(cfg, d.master, d.m, d.v, d.grad, d.param, d.n, stats, workspace,
+                                    gscale_dev, skip_dev, stream);
+      if (rc != PTK_OK) return rc;
+    }
+    return PTK_OK;
+  }
+  ChunkList list{};
+  list.table = t->dev;
+  list.one = t->host[0];
+  list.n_chunks = static_cast<int32_t>(t->host.size());
+  list.total_tiles = t->total_tiles;
+  const int rc = launch_tma_list(s, list, ws, stats, gscale_dev, skip_dev, st);
+  return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma (table) launch");
 }
 
 int ptk_grad_stats(const uint16_t* grad, int64_t n, float scale, float* out_f32,
@@ -1181,6 +1496,126 @@ int ptk_clip_coef(const ptk_grad_stats_t* stats, double max_norm, float* coef_ou
   return check_cuda(cudaGetLastError(), "clip_coef_kernel launch");
 }
 
+// ---- fused RS -> Adam -> AG ----
+
+int ptk_fused_table_create(const ptk_fused_desc* descs, int32_t n_chunks, int32_t world,
+                           int32_t rank, int32_t kernel, ptk_fused_table** out) {
+  if (!out || (!descs && n_chunks > 0) || n_chunks < 0)
+    return fail(PTK_EINVAL, "ptk_fused_table_create: bad arguments");
+  *out = nullptr;
+  if (world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(PTK_EINVAL, "ptk_fused_table_create: bad world/rank");
+  if (kernel != PTK_FUSED_AUTO && kernel != PTK_FUSED_TMA && kernel != PTK_FUSED_LDG)
+    return fail(PTK_EINVAL, "ptk_fused_table_create: unknown kernel selector");
+  auto* t = new ptk_fused_table;
+  t->world = world;
+  t->rank = rank;
+  t->device = current_device();
+  const int tile = fused_tile_for(world);
+  bool all_local = true;
+  int64_t tile0 = 0;
+  for (int32_t c = 0; c < n_chunks; ++c) {
+    const ptk_fused_desc& d = descs[c];
+    const char* bad = nullptr;
+    if (d.shard < 0 || (d.shard & 7) != 0) bad = "shard must be a non-negative multiple of 8 elements";
+    if (!d.master || !d.exp_avg || !d.exp_avg_sq || !aligned16(d.master) || !aligned16(d.exp_avg) ||
+        !aligned16(d.exp_avg_sq))
+      bad = "state buffers must be non-null and 16-byte aligned";
+    FusedDesc f{};
+    for (int r = 0; r < world && !bad; ++r) {
+      if (!d.grad_peers[r] || !d.param_peers[r] || !aligned16(d.grad_peers[r]) ||
+          !aligned16(d.param_peers[r]))
+        bad = "peer buffers must be non-null and 16-byte aligned";
+      f.grad[r] = d.grad_peers[r];
+      f.param[r] = d.param_peers[r];
+      if (!bad && kernel == PTK_FUSED_AUTO)
+        all_local = all_local && on_device(d.grad_peers[r], t->device) &&
+                    on_device(d.param_peers[r], t->device);
+    }
+    if (bad) {
+      delete t;
+      return fail(PTK_EINVAL, std::string("ptk_fused_table_create: ") + bad);
+    }
+    f.master = d.master;
+    f.m = d.exp_avg;
+    f.v = d.exp_avg_sq;
+    f.shard = d.shard;
+    f.tile0 = tile0;
+    tile0 += (d.shard + tile - 1) / tile;
+    if (d.shard > t->max_shard) t->max_shard = d.shard;
+    t->host.push_back(f);
+  }
+  t->total_tiles = tile0;
+  // Kernel choice, once per table: the caller's, else PTK_FUSED_KERNEL, else
+  // the TMA ring when every peer buffer is on this device (virtual ranks,
+  // same-GPU cudaIpc mappings) and the register-staged kernel across GPUs.
+  int k = kernel;
+  if (k == PTK_FUSED_AUTO) k = fused_env_override();
+  if (k == PTK_FUSED_AUTO) k = all_local ? PTK_FUSED_TMA : PTK_FUSED_LDG;
+  t->kernel = k;
+  if (n_chunks > 0) {
+    const size_t bytes = sizeof(FusedDesc) * t->host.size();
+    cudaError_t e = cudaMalloc(&t->dev, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(t->dev, t->host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      if (t->dev) cudaFree(t->dev);
+      delete t;
+      return check_cuda(e, "ptk_fused_table_create: device table");
+    }
+  }
+  *out = t;
+  return PTK_OK;
+}
+
+int ptk_fused_table_destroy(ptk_fused_table* t) {
+  if (!t) return PTK_OK;
+  const cudaError_t e = t->dev ? cudaFree(t->dev) : cudaSuccess;
+  delete t;
+  return check_cuda(e, "ptk_fused_table_destroy");
+}
+
+int32_t ptk_fused_table_kernel(const ptk_fused_table* t) { return t ? t->kernel : -1; }
+
+namespace {
+int fused_table_launch(FusedOp op, const ptk_adam_config* cfg, const ptk_fused_table* t,
+                       ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                       const int32_t* skip_dev, void* stream, const char* what) {
+  if (!cfg || !t) return fail(PTK_EINVAL, std::string(what) + ": null argument");
+  if (cfg->step < 1) return fail(PTK_EINVAL, std::string(what) + ": step must be >= 1");
+  if (stats && !workspace) return fail(PTK_EINVAL, std::string(what) + ": stats requires workspace");
+  if (op == FusedOp::Stats && !stats) return fail(PTK_EINVAL, std::string(what) + ": null stats");
+  if (t->host.empty()) return PTK_OK;
+  if (t->device != current_device())
+    return fail(PTK_EINVAL, std::string(what) + ": table was created on another device");
+  FusedList list{};
+  list.table = t->dev;
+  list.one = t->host[0];
+  list.n_chunks = static_cast<int32_t>(t->host.size());
+  list.total_tiles = t->total_tiles;
+  list.rank = t->rank;
+  const ptk_adam_scalars s = derive_scalars(*cfg);
+  const int rc = dispatch_fused(t->world, op, s, list, t->max_shard,
+                                static_cast<StatsWorkspace*>(workspace), stats, gscale_dev,
+                                skip_dev, as_stream(stream), t->kernel == PTK_FUSED_TMA);
+  if (rc != PTK_OK) return rc;
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), what);
+}
+}  // namespace
+
+int ptk_fused_step_table(const ptk_adam_config* cfg, const ptk_fused_table* t,
+                         ptk_grad_stats_t* stats, void* workspace, const float* gscale_dev,
+                         const int32_t* skip_dev, void* stream) {
+  return fused_table_launch(FusedOp::Step, cfg, t, stats, workspace, gscale_dev, skip_dev, stream,
+                            "ptk_fused_step_table");
+}
+
+int ptk_fused_grad_stats_table(const ptk_adam_config* cfg, const ptk_fused_table* t,
+                               ptk_grad_stats_t* stats, void* workspace, void* stream) {
+  return fused_table_launch(FusedOp::Stats, cfg, t, stats, workspace, nullptr, nullptr, stream,
+                            "ptk_fused_grad_stats_table");
+}
+
 int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad_peers,
                          uint16_t* const* param_peers, int32_t world, int32_t rank, int64_t shard,
                          float* master, float* exp_avg, float* exp_avg_sq,
@@ -1193,38 +1628,38 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
     return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: shard must be a multiple of 8 elements");
   if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: step must be >= 1");
   if (stats && !workspace) return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: stats requires workspace");
-  PeerTable t{};
+  FusedList list{};
   for (int r = 0; r < world; ++r) {
     if (!grad_peers[r] || !param_peers[r] || !aligned16(grad_peers[r]) || !aligned16(param_peers[r]))
       return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: peer buffers must be non-null and 16-byte aligned");
-    t.grad[r] = grad_peers[r];
-    t.param[r] = param_peers[r];
+    list.one.grad[r] = grad_peers[r];
+    list.one.param[r] = param_peers[r];
   }
   if (!aligned16(master) || !aligned16(exp_avg) || !aligned16(exp_avg_sq))
     return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: state buffers must be 16-byte aligned");
   if (shard == 0) return PTK_OK;
+  const int dev = current_device();
+  int k = fused_env_override();
+  if (k == PTK_FUSED_AUTO) {
+    bool local = true;
+    for (int r = 0; r < world && local; ++r)
+      local = on_device(grad_peers[r], dev) && on_device(param_peers[r], dev);
+    k = local ? PTK_FUSED_TMA : PTK_FUSED_LDG;
+  }
+  list.table = nullptr;
+  list.one.master = master;
+  list.one.m = exp_avg;
+  list.one.v = exp_avg_sq;
+  list.one.shard = shard;
+  list.one.tile0 = 0;
+  list.n_chunks = 1;
+  list.rank = rank;
+  const int tile = fused_tile_for(world);
+  list.total_tiles = (shard + tile - 1) / tile;
   const ptk_adam_scalars s = derive_scalars(*cfg);
-  const int64_t off = static_cast<int64_t>(rank) * shard;
-  auto* ws = static_cast<StatsWorkspace*>(workspace);
-  cudaStream_t st = as_stream(stream);
-  bool tma = fused_mode() != 2;
-  if (fused_mode() == 0) {
-    int dev = 0;
-    PTK_TRY_CUDA(cudaGetDevice(&dev));
-    for (int r = 0; r < world && tma; ++r)
-      tma = same_device(grad_peers[r], dev) && same_device(param_peers[r], dev);
-  }
-  int rc = PTK_OK;
-  switch (world) {
-    case 1: rc = launch_fused<1>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 2: rc = launch_fused<2>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 3: rc = launch_fused<3>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 4: rc = launch_fused<4>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 5: rc = launch_fused<5>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 6: rc = launch_fused<6>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    case 7: rc = launch_fused<7>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-    default: rc = launch_fused<8>(s, t, off, shard, master, exp_avg, exp_avg_sq, ws, stats, st, tma); break;
-  }
+  const int rc = dispatch_fused(world, FusedOp::Step, s, list, shard,
+                                static_cast<StatsWorkspace*>(workspace), stats, nullptr, nullptr,
+                                as_stream(stream), k == PTK_FUSED_TMA);
   if (rc != PTK_OK) return rc;
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "fused_peer_kernel launch");
@@ -1239,14 +1674,40 @@ int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank, 
     if (!signal_peers[r]) return fail(PTK_EINVAL, "ptk_peer_barrier: null signal slot");
     t.slot[r] = signal_peers[r];
   }
-  static const int64_t timeout_ns = [] {
-    const char* e = std::getenv("PTK_PEER_BARRIER_TIMEOUT_MS");
-    const long long ms = e ? std::atoll(e) : 60000;
-    return static_cast<int64_t>(ms > 0 ? ms : 60000) * 1000000;
-  }();
-  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch, timeout_ns);
+  peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(t, world, rank, epoch, peer_timeout_ns());
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "peer_barrier_kernel launch");
+}
+
+int64_t ptk_stats_mailbox_bytes(void) {
+  return static_cast<int64_t>(sizeof(MailSlot)) * PTK_MAX_PEERS;
+}
+
+int ptk_stats_publish(const ptk_grad_stats_t* stats, void* const* mailbox_peers, int32_t world,
+                      int32_t rank, int32_t epoch, void* stream) {
+  if (!stats || !mailbox_peers || world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world)
+    return fail(PTK_EINVAL, "ptk_stats_publish: bad arguments");
+  MailTable t{};
+  for (int r = 0; r < world; ++r) {
+    if (!mailbox_peers[r] || (reinterpret_cast<uintptr_t>(mailbox_peers[r]) & 31u) != 0)
+      return fail(PTK_EINVAL, "ptk_stats_publish: mailboxes must be non-null and 32-byte aligned");
+    t.box[r] = static_cast<MailSlot*>(mailbox_peers[r]);
+  }
+  stats_publish_kernel<<<1, 32, 0, as_stream(stream)>>>(stats, t, world, rank, epoch);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "stats_publish_kernel launch");
+}
+
+int ptk_stats_collect(const void* mailbox, int32_t world, int32_t epoch, double max_norm,
+                      ptk_grad_stats_t* global_out, float* coef_out, int32_t* skip_out,
+                      void* stream) {
+  if (!mailbox || world < 1 || world > PTK_MAX_PEERS)
+    return fail(PTK_EINVAL, "ptk_stats_collect: bad arguments");
+  stats_collect_kernel<<<1, 32, 0, as_stream(stream)>>>(static_cast<const MailSlot*>(mailbox), world,
+                                                        epoch, max_norm, peer_timeout_ns(),
+                                                        global_out, coef_out, skip_out);
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "stats_collect_kernel launch");
 }
 
 int ptk_busy_wait(int64_t ns, void* stream) {

@@ -44,6 +44,7 @@ def _load():
     lib.oracle_fill_uniform_f32.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_float]
     lib.oracle_fill_uniform_bf16.argtypes = [c_void_p, c_int64, c_uint64, c_int64, c_float]
     lib.oracle_num_threads.restype = c_int
+    lib.oracle_set_num_threads.argtypes = [c_int]
     return lib
 
 
@@ -123,3 +124,7 @@ def f32_to_bf16(a: np.ndarray) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib.oracle_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    lib.oracle_set_num_threads(int(n))

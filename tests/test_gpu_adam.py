@@ -204,3 +204,97 @@ def test_fill_matches_oracle(cuda_device):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(_bits(a), ol.fill_f32(n, 42, 0.05, 1000).view(np.uint32))
     np.testing.assert_array_equal(_bits(b), ol.fill_bf16(n, 43, 1e-3, 7))
+
+
+# ---- one launch over a chunk table (ptk_chunk_adam_table) ----
+
+TABLE_CASES = {
+    # unpadded lengths (n % 8 tails), empty and sub-tile chunks, many small chunks
+    "ragged": [1, 7, 0, 8, 1536, 1536 * 148 + 8, 100_003, 5, 4096, 0, 1537],
+    "many_small": [12_288 + 8 * i for i in range(64)],
+    "one_big": [1536 * 148 * 5 + 24],
+}
+
+
+@pytest.mark.parametrize("case", sorted(TABLE_CASES))
+def test_chunk_table_bit_exact(cuda_device, case):
+    """Every chunk of a table updated by ONE persistent TMA launch (tiles of
+    all chunks walked by each CTA in global order): bit-identical to the
+    oracle per chunk, statistics summed over the whole table."""
+    nat = _nat()
+    sizes = TABLE_CASES[case]
+    states, host = [], []
+    for i, n in enumerate(sizes):
+        master = ol.fill_f32(n, 500 + i, 0.05)
+        states.append(DevState(master, cuda_device))
+        host.append([master, np.zeros(n, np.float32), np.zeros(n, np.float32),
+                     np.zeros(n, np.uint16)])
+    grads = [_dev_bits16(ol.fill_bf16(n, 900 + i, 1e-3), cuda_device) for i, n in enumerate(sizes)]
+    descs = (nat.ChunkDesc * len(sizes))()
+    for d, st, g in zip(descs, states, grads):
+        d.master, d.exp_avg, d.exp_avg_sq = st.master.data_ptr(), st.m.data_ptr(), st.v.data_ptr()
+        d.grad, d.param_out, d.n = g.data_ptr(), st.p.data_ptr(), st.n
+    table = ctypes.c_void_p()
+    nat.lib.ptk_chunk_table_create(descs, len(sizes), ctypes.byref(table))
+    assert nat.raw.ptk_chunk_table_params(table) == sum(sizes)
+    ws, stats = states[0].ws, states[0].stats
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    want_sq = 0.0
+    for step in (1, 2, 3):
+        cfg = nat.adam_config(lr=1e-3, weight_decay=0.01, adamw=True, step=step,
+                              grad_scale=0.5 if step == 2 else 1.0)
+        nat.lib.ptk_stats_reset(_vp(stats), s)
+        nat.lib.ptk_chunk_adam_table(ctypes.byref(cfg), table, _vp(stats), _vp(ws), None, None, s)
+        want_sq = 0.0
+        for i, (n, h) in enumerate(zip(sizes, host)):
+            sq, _ = ol.adam_step(ol.scalars(lr=1e-3, weight_decay=0.01, adamw=True, step=step,
+                                            grad_scale=0.5 if step == 2 else 1.0),
+                                 h[0], h[1], h[2], ol.fill_bf16(n, 900 + i, 1e-3), h[3])
+            want_sq += sq
+    torch.cuda.synchronize()
+    for st, h, n in zip(states, host, sizes):
+        np.testing.assert_array_equal(_bits(st.master), h[0].view(np.uint32))
+        np.testing.assert_array_equal(_bits(st.m), h[1].view(np.uint32))
+        np.testing.assert_array_equal(_bits(st.v), h[2].view(np.uint32))
+        np.testing.assert_array_equal(_bits(st.p)[:n], h[3])
+    assert abs(float(stats[0]) - want_sq) <= 1e-6 * want_sq
+    # device skip flag: the whole table is a no-op
+    before = [_bits(st.master).copy() for st in states]
+    skip = torch.ones(1, dtype=torch.int32, device=cuda_device)
+    cfg = nat.adam_config(step=4)
+    nat.lib.ptk_chunk_adam_table(ctypes.byref(cfg), table, None, None, None, _vp(skip), s)
+    torch.cuda.synchronize()
+    for b, st in zip(before, states):
+        np.testing.assert_array_equal(_bits(st.master), b)
+    nat.lib.ptk_chunk_table_destroy(table)
+
+
+def test_chunk_table_graph_capture_and_bad_args(cuda_device):
+    nat = _nat()
+    n = 50_000
+    st = DevState(ol.fill_f32(n, 1, 0.05), cuda_device)
+    ref = DevState(ol.fill_f32(n, 1, 0.05), cuda_device)
+    g = _dev_bits16(ol.fill_bf16(n, 2, 1e-3), cuda_device)
+    d = (nat.ChunkDesc * 1)()
+    d[0].master, d[0].exp_avg, d[0].exp_avg_sq = st.master.data_ptr(), st.m.data_ptr(), st.v.data_ptr()
+    d[0].grad, d[0].param_out, d[0].n = g.data_ptr(), st.p.data_ptr(), n
+    table = ctypes.c_void_p()
+    nat.lib.ptk_chunk_table_create(d, 1, ctypes.byref(table))
+    graph = torch.cuda.CUDAGraph()
+    cfgs = [nat.adam_config(step=k) for k in (1, 2)]
+    with torch.cuda.graph(graph):
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for cfg in cfgs:
+            nat.lib.ptk_chunk_adam_table(ctypes.byref(cfg), table, None, None, None, None, s)
+    graph.replay()
+    for cfg in cfgs:
+        ref.step(cfg, g, stats=False)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits(st.master), _bits(ref.master))
+    np.testing.assert_array_equal(_bits(st.p), _bits(ref.p))
+    nat.lib.ptk_chunk_table_destroy(table)
+    # misaligned buffers are refused at creation
+    d[0].grad = g.data_ptr() + 2
+    t2 = ctypes.c_void_p()
+    assert nat.raw.ptk_chunk_table_create(d, 1, ctypes.byref(t2)) == -1
+    assert "aligned" in nat.last_error()

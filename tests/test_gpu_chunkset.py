@@ -96,11 +96,104 @@ def test_fused_ldg_variant_bit_exact(cuda_device):
     import sys
     env = dict(os.environ, PTK_FUSED_KERNEL="ldg")
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-p",
-                        "no:cacheprovider", "-k", "test_fused_virtual_ranks_bit_exact"],
-                       env=env, capture_output=True, text=True, timeout=600,
+                        "no:cacheprovider", "-k",
+                        "fused_virtual_ranks or fused_global_norm or fused_nonfinite"],
+                       env=env, capture_output=True, text=True, timeout=900,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "7 passed" in r.stdout
+    assert "12 passed" in r.stdout, r.stdout[-2000:]
+
+
+def _fused_sets(ch, numels, world, dev):
+    sets = [ch.ChunkSet(numels, world=world, rank=r, device=dev, mode="fused")
+            for r in range(world)]
+    for cs in sets:
+        cs.init_synthetic()
+        cs.fill_grads(0)
+        cs.attach_virtual_peers(sets)
+    return sets
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_fused_global_norm_clipping_virtual_ranks(cuda_device, world):
+    """Clipping in the fused exchange: statistics pass over every rank's
+    reduced gradient shards (ptk_fused_grad_stats_table), 16-byte partials
+    exchanged through the peer mailboxes (rank-order sum: the same bits on
+    every rank), device clip coefficient read by the fused update. Checked
+    against the oracle's fp64 global norm (1e-6) and, given the device
+    coefficient, bit-exactly on every rank's state and gathered chunk."""
+    nat, ch = _modules()
+    numels = [10_007, 3 * 4096 + 8]
+    sets = _fused_sets(ch, numels, world, cuda_device)
+    hyper = ch.AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True)
+    max_norm = 0.01
+    ch.fused_group_step(sets, hyper, max_grad_norm=max_norm)
+    torch.cuda.synchronize()
+    coefs = [float(cs.clip_coef[0]) for cs in sets]
+    assert len(set(coefs)) == 1, coefs                 # identical on every rank
+    assert len({tuple(cs.stats.cpu().tolist()) for cs in sets}) == 1
+    coef = coefs[0]
+    sq = 0.0
+    reduced = {}
+    for ci, n in enumerate(numels):
+        shard = ol.shard_elems(n, world)
+        grads = []
+        for q in range(world):
+            g = ol.fill_bf16(shard * world, ch.grad_seed(ci, q, 0), ch.GRAD_SCALE)
+            g[n:] = 0
+            grads.append(g)
+        for r in range(world):
+            red = ol.reduce_scatter(grads, r, shard, fp32=True)
+            reduced[ci, r] = red
+            scaled = (red * np.float32(1.0 / world)).astype(np.float64)
+            sq += float(np.dot(scaled, scaled))
+    want = min(1.0, max_norm / (np.sqrt(sq) + 1e-6))
+    assert want < 1.0 and abs(coef - want) <= 1e-6 * want
+    assert abs(float(sets[0].stats[0]) - sq) <= 1e-6 * sq
+    for ci, n in enumerate(numels):
+        shard = ol.shard_elems(n, world)
+        master_full = ol.fill_f32(shard * world, ch.master_seed(ci), ch.MASTER_SCALE)
+        master_full[n:] = 0
+        params = []
+        for r in range(world):
+            mst = master_full[r * shard:(r + 1) * shard].copy()
+            m = np.zeros(shard, np.float32)
+            v = np.zeros(shard, np.float32)
+            out = np.zeros(shard, np.uint16)
+            s = ol.scalars(lr=1e-3, weight_decay=0.01, adamw=True, step=1, grad_scale=1.0 / world)
+            s.gscale = float(np.float32(s.gscale) * np.float32(coef))
+            ol.adam_step(s, mst, m, v, reduced[ci, r], out)
+            c = sets[r].chunks[ci]
+            np.testing.assert_array_equal(_bits(c.master), mst.view(np.uint32))
+            np.testing.assert_array_equal(_bits(c.exp_avg_sq), v.view(np.uint32))
+            params.append(out)
+        gathered = ol.allgather(params)
+        for r in range(world):
+            np.testing.assert_array_equal(_bf16_bits(sets[r].chunks[ci].param), gathered)
+    # a second clipped step uses fresh epochs of the same mailboxes
+    for cs in sets:
+        cs.fill_grads(1)
+    ch.fused_group_step(sets, hyper, max_grad_norm=max_norm)
+    torch.cuda.synchronize()
+    assert len({float(cs.clip_coef[0]) for cs in sets}) == 1
+
+
+def test_fused_nonfinite_skips_every_rank(cuda_device):
+    """One rank's non-finite gradient element skips the step on ALL ranks
+    (global overflow flag from the mailbox exchange): no state or parameter
+    changes anywhere."""
+    nat, ch = _modules()
+    world = 4
+    sets = _fused_sets(ch, [4096, 8200], world, cuda_device)
+    sets[2].chunks[1].grad[100] = float("inf")
+    before = [[(c.master.clone(), c.param.clone()) for c in cs.chunks] for cs in sets]
+    ch.fused_group_step(sets, ch.AdamHyper(), skip_nonfinite=True)
+    torch.cuda.synchronize()
+    for cs, b in zip(sets, before):
+        assert int(cs.skip_flag[0]) == 1
+        assert int(cs.stats.view(torch.int64)[1]) == 1
+        for (m0, p0), c in zip(b, cs.chunks):
+            assert torch.equal(m0, c.master) and torch.equal(p0, c.param)
 
 
 def _world1_comm(nat):
