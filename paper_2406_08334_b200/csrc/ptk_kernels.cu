@@ -373,17 +373,6 @@ struct ChunkDesc {
   int64_t tile0;
 };
 
-struct ChunkList {
-  const ChunkDesc* table;  // device table of n_chunks descriptors, or nullptr -> `one`
-  ChunkDesc one;
-  int64_t total_tiles;
-  int32_t n_chunks;
-};
-
-__device__ __forceinline__ const ChunkDesc& chunk_at(const ChunkList& l, int c) {
-  return l.table != nullptr ? l.table[c] : l.one;
-}
-
 struct FusedDesc {
   const uint16_t* grad[PTK_MAX_PEERS];  // rank r's full gradient chunk
   uint16_t* param[PTK_MAX_PEERS];       // rank r's full parameter chunk
@@ -406,22 +395,37 @@ __device__ __forceinline__ const FusedDesc& fused_at(const FusedList& l, int c) 
   return l.table != nullptr ? l.table[c] : l.one;
 }
 
-// Producer-side cursor over the global tile order (monotone per CTA).
+// tid 0's cursor over the global tile order (monotone per CTA) with the
+// current chunk's descriptor cached in registers: descriptors are read from
+// the table once per chunk, not once per tile (the elected thread's per-tile
+// latency is on every CTA's critical path).
+template <class D>
 struct TileCursor {
-  int c = 0;
-  int64_t end = 0;
+  int c = -1;
+  int64_t end = 0;  // first global tile of chunk c + 1
+  D d;
 };
 
-__device__ __forceinline__ const ChunkDesc& desc_at(const ChunkList& l, int c) { return chunk_at(l, c); }
 __device__ __forceinline__ const FusedDesc& desc_at(const FusedList& l, int c) { return fused_at(l, c); }
 
-template <class L>
-__device__ __forceinline__ int cursor_seek(const L& l, TileCursor& cur, int64_t t) {
-  while (t >= cur.end) {  // skips chunks without tiles (tile0 equal to the next one)
+template <class L, class D>
+__device__ __forceinline__ void cursor_seek(const L& l, TileCursor<D>& cur, int64_t t) {
+  if (t < cur.end) return;
+  do {  // skips chunks without tiles (tile0 equal to the next one)
     ++cur.c;
     cur.end = cur.c + 1 < l.n_chunks ? desc_at(l, cur.c + 1).tile0 : l.total_tiles;
+  } while (t >= cur.end);
+  cur.d = desc_at(l, cur.c);
+}
+
+// The store side follows the same chunks in the same order.
+template <class L, class D>
+__device__ __forceinline__ const D& cursor_at(const L& l, TileCursor<D>& cur, int c) {
+  if (c != cur.c) {
+    cur.c = c;
+    cur.d = desc_at(l, c);
   }
-  return cur.c;
+  return cur.d;
 }
 
 struct ItemMeta {
@@ -439,6 +443,14 @@ struct ItemMeta {
 // tiles of shared memory form a ring; the producer runs kStages-2 tiles ahead
 // of the consumers, and a stage is refilled only after the bulk store that
 // last read it has finished reading shared memory (wait_group.read 1).
+//
+// The chunk table travels in the KERNEL PARAMETERS (__grid_constant__, the
+// constant bank): every thread walks it with warp-uniform indices, so the
+// descriptor fields load into uniform registers (LDCU) and the elected
+// thread's bulk-copy addresses need no per-thread -> uniform conversion. Its
+// per-tile scalar work then stays as small as with a single chunk (every
+// warp waits for it at the CTA barrier). Tables larger than kCap chunks are
+// launched in batches of kCap.
 
 template <int kTile>
 struct TmaStage {
@@ -449,9 +461,32 @@ struct TmaStage {
   uint16_t param[kTile];
 };
 
-template <int kTile, int kStages, int kThr, bool kStats, bool kHint>
+template <int kCap>
+struct ChunkBatch {
+  ChunkDesc d[kCap];  // tile0 counted from this batch's first chunk
+  int64_t total_tiles;
+  int32_t n_chunks;
+};
+
+// Uniform cursor over a batch's tiles (every thread keeps its own copy).
+template <int kCap>
+struct BatchCursor {
+  int c = 0;
+  int64_t end;
+  __device__ __forceinline__ explicit BatchCursor(const ChunkBatch<kCap>& b)
+      : end(b.n_chunks > 1 ? b.d[1].tile0 : b.total_tiles) {}
+  __device__ __forceinline__ int seek(const ChunkBatch<kCap>& b, int64_t t) {
+    while (t >= end) {  // skips chunks without tiles
+      ++c;
+      end = c + 1 < b.n_chunks ? b.d[c + 1].tile0 : b.total_tiles;
+    }
+    return c;
+  }
+};
+
+template <int kTile, int kStages, int kThr, bool kStats, bool kHint, int kCap>
 __global__ void __launch_bounds__(kThr, 1)
-chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list,
+chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkBatch<kCap> b,
                       StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
                       const int32_t* skip_dev) {
   static_assert(kTile % (kThr * 4) == 0, "tile must be a multiple of 4 elements per thread");
@@ -459,12 +494,11 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<TmaStage<kTile>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
-  __shared__ ItemMeta meta[kStages];
 
   if (skip_dev != nullptr && *skip_dev != 0) return;
   const float gs = launch_gscale(s, gscale_dev);
   const int tid = threadIdx.x;
-  const int64_t T = list.total_tiles;
+  const int64_t T = b.total_tiles;
   const int64_t my_items = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (tid == 0) {
@@ -482,27 +516,29 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
     if (kHint) bulk_store_hint(dst, src, bytes, policy);
     else bulk_store(dst, src, bytes);
   };
-  TileCursor cur;
-  cur.end = list.n_chunks > 1 ? chunk_at(list, 1).tile0 : T;
-  // Ring positions are carried as (stage, phase) counters -- the pipeline
-  // state of CUTLASS -- rather than k % kStages.
+  // item k of this CTA -> (chunk, first element, length); len is a multiple
+  // of 8 (the chunk's multiple-of-8 prefix is tiled)
+  auto item = [&](BatchCursor<kCap>& cur, int64_t k, int& c, int64_t& e, int& len) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    c = cur.seek(b, t);
+    e = (t - b.d[c].tile0) * kTile;
+    const int64_t left = (b.d[c].n & ~int64_t{7}) - e;
+    len = left < kTile ? static_cast<int>(left) : kTile;
+  };
+  BatchCursor<kCap> lcur(b), ccur(b);  // load-ahead cursor (tid 0) / current item
   int load_st = 0;
   auto issue_load = [&](int64_t k) {  // k-th item of this CTA, into stage load_st
     const int st = load_st;
     load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    const int64_t t = blockIdx.x + k * gridDim.x;
-    const int c = cursor_seek(list, cur, t);
-    const ChunkDesc& d = chunk_at(list, c);
-    const int64_t e = (t - d.tile0) * kTile;
-    const int64_t left = (d.n & ~int64_t{7}) - e;
-    const int len = left < kTile ? static_cast<int>(left) : kTile;
-    meta[st] = ItemMeta{e, c, len};  // published to the consumers by the arrive below
+    int c, len;
+    int64_t e;
+    item(lcur, k, c, e, len);
     TmaStage<kTile>& S = stage[st];
     mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + sizeof(uint16_t)));
-    load(S.master, d.master + e, len * 4, &full[st]);
-    load(S.m, d.m + e, len * 4, &full[st]);
-    load(S.v, d.v + e, len * 4, &full[st]);
-    load(S.grad, d.grad + e, len * 2, &full[st]);
+    load(S.master, b.d[c].master + e, len * 4, &full[st]);
+    load(S.m, b.d[c].m + e, len * 4, &full[st]);
+    load(S.v, b.d[c].v + e, len * 4, &full[st]);
+    load(S.grad, b.d[c].grad + e, len * 2, &full[st]);
   };
 
   constexpr int kAhead = kStages - 2;
@@ -518,14 +554,16 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
       bulk_wait_read<1>();  // the store of item k-2 (same stage) has read its smem
       issue_load(k + kAhead);
     }
+    int c, len;
+    int64_t ge;
+    item(ccur, k, c, ge, len);
     mbar_wait(&full[st], phase);
-    const int len = meta[st].len;
     TmaStage<kTile>& S = stage[st];
     float usq = 0.0f;
 #pragma unroll
     for (int j = 0; j < kTile / (kThr * 4); ++j) {
       const int e = (j * kThr + tid) * 4;
-      if (e >= len) break;  // only in a chunk's last tile (len is a multiple of 8)
+      if (e >= len) break;  // only in a chunk's last tile
       float4 p = *reinterpret_cast<float4*>(&S.master[e]);
       float4 m = *reinterpret_cast<float4*>(&S.m[e]);
       float4 v = *reinterpret_cast<float4*>(&S.v[e]);
@@ -550,12 +588,10 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
     fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     __syncthreads();
     if (tid == 0) {
-      const ItemMeta it = meta[st];
-      const ChunkDesc& d = chunk_at(list, it.c);
-      store(d.master + it.e, S.master, it.len * 4);
-      store(d.m + it.e, S.m, it.len * 4);
-      store(d.v + it.e, S.v, it.len * 4);
-      if (d.param != nullptr) store(d.param + it.e, S.param, it.len * 2);
+      store(b.d[c].master + ge, S.master, len * 4);
+      store(b.d[c].m + ge, S.m, len * 4);
+      store(b.d[c].v + ge, S.v, len * 4);
+      if (b.d[c].param != nullptr) store(b.d[c].param + ge, S.param, len * 2);
       bulk_commit();
     }
     if (++st == kStages) {
@@ -565,8 +601,8 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
   }
   if (tid == 0) bulk_wait_all();
   // the < 8 trailing elements of chunks whose length is not a multiple of 8
-  for (int c = blockIdx.x; c < list.n_chunks; c += gridDim.x) {
-    const ChunkDesc& d = chunk_at(list, c);
+  for (int c = blockIdx.x; c < b.n_chunks; c += gridDim.x) {
+    const ChunkDesc& d = b.d[c];
     const int64_t e = (d.n & ~int64_t{7}) + tid;
     if (e < d.n) {
       float usq = 0.0f;
@@ -583,6 +619,25 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkList list
   }
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
+
+// Warp-specialized ring pieces used by the fused kernel below.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+struct RingPos {
+  int st = 0;
+  uint32_t ph = 0;
+  template <int kStages>
+  __device__ __forceinline__ void next() {
+    if (++st == kStages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+constexpr int kRoleThreads = 64;  // producer warp + storer warp
 
 // -------------------------------------------------------------- K2 -------
 
@@ -778,116 +833,137 @@ constexpr int fused_stages() {
 }
 
 template <int W, int kStages>
-__global__ void __launch_bounds__(fused_threads<W>(), 1)
+__global__ void __launch_bounds__(fused_threads<W>() + kRoleThreads, 1)
 fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list,
                       StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
                       const int32_t* skip_dev) {
   constexpr int kFusedTile = fused_tile<W>();
-  static_assert(kStages >= 3, "ring needs >= 3 stages");
+  constexpr int kThr = fused_threads<W>();
+  constexpr int kConsumerWarps = kThr / 32;
+  static_assert(kStages >= 2, "ring needs >= 2 stages");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<FusedStage<W>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t done[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
   __shared__ ItemMeta meta[kStages];
   if (skip_dev != nullptr && *skip_dev != 0) return;
   const float gs = launch_gscale(s, gscale_dev);
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int64_t T = list.total_tiles;
   const int64_t my_items = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&done[i], kConsumerWarps);
+      mbar_init(&empty[i], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
-  TileCursor cur;
-  cur.end = list.n_chunks > 1 ? fused_at(list, 1).tile0 : T;
-  int load_st = 0;
-  auto issue_load = [&](int64_t k) {
-    const int st = load_st;
-    load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    const int64_t t = blockIdx.x + k * gridDim.x;
-    const int c = cursor_seek(list, cur, t);
-    const FusedDesc& d = fused_at(list, c);
-    const int64_t e = (t - d.tile0) * kFusedTile;
-    const int64_t left = d.shard - e;
-    const int len = left < kFusedTile ? static_cast<int>(left) : kFusedTile;
-    const int64_t off = static_cast<int64_t>(list.rank) * d.shard + e;
-    meta[st] = ItemMeta{e, c, len};
-    FusedStage<W>& S = stage[st];
-    mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + W * sizeof(uint16_t)));
-    bulk_load(S.master, d.master + e, len * 4, &full[st]);
-    bulk_load(S.m, d.m + e, len * 4, &full[st]);
-    bulk_load(S.v, d.v + e, len * 4, &full[st]);
-#pragma unroll
-    for (int r = 0; r < W; ++r) bulk_load(S.grad[r], d.grad[r] + off, len * 2, &full[st]);
-  };
-  constexpr int kAhead = kStages - 2;
-  if (tid == 0)
-    for (int64_t k = 0; k < kAhead && k < my_items; ++k) issue_load(k);
-
   double sq = 0.0;
   unsigned bad = 0;
-  int st = 0;
-  uint32_t phase = 0;
-  for (int64_t k = 0; k < my_items; ++k) {
-    if (tid == 0 && k + kAhead < my_items) {
-      bulk_wait_read<1>();
-      issue_load(k + kAhead);
-    }
-    mbar_wait(&full[st], phase);
-    const int len = meta[st].len;
-    FusedStage<W>& S = stage[st];
-    const int e = tid * 4;
-    if (e < len) {  // always, except in a chunk's last tile
-      float4 p = *reinterpret_cast<float4*>(&S.master[e]);
-      float4 m = *reinterpret_cast<float4*>(&S.m[e]);
-      float4 v = *reinterpret_cast<float4*>(&S.v[e]);
-      uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[0][e]);
-      float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: local state + every rank's gradient tile --
+    if (lane == 0) {
+      TileCursor<FusedDesc> cur;
+      RingPos pos;
+      for (int64_t k = 0; k < my_items; ++k) {
+        if (k >= kStages) mbar_wait(&empty[pos.st], pos.ph ^ 1u);
+        const int64_t t = blockIdx.x + k * gridDim.x;
+        cursor_seek(list, cur, t);
+        const FusedDesc& d = cur.d;
+        const int64_t e = (t - d.tile0) * kFusedTile;
+        const int64_t left = d.shard - e;
+        const int len = left < kFusedTile ? static_cast<int>(left) : kFusedTile;
+        const int64_t off = static_cast<int64_t>(list.rank) * d.shard + e;
+        meta[pos.st] = ItemMeta{e, cur.c, len};
+        FusedStage<W>& S = stage[pos.st];
+        uint64_t* bar = &full[pos.st];
+        mbar_expect_tx(bar, static_cast<uint32_t>(len) * (3 * sizeof(float) + W * sizeof(uint16_t)));
+        bulk_load(S.master, d.master + e, len * 4, bar);
+        bulk_load(S.m, d.m + e, len * 4, bar);
+        bulk_load(S.v, d.v + e, len * 4, bar);
 #pragma unroll
-      for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
-        g2 = *reinterpret_cast<const uint2*>(&S.grad[r][e]);
-        g[0] = __fadd_rn(g[0], bf_lo(g2.x));
-        g[1] = __fadd_rn(g[1], bf_hi(g2.x));
-        g[2] = __fadd_rn(g[2], bf_lo(g2.y));
-        g[3] = __fadd_rn(g[3], bf_hi(g2.y));
+        for (int r = 0; r < W; ++r) bulk_load(S.grad[r], d.grad[r] + off, len * 2, bar);
+        pos.next<kStages>();
       }
-      float* pp = &p.x;
-      float* mm = &m.x;
-      float* vv = &v.x;
-      float usq = 0.0f;
+    }
+  } else if (warp == kConsumerWarps + 1) {
+    // ------------- storer: local state + the bf16 tile into every rank --
+    if (lane == 0) {
+      TileCursor<FusedDesc> scur;
+      RingPos pos;
+      int prev = -1;
+      for (int64_t k = 0; k < my_items; ++k) {
+        mbar_wait(&done[pos.st], pos.ph);
+        const ItemMeta it = meta[pos.st];
+        const FusedDesc& d = cursor_at(list, scur, it.c);
+        const int64_t off = static_cast<int64_t>(list.rank) * d.shard + it.e;
+        FusedStage<W>& S = stage[pos.st];
+        bulk_store(d.master + it.e, S.master, it.len * 4);
+        bulk_store(d.m + it.e, S.m, it.len * 4);
+        bulk_store(d.v + it.e, S.v, it.len * 4);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float gk = __fmul_rn(g[q], gs);
-        accum_stats(gk, usq, bad);
-        adam_elem(s, gk, pp[q], mm[q], vv[q]);
+        for (int r = 0; r < W; ++r) bulk_store(d.param[r] + off, S.param, it.len * 2);
+        bulk_commit();
+        if (prev >= 0) {
+          bulk_wait_read<1>();
+          mbar_arrive(&empty[prev]);
+        }
+        prev = pos.st;
+        pos.next<kStages>();
       }
-      sq += usq;
-      *reinterpret_cast<float4*>(&S.master[e]) = p;
-      *reinterpret_cast<float4*>(&S.m[e]) = m;
-      *reinterpret_cast<float4*>(&S.v[e]) = v;
-      *reinterpret_cast<uint2*>(&S.param[e]) =
-          make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
+      bulk_wait_all();
     }
-    fence_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      const ItemMeta it = meta[st];
-      const FusedDesc& d = fused_at(list, it.c);
-      const int64_t off = static_cast<int64_t>(list.rank) * d.shard + it.e;
-      bulk_store(d.master + it.e, S.master, it.len * 4);
-      bulk_store(d.m + it.e, S.m, it.len * 4);
-      bulk_store(d.v + it.e, S.v, it.len * 4);
+  } else {
+    // ------------------------------------------------------ consumers --
+    RingPos pos;
+    for (int64_t k = 0; k < my_items; ++k) {
+      mbar_wait(&full[pos.st], pos.ph);
+      const int len = meta[pos.st].len;
+      FusedStage<W>& S = stage[pos.st];
+      const int e = tid * 4;
+      if (e < len) {  // always, except in a chunk's last tile
+        float4 p = *reinterpret_cast<float4*>(&S.master[e]);
+        float4 m = *reinterpret_cast<float4*>(&S.m[e]);
+        float4 v = *reinterpret_cast<float4*>(&S.v[e]);
+        uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[0][e]);
+        float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
 #pragma unroll
-      for (int r = 0; r < W; ++r) bulk_store(d.param[r] + off, S.param, it.len * 2);
-      bulk_commit();
-    }
-    if (++st == kStages) {
-      st = 0;
-      phase ^= 1u;
+        for (int r = 1; r < W; ++r) {  // fp32 sum in rank order (deterministic)
+          g2 = *reinterpret_cast<const uint2*>(&S.grad[r][e]);
+          g[0] = __fadd_rn(g[0], bf_lo(g2.x));
+          g[1] = __fadd_rn(g[1], bf_hi(g2.x));
+          g[2] = __fadd_rn(g[2], bf_lo(g2.y));
+          g[3] = __fadd_rn(g[3], bf_hi(g2.y));
+        }
+        float* pp = &p.x;
+        float* mm = &m.x;
+        float* vv = &v.x;
+        float usq = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float gk = __fmul_rn(g[q], gs);
+          accum_stats(gk, usq, bad);
+          adam_elem(s, gk, pp[q], mm[q], vv[q]);
+        }
+        sq += usq;
+        *reinterpret_cast<float4*>(&S.master[e]) = p;
+        *reinterpret_cast<float4*>(&S.m[e]) = m;
+        *reinterpret_cast<float4*>(&S.v[e]) = v;
+        *reinterpret_cast<uint2*>(&S.param[e]) =
+            make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[pos.st]);
+      pos.next<kStages>();
     }
   }
-  if (tid == 0) bulk_wait_all();
+  __syncthreads();
   if (stats != nullptr) reduce_stats(sq, bad, ws, stats);
 }
 
@@ -1070,16 +1146,17 @@ constexpr int kUnroll = 2;
 #ifdef PTK_BENCH_VARIANTS
 #define PTK_TMA_VARIANTS(X)                     \
   X(Tma1536x9t384, 1536, 9, 1, 384, false)      \
-  X(Tma1536x8t384, 1536, 8, 1, 384, false)      \
-  X(Tma1536x8t384h, 1536, 8, 1, 384, true)      \
-  X(Tma1536x9t384h, 1536, 9, 1, 384, true)      \
-  X(Tma1536x4x2t384, 1536, 4, 2, 384, false)    \
-  X(Tma2048x6, 2048, 6, 1, 256, false)          \
-  X(Tma2048x6h, 2048, 6, 1, 256, true)          \
+  X(Tma2048x6t512, 2048, 6, 1, 512, false)      \
+  X(Tma2048x6t256, 2048, 6, 1, 256, false)      \
+  X(Tma2048x6t512h, 2048, 6, 1, 512, true)      \
+  X(Tma2560x5t640, 2560, 5, 1, 640, false)      \
   X(Tma3072x4t384, 3072, 4, 1, 384, false)      \
-  X(Tma1792x7t448, 1792, 7, 1, 448, false)
+  X(Tma3072x4t768, 3072, 4, 1, 768, false)      \
+  X(Tma1024x13t256, 1024, 13, 1, 256, false)    \
+  X(Tma1792x7t448, 1792, 7, 1, 448, false)      \
+  X(Tma1024x6x2t256, 1024, 6, 2, 256, false)
 #else
-#define PTK_TMA_VARIANTS(X) X(Tma1536x9t384, 1536, 9, 1, 384, false)
+#define PTK_TMA_VARIANTS(X) X(Tma2048x6t512, 2048, 6, 1, 512, false)
 #endif
 
 #define PTK_ENUM_ENTRY(V, T, S, P, THR, H) V,
@@ -1102,7 +1179,7 @@ AdamVariant adam_variant() {
     }
     PTK_TMA_VARIANTS(PTK_NAME_ENTRY)
 #undef PTK_NAME_ENTRY
-    return AdamVariant::Tma1536x9t384;
+    return AdamVariant::Tma2048x6t512;
   }();
   return v;
 }
@@ -1115,7 +1192,7 @@ int adam_tile() {
     PTK_TMA_VARIANTS(PTK_TILE_CASE)
 #undef PTK_TILE_CASE
     default:
-      return 1536;
+      return 2048;
   }
 }
 
@@ -1131,52 +1208,73 @@ void launch_ldg(const ptk_adam_scalars& s, float* master, float* m, float* v,
   launch_counter()++;
 }
 
-template <int kTile, int kStages, int kPerSm, int kThr, bool kStats, bool kHint>
-int launch_tma(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
+template <int kTile, int kStages, int kPerSm, int kThr, bool kStats, bool kHint, int kCap>
+int launch_tma(const ptk_adam_scalars& s, const ChunkBatch<kCap>& b, StatsWorkspace* ws,
                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                cudaStream_t st) {
-  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint>;
+  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint, kCap>;
   constexpr int kSmem = kStages * static_cast<int>(sizeof(TmaStage<kTile>));
   static std::atomic<bool> configured[kMaxDevices];
   const int rc = ensure_smem(k, kSmem, configured, "chunk_adam_tma_kernel smem attribute");
   if (rc != PTK_OK) return rc;
   int64_t grid = static_cast<int64_t>(sm_count()) * kPerSm;
-  if (grid > list.total_tiles) grid = list.total_tiles;
+  if (grid > b.total_tiles) grid = b.total_tiles;
   if (grid < 1) grid = 1;  // tails only
-  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, list, ws, stats, gscale_dev, skip_dev);
+  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, b, ws, stats, gscale_dev, skip_dev);
   launch_counter()++;
   return PTK_OK;
 }
 
-template <int kTile, int kStages, int kPerSm, int kThr, bool kHint>
-int launch_tma_any(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
+template <int kTile, int kStages, int kPerSm, int kThr, bool kHint, int kCap>
+int launch_tma_any(const ptk_adam_scalars& s, const ChunkBatch<kCap>& b, StatsWorkspace* ws,
                    ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                    cudaStream_t st) {
-  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true, kHint>(s, list, ws, stats,
-                                                                       gscale_dev, skip_dev, st)
-               : launch_tma<kTile, kStages, kPerSm, kThr, false, kHint>(s, list, ws, stats,
-                                                                        gscale_dev, skip_dev, st);
+  return stats ? launch_tma<kTile, kStages, kPerSm, kThr, true, kHint, kCap>(
+                     s, b, ws, stats, gscale_dev, skip_dev, st)
+               : launch_tma<kTile, kStages, kPerSm, kThr, false, kHint, kCap>(
+                     s, b, ws, stats, gscale_dev, skip_dev, st);
 }
 
 int64_t tiles_of(int64_t n, int tile) { return ((n & ~int64_t{7}) + tile - 1) / tile; }
 
-// One TMA launch over `list` (tile0 computed for adam_tile()).
-int launch_tma_list(const ptk_adam_scalars& s, const ChunkList& list, StatsWorkspace* ws,
-                    ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
-                    cudaStream_t st) {
+// One TMA launch over a batch (tile0 computed for adam_tile()).
+template <int kCap>
+int launch_tma_batch(const ptk_adam_scalars& s, const ChunkBatch<kCap>& b, StatsWorkspace* ws,
+                     ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
+                     cudaStream_t st) {
   switch (adam_variant()) {
 #define PTK_TMA_CASE(V, T, S, P, THR, H) \
   case AdamVariant::V:                   \
-    return launch_tma_any<T, S, P, THR, H>(s, list, ws, stats, gscale_dev, skip_dev, st);
+    return launch_tma_any<T, S, P, THR, H, kCap>(s, b, ws, stats, gscale_dev, skip_dev, st);
     PTK_TMA_VARIANTS(PTK_TMA_CASE)
 #undef PTK_TMA_CASE
     default:
-      return fail(PTK_EINVAL, "launch_tma_list: not a TMA variant");
+      return fail(PTK_EINVAL, "launch_tma_batch: not a TMA variant");
   }
+}
+
+// Batch capacities: one chunk (ptk_chunk_adam), small tables (a model's
+// handful of 512 MiB - 1 GiB chunks) and large tables (up to 128 chunks per
+// launch: 7 KB of kernel parameters).
+constexpr int kSmallCap = 16;
+constexpr int kLargeCap = 128;
+
+template <int kCap>
+void fill_batch(ChunkBatch<kCap>& b, const ChunkDesc* descs, int n, int tile) {
+  b = ChunkBatch<kCap>{};
+  int64_t tile0 = 0;
+  for (int c = 0; c < n; ++c) {
+    b.d[c] = descs[c];
+    b.d[c].tile0 = tile0;
+    tile0 += tiles_of(descs[c].n, tile);
+  }
+  b.n_chunks = n;
+  b.total_tiles = tile0;
 }
 
 int validate_adam_buffers(const float* master, const float* m, const float* v, const void* grad,
                           const uint16_t* param_out, int64_t n, const char* what) {
+  if (n == 0) return PTK_OK;  // an empty chunk touches no buffer
   if (!master || !m || !v || !grad) return fail(PTK_EINVAL, std::string(what) + ": null buffer");
   if (n < 0) return fail(PTK_EINVAL, std::string(what) + ": negative n");
   if (!aligned16(master) || !aligned16(m) || !aligned16(v) || !aligned16(grad) ||
@@ -1201,12 +1299,10 @@ int launch_adam(const ptk_adam_config* cfg, float* master, float* m, float* v,
   cudaStream_t st = as_stream(stream);
   if constexpr (std::is_same_v<G, GradBf16>) {
     if (adam_variant() != AdamVariant::Ldg) {
-      ChunkList list{};
-      list.table = nullptr;
-      list.one = ChunkDesc{master, m, v, grad, param_out, n, 0};
-      list.n_chunks = 1;
-      list.total_tiles = tiles_of(n, adam_tile());
-      rc = launch_tma_list(s, list, ws, stats, gscale_dev, skip_dev, st);
+      const ChunkDesc one{master, m, v, grad, param_out, n, 0};
+      ChunkBatch<1> b;
+      fill_batch(b, &one, 1, adam_tile());
+      rc = launch_tma_batch(s, b, ws, stats, gscale_dev, skip_dev, st);
       return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma launch");
     }
   }
@@ -1277,7 +1373,7 @@ int launch_fused(FusedOp op, const ptk_adam_scalars& s, const FusedList& list, i
   int64_t grid = sm_count();
   if (grid > list.total_tiles) grid = list.total_tiles;
   if (grid < 1) grid = 1;
-  k<<<static_cast<int>(grid), fused_threads<W>(), kSmem, st>>>(s, list, ws, stats, gscale_dev,
+  k<<<static_cast<int>(grid), fused_threads<W>() + kRoleThreads, kSmem, st>>>(s, list, ws, stats, gscale_dev,
                                                                 skip_dev);
   return PTK_OK;
 }
@@ -1313,11 +1409,10 @@ using namespace ptk;
 
 // Opaque table handles of the C-ABI (include/ptk.h).
 struct ptk_chunk_table {
-  std::vector<ChunkDesc> host;  // tile0 for `tile`
-  ChunkDesc* dev = nullptr;
-  int64_t total_tiles = 0;
-  int tile = 0;
-  int device = 0;
+  std::vector<ChunkDesc> host;                    // the caller's chunks
+  ChunkBatch<kSmallCap> small{};                  // n <= kSmallCap: one launch
+  std::vector<ChunkBatch<kLargeCap>> large;       // else batches of kLargeCap
+  int tile = 0;                                   // tile size the batches were cut for
 };
 
 struct ptk_fused_table {
@@ -1383,9 +1478,6 @@ int ptk_chunk_table_create(const ptk_chunk_desc* descs, int32_t n_chunks, ptk_ch
     return fail(PTK_EINVAL, "ptk_chunk_table_create: bad arguments");
   *out = nullptr;
   auto* t = new ptk_chunk_table;
-  t->tile = adam_tile();
-  t->device = current_device();
-  int64_t tile0 = 0;
   for (int32_t c = 0; c < n_chunks; ++c) {
     const ptk_chunk_desc& d = descs[c];
     const int rc = validate_adam_buffers(d.master, d.exp_avg, d.exp_avg_sq, d.grad, d.param_out,
@@ -1394,18 +1486,18 @@ int ptk_chunk_table_create(const ptk_chunk_desc* descs, int32_t n_chunks, ptk_ch
       delete t;
       return rc;
     }
-    t->host.push_back(ChunkDesc{d.master, d.exp_avg, d.exp_avg_sq, d.grad, d.param_out, d.n, tile0});
-    tile0 += tiles_of(d.n, t->tile);
+    t->host.push_back(ChunkDesc{d.master, d.exp_avg, d.exp_avg_sq, d.grad, d.param_out, d.n, 0});
   }
-  t->total_tiles = tile0;
-  if (n_chunks > 0) {
-    const size_t bytes = sizeof(ChunkDesc) * t->host.size();
-    cudaError_t e = cudaMalloc(&t->dev, bytes);
-    if (e == cudaSuccess) e = cudaMemcpy(t->dev, t->host.data(), bytes, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-      if (t->dev) cudaFree(t->dev);
-      delete t;
-      return check_cuda(e, "ptk_chunk_table_create: device table");
+  // the table lives in host memory and travels in the kernel parameters
+  t->tile = adam_tile();
+  const int n = static_cast<int>(t->host.size());
+  if (n <= kSmallCap) {
+    fill_batch(t->small, t->host.data(), n, t->tile);
+  } else {
+    for (int lo = 0; lo < n; lo += kLargeCap) {
+      t->large.emplace_back();
+      fill_batch(t->large.back(), t->host.data() + lo, n - lo < kLargeCap ? n - lo : kLargeCap,
+                 t->tile);
     }
   }
   *out = t;
@@ -1413,10 +1505,8 @@ int ptk_chunk_table_create(const ptk_chunk_desc* descs, int32_t n_chunks, ptk_ch
 }
 
 int ptk_chunk_table_destroy(ptk_chunk_table* t) {
-  if (!t) return PTK_OK;
-  const cudaError_t e = t->dev ? cudaFree(t->dev) : cudaSuccess;
   delete t;
-  return check_cuda(e, "ptk_chunk_table_destroy");
+  return PTK_OK;
 }
 
 int64_t ptk_chunk_table_params(const ptk_chunk_table* t) {
@@ -1433,13 +1523,8 @@ int ptk_chunk_adam_table(const ptk_adam_config* cfg, const ptk_chunk_table* t,
   if (cfg->step < 1) return fail(PTK_EINVAL, "ptk_chunk_adam_table: step must be >= 1");
   if (stats && !workspace) return fail(PTK_EINVAL, "ptk_chunk_adam_table: stats requires workspace");
   if (t->host.empty()) return PTK_OK;
-  if (t->device != current_device())
-    return fail(PTK_EINVAL, "ptk_chunk_adam_table: table was created on another device");
-  const ptk_adam_scalars s = derive_scalars(*cfg);
-  auto* ws = static_cast<StatsWorkspace*>(workspace);
-  cudaStream_t st = as_stream(stream);
   if (adam_variant() == AdamVariant::Ldg || t->tile != adam_tile()) {
-    // per-chunk launches (the "ldg" variant, or a table built for another tile)
+    // per-chunk launches (the "ldg" variant)
     for (const auto& d : t->host) {
       const int rc = ptk_chunk_adam(cfg, d.master, d.m, d.v, d.grad, d.param, d.n, stats, workspace,
                                     gscale_dev, skip_dev, stream);
@@ -1447,12 +1532,18 @@ int ptk_chunk_adam_table(const ptk_adam_config* cfg, const ptk_chunk_table* t,
     }
     return PTK_OK;
   }
-  ChunkList list{};
-  list.table = t->dev;
-  list.one = t->host[0];
-  list.n_chunks = static_cast<int32_t>(t->host.size());
-  list.total_tiles = t->total_tiles;
-  const int rc = launch_tma_list(s, list, ws, stats, gscale_dev, skip_dev, st);
+  const ptk_adam_scalars s = derive_scalars(*cfg);
+  auto* ws = static_cast<StatsWorkspace*>(workspace);
+  cudaStream_t st = as_stream(stream);
+  int rc = PTK_OK;
+  if (t->large.empty()) {
+    rc = launch_tma_batch(s, t->small, ws, stats, gscale_dev, skip_dev, st);
+  } else {
+    for (const auto& b : t->large) {
+      rc = launch_tma_batch(s, b, ws, stats, gscale_dev, skip_dev, st);
+      if (rc != PTK_OK) break;
+    }
+  }
   return rc != PTK_OK ? rc : check_cuda(cudaGetLastError(), "chunk_adam_tma (table) launch");
 }
 
