@@ -46,11 +46,31 @@ constexpr int kMaxGrid = 4096;
 constexpr int kMaxDevices = 64;
 
 struct StatsWorkspace {
-  double sq[kMaxGrid];
+  unsigned long long sq[3][kMaxGrid];  // per-CTA fixed-point partial sums (SumSq words)
   unsigned long long bad[kMaxGrid];
   unsigned int arrived;
-  unsigned int pad[3];
+  unsigned int exited;             // tile scheduler: CTAs done taking tiles this launch
+  unsigned long long next_tile;    // tile scheduler: next unclaimed tile of this launch
 };
+
+// Dynamic tile scheduler of the persistent TMA kernels: the producer of every
+// CTA claims the next tile of the step with one atomic, so SMs that stream
+// faster (ncu: SM active cycles min/avg/max 0.85/1.00/1.14 under a static
+// round-robin split) take more tiles and all finish together. A CTA's claims
+// are increasing, so its chunk cursor still only moves forward. The last CTA
+// to finish claiming re-arms the counter for the next launch on the stream
+// (one workspace per stream at a time, as for the statistics).
+__device__ __forceinline__ int64_t claim_tile(StatsWorkspace* ws) {
+  return static_cast<int64_t>(atomicAdd(&ws->next_tile, 1ull));
+}
+__device__ __forceinline__ void release_scheduler(StatsWorkspace* ws) {
+  __threadfence();
+  if (atomicAdd(&ws->exited, 1u) == gridDim.x - 1) {
+    ws->next_tile = 0;
+    ws->exited = 0;
+    __threadfence();
+  }
+}
 
 // ---------------------------------------------------------------- helpers --
 
@@ -116,12 +136,60 @@ __device__ __forceinline__ float adam_elem(const ptk_adam_scalars& s, float g, f
   return p;
 }
 
-// Statistics: squares are summed in fp32 over one 4- or 8-element unit, the
-// unit sums in fp64 per thread (keeps the full-step sum within ~1e-7 relative).
+// Statistics: squares are summed in fp32 over one 4- or 8-element unit; the
+// unit sums are accumulated EXACTLY in a 192-bit fixed-point integer (units of
+// 2^-64, range 2^128) per thread, then per warp, CTA and grid. Integer sums do
+// not depend on the order of the terms, so the statistics (and the clip
+// coefficient derived from them) are bit-identical from run to run whichever
+// CTA processed which tile -- the dynamic tile scheduler's order varies. Unit
+// sums below 2^-64 (|g| < 2^-33) are dropped and sums above 2^90 saturate at
+// 2^90 (a norm >= 3.5e13; 2^32 such units still fit in the range).
 __device__ __forceinline__ void accum_stats(float g, float& sq, unsigned& bad) {
   sq = __fmaf_rn(g, g, sq);
   bad += isfinite(g) ? 0u : 1u;
 }
+
+struct SumSq {
+  unsigned long long w0 = 0, w1 = 0, w2 = 0;  // value = (w2:w1:w0) * 2^-64
+
+  __device__ __forceinline__ void add(unsigned long long a0, unsigned long long a1,
+                                      unsigned long long a2) {
+    asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u64 %2, %2, %5;"
+        : "+l"(w0), "+l"(w1), "+l"(w2)
+        : "l"(a0), "l"(a1), "l"(a2));
+  }
+  __device__ __forceinline__ void add(const SumSq& o) { add(o.w0, o.w1, o.w2); }
+  // x >= 0 (a sum of squares); NaN / inf are counted by `bad` and skipped here
+  __device__ __forceinline__ void add(float x) {
+    const uint32_t b = __float_as_uint(x);
+    int ef = static_cast<int>((b >> 23) & 0xffu);
+    if (ef == 0 || ef == 255 || (b >> 31)) return;
+    unsigned long long m = (b & 0x7fffffu) | 0x800000u;
+    if (ef > 127 + 90) {  // saturate at 2^90
+      ef = 127 + 90;
+      m = 0x800000u;
+    }
+    int sh = ef - 150 + 64;  // x = m * 2^(ef-150); units of 2^-64
+    if (sh < 0) {
+      if (sh <= -24) return;
+      m >>= -sh;
+      sh = 0;
+    }
+    const int word = sh >> 6, bit = sh & 63;
+    const unsigned long long lo = m << bit;
+    const unsigned long long hi = bit ? m >> (64 - bit) : 0ull;
+    if (word == 0) add(lo, hi, 0ull);
+    else add(0ull, lo, hi);  // sh < 128 + 24: word <= 1 after saturation
+  }
+  __device__ __forceinline__ void shfl_add(int o) {
+    add(__shfl_xor_sync(0xffffffffu, w0, o), __shfl_xor_sync(0xffffffffu, w1, o),
+        __shfl_xor_sync(0xffffffffu, w2, o));
+  }
+  __device__ __forceinline__ double to_double() const {
+    return static_cast<double>(w2) * 0x1p64 + static_cast<double>(w1) +
+           static_cast<double>(w0) * 0x1p-64;
+  }
+};
 
 // Effective gradient scale of a launch: the host scalar times the optional
 // device multiplier (a clip coefficient); skip_dev != 0 makes it a no-op.
@@ -129,34 +197,38 @@ __device__ __forceinline__ float launch_gscale(const ptk_adam_scalars& s, const 
   return gscale_dev != nullptr ? __fmul_rn(s.gscale, *gscale_dev) : s.gscale;
 }
 
-// Deterministic grid reduction: warp shuffle -> CTA (fixed order) -> the last
-// CTA to arrive sums the per-CTA partials in a fixed lane-strided order + xor
-// tree and ADDS the result to *stats. Safe across back-to-back launches on
-// one stream (the arrival counter is re-armed by the last CTA).
-__device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorkspace* ws,
+// Grid reduction of the statistics: warp shuffle -> CTA -> the last CTA to
+// arrive sums the per-CTA partials, converts the exact sum to fp64 once and
+// ADDS it to *stats (launch order across launches: deterministic). Safe
+// across back-to-back launches on one stream (the arrival counter is re-armed
+// by the last CTA).
+__device__ __forceinline__ void reduce_stats(SumSq sq, unsigned bad, StatsWorkspace* ws,
                                              ptk_grad_stats_t* stats) {
-  __shared__ double s_sq[32];
+  __shared__ SumSq s_sq[32];
   __shared__ unsigned long long s_bad[32];
   __shared__ bool s_last;
+  unsigned long long wbad = bad;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    sq.shfl_add(o);
+    wbad += __shfl_xor_sync(0xffffffffu, wbad, o);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
     s_sq[warp] = sq;
-    s_bad[warp] = bad;
+    s_bad[warp] = wbad;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double bsq = 0.0;
+    SumSq bsq;
     unsigned long long bbad = 0;
     for (unsigned w = 0; w < blockDim.x / 32; ++w) {
-      bsq += s_sq[w];
+      bsq.add(s_sq[w]);
       bbad += s_bad[w];
     }
-    ws->sq[blockIdx.x] = bsq;
+    ws->sq[0][blockIdx.x] = bsq.w0;
+    ws->sq[1][blockIdx.x] = bsq.w1;
+    ws->sq[2][blockIdx.x] = bsq.w2;
     ws->bad[blockIdx.x] = bbad;
     __threadfence();
     const unsigned prev = atomicAdd(&ws->arrived, 1u);
@@ -166,21 +238,23 @@ __device__ __forceinline__ void reduce_stats(double sq, unsigned bad, StatsWorks
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x < 32) {
-    double tsq = 0.0;
+    SumSq tsq;
     unsigned long long tbad = 0;
-    const volatile double* vsq = ws->sq;
+    const volatile unsigned long long* v0 = ws->sq[0];
+    const volatile unsigned long long* v1 = ws->sq[1];
+    const volatile unsigned long long* v2 = ws->sq[2];
     const volatile unsigned long long* vbad = ws->bad;
     for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-      tsq += vsq[b];
+      tsq.add(v0[b], v1[b], v2[b]);
       tbad += vbad[b];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      tsq += __shfl_xor_sync(0xffffffffu, tsq, o);
+      tsq.shfl_add(o);
       tbad += __shfl_xor_sync(0xffffffffu, tbad, o);
     }
     if (threadIdx.x == 0) {
-      stats->sumsq += tsq;
+      stats->sumsq += tbad != 0 ? __longlong_as_double(0x7ff0000000000000ll) : tsq.to_double();
       stats->nonfinite += tbad;
       ws->arrived = 0;
     }
@@ -200,7 +274,7 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
                   ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
   if (skip_dev != nullptr && *skip_dev != 0) return;  // grid-uniform
   const float gs = launch_gscale(s, gscale_dev);
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
 
   const int64_t nvec = n >> 3;
@@ -227,7 +301,7 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
         if (kStats) accum_stats(gk, usq, bad);
         adam_elem(s, gk, p[u][k], m[u][k], v[u][k]);
       }
-      if (kStats) sq += usq;
+      if (kStats) sq.add(usq);
       st8f(master + e, p[u]);
       st8f(exp_avg + e, m[u]);
       st8f(exp_avg_sq + e, v[u]);
@@ -248,7 +322,7 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
       if (kStats) accum_stats(gk, usq, bad);
       adam_elem(s, gk, p[k], m[k], v[k]);
     }
-    if (kStats) sq += usq;
+    if (kStats) sq.add(usq);
     st8f(master + e, p);
     st8f(exp_avg + e, m);
     st8f(exp_avg_sq + e, v);
@@ -260,7 +334,7 @@ chunk_adam_kernel(ptk_adam_scalars s, float* __restrict__ master, float* __restr
     const float gk = __fmul_rn(G::load1(grad + e), gs);
     float usq = 0.0f;
     if (kStats) accum_stats(gk, usq, bad);
-    sq += usq;
+    sq.add(usq);
     float p = master[e], m = exp_avg[e], v = exp_avg_sq[e];
     adam_elem(s, gk, p, m, v);
     master[e] = p;
@@ -286,6 +360,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -434,23 +512,42 @@ struct ItemMeta {
   int32_t len;
 };
 
+// Warp-specialized rings: stage / phase position of a role.
+
+struct RingPos {
+  int st = 0;
+  uint32_t ph = 0;
+  template <int kStages>
+  __device__ __forceinline__ void next() {
+    if (++st == kStages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+constexpr int kRoleThreads = 64;  // producer warp + storer warp
+
 // ------------------------------------------- K1 + K2, TMA bulk pipeline --
 //
-// Persistent CTAs (one per SM) walk the step's tiles. One elected thread moves
-// every tile with 1-D bulk copies (cp.async.bulk, the TMA engine): master/m/v/
-// grad global -> shared, completion counted on an mbarrier (complete_tx), and
-// after the update master/m/v/param shared -> global as a bulk_group. kStages
-// tiles of shared memory form a ring; the producer runs kStages-2 tiles ahead
-// of the consumers, and a stage is refilled only after the bulk store that
-// last read it has finished reading shared memory (wait_group.read 1).
+// Persistent CTAs (one per SM) stream the step's tiles through a ring of
+// kStages shared-memory stages, with the roles split by warp:
+//   * producer warp (one elected lane): claims the next tile (dynamic
+//     scheduler) and moves master/m/v/grad global -> shared with 1-D bulk
+//     copies (cp.async.bulk, the TMA engine), completion counted on the
+//     stage's `full` mbarrier (complete_tx);
+//   * consumer warps (kThr threads, one 4-element unit each per tile): Adam
+//     + statistics in shared memory, then arrive on the stage's `done`;
+//   * storer warp (one elected lane): bulk-stores master/m/v/param shared ->
+//     global as a bulk_group and frees the stage (`empty`) once the store has
+//     read it (wait_group.read).
+// No CTA-wide barrier sits on the per-tile path, so the producer's claim /
+// descriptor latency and the stores overlap the math of other stages.
 //
 // The chunk table travels in the KERNEL PARAMETERS (__grid_constant__, the
-// constant bank): every thread walks it with warp-uniform indices, so the
-// descriptor fields load into uniform registers (LDCU) and the elected
-// thread's bulk-copy addresses need no per-thread -> uniform conversion. Its
-// per-tile scalar work then stays as small as with a single chunk (every
-// warp waits for it at the CTA barrier). Tables larger than kCap chunks are
-// launched in batches of kCap.
+// constant bank): the descriptor fields load into uniform registers and the
+// elected lanes' bulk-copy addresses need no per-thread -> uniform
+// conversion. Tables larger than kCap chunks are launched in batches of kCap.
 
 template <int kTile>
 struct TmaStage {
@@ -484,122 +581,157 @@ struct BatchCursor {
   }
 };
 
-template <int kTile, int kStages, int kThr, bool kStats, bool kHint, int kCap>
-__global__ void __launch_bounds__(kThr, 1)
+template <int kTile, int kStages, int kThr, bool kStats, bool kHint, int kCap, bool kDynamic>
+__global__ void __launch_bounds__(kThr + kRoleThreads, 1)
 chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkBatch<kCap> b,
                       StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
                       const int32_t* skip_dev) {
-  static_assert(kTile % (kThr * 4) == 0, "tile must be a multiple of 4 elements per thread");
-  static_assert(kStages >= 3, "ring needs >= 3 stages");
+  static_assert(kTile == kThr * 4, "one 4-element unit per consumer thread per tile");
+  static_assert(kStages >= 2, "ring needs >= 2 stages");
+  constexpr int kConsumerWarps = kThr / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   auto* stage = reinterpret_cast<TmaStage<kTile>*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t done[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  __shared__ ItemMeta meta[kStages];
 
   if (skip_dev != nullptr && *skip_dev != 0) return;
   const float gs = launch_gscale(s, gscale_dev);
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int64_t T = b.total_tiles;
   const int64_t my_items = T > blockIdx.x ? (T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&done[i], kConsumerWarps);
+      mbar_init(&empty[i], 1);
+    }
     fence_mbar_init();  // the inits are visible to the async proxy (complete_tx)
   }
   __syncthreads();
 
-  const uint64_t policy = kHint ? evict_first_policy() : 0;
-  auto load = [&](void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    if (kHint) bulk_load_hint(dst, src, bytes, bar, policy);
-    else bulk_load(dst, src, bytes, bar);
-  };
-  auto store = [&](void* dst, const void* src, uint32_t bytes) {
-    if (kHint) bulk_store_hint(dst, src, bytes, policy);
-    else bulk_store(dst, src, bytes);
-  };
-  // item k of this CTA -> (chunk, first element, length); len is a multiple
-  // of 8 (the chunk's multiple-of-8 prefix is tiled)
-  auto item = [&](BatchCursor<kCap>& cur, int64_t k, int& c, int64_t& e, int& len) {
-    const int64_t t = blockIdx.x + k * gridDim.x;
-    c = cur.seek(b, t);
-    e = (t - b.d[c].tile0) * kTile;
-    const int64_t left = (b.d[c].n & ~int64_t{7}) - e;
-    len = left < kTile ? static_cast<int>(left) : kTile;
-  };
-  BatchCursor<kCap> lcur(b), ccur(b);  // load-ahead cursor (tid 0) / current item
-  int load_st = 0;
-  auto issue_load = [&](int64_t k) {  // k-th item of this CTA, into stage load_st
-    const int st = load_st;
-    load_st = load_st + 1 == kStages ? 0 : load_st + 1;
-    int c, len;
-    int64_t e;
-    item(lcur, k, c, e, len);
-    TmaStage<kTile>& S = stage[st];
-    mbar_expect_tx(&full[st], static_cast<uint32_t>(len) * (3 * sizeof(float) + sizeof(uint16_t)));
-    load(S.master, b.d[c].master + e, len * 4, &full[st]);
-    load(S.m, b.d[c].m + e, len * 4, &full[st]);
-    load(S.v, b.d[c].v + e, len * 4, &full[st]);
-    load(S.grad, b.d[c].grad + e, len * 2, &full[st]);
-  };
-
-  constexpr int kAhead = kStages - 2;
-  if (tid == 0)
-    for (int64_t k = 0; k < kAhead && k < my_items; ++k) issue_load(k);
-
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
-  int st = 0;
-  uint32_t phase = 0;
-  for (int64_t k = 0; k < my_items; ++k) {
-    if (tid == 0 && k + kAhead < my_items) {
-      bulk_wait_read<1>();  // the store of item k-2 (same stage) has read its smem
-      issue_load(k + kAhead);
-    }
-    int c, len;
-    int64_t ge;
-    item(ccur, k, c, ge, len);
-    mbar_wait(&full[st], phase);
-    TmaStage<kTile>& S = stage[st];
-    float usq = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kTile / (kThr * 4); ++j) {
-      const int e = (j * kThr + tid) * 4;
-      if (e >= len) break;  // only in a chunk's last tile
-      float4 p = *reinterpret_cast<float4*>(&S.master[e]);
-      float4 m = *reinterpret_cast<float4*>(&S.m[e]);
-      float4 v = *reinterpret_cast<float4*>(&S.v[e]);
-      const uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[e]);
-      float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
-      float* pp = &p.x;
-      float* mm = &m.x;
-      float* vv = &v.x;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float gk = __fmul_rn(g[q], gs);
-        if (kStats) accum_stats(gk, usq, bad);
-        adam_elem(s, gk, pp[q], mm[q], vv[q]);
+  if (warp == kConsumerWarps) {
+    // ------------------------- producer: master/m/v/grad tiles -> stage --
+    if (lane == 0) {
+      const uint64_t policy = kHint ? evict_first_policy() : 0;
+      BatchCursor<kCap> cur(b);
+      RingPos pos;
+      int64_t claimed = kDynamic ? claim_tile(ws) : 0;  // one claim in flight ahead
+      for (int64_t k = 0; kDynamic || k < my_items; ++k) {
+        if (k >= kStages) mbar_wait(&empty[pos.st], pos.ph ^ 1u);
+        int64_t t = blockIdx.x + k * gridDim.x;
+        if (kDynamic) {
+          t = claimed;
+          if (t >= T) {  // end of the step: a tile-less stage tells the others
+            meta[pos.st] = ItemMeta{0, -1, 0};
+            mbar_arrive(&full[pos.st]);
+            release_scheduler(ws);
+            break;
+          }
+          claimed = claim_tile(ws);
+        }
+        const int c = cur.seek(b, t);
+        const ChunkDesc& d = b.d[c];
+        const int64_t e = (t - d.tile0) * kTile;
+        const int64_t left = (d.n & ~int64_t{7}) - e;
+        const int len = left < kTile ? static_cast<int>(left) : kTile;
+        meta[pos.st] = ItemMeta{e, c, len};
+        TmaStage<kTile>& S = stage[pos.st];
+        uint64_t* bar = &full[pos.st];
+        mbar_expect_tx(bar, static_cast<uint32_t>(len) * (3 * sizeof(float) + sizeof(uint16_t)));
+        if (kHint) {
+          bulk_load_hint(S.master, d.master + e, len * 4, bar, policy);
+          bulk_load_hint(S.m, d.m + e, len * 4, bar, policy);
+          bulk_load_hint(S.v, d.v + e, len * 4, bar, policy);
+          bulk_load_hint(S.grad, d.grad + e, len * 2, bar, policy);
+        } else {
+          bulk_load(S.master, d.master + e, len * 4, bar);
+          bulk_load(S.m, d.m + e, len * 4, bar);
+          bulk_load(S.v, d.v + e, len * 4, bar);
+          bulk_load(S.grad, d.grad + e, len * 2, bar);
+        }
+        pos.next<kStages>();
       }
-      *reinterpret_cast<float4*>(&S.master[e]) = p;
-      *reinterpret_cast<float4*>(&S.m[e]) = m;
-      *reinterpret_cast<float4*>(&S.v[e]) = v;
-      *reinterpret_cast<uint2*>(&S.param[e]) =
-          make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
     }
-    if (kStats) sq += usq;
-    fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
-    __syncthreads();
-    if (tid == 0) {
-      store(b.d[c].master + ge, S.master, len * 4);
-      store(b.d[c].m + ge, S.m, len * 4);
-      store(b.d[c].v + ge, S.v, len * 4);
-      if (b.d[c].param != nullptr) store(b.d[c].param + ge, S.param, len * 2);
-      bulk_commit();
+  } else if (warp == kConsumerWarps + 1) {
+    // ---------------------------- storer: stage -> master/m/v/param -----
+    if (lane == 0) {
+      const uint64_t policy = kHint ? evict_first_policy() : 0;
+      RingPos pos;
+      int prev = -1;
+      for (int64_t k = 0; kDynamic || k < my_items; ++k) {
+        mbar_wait(&done[pos.st], pos.ph);
+        const ItemMeta it = meta[pos.st];
+        if (kDynamic && it.c < 0) break;
+        const ChunkDesc& d = b.d[it.c];
+        TmaStage<kTile>& S = stage[pos.st];
+        if (kHint) {
+          bulk_store_hint(d.master + it.e, S.master, it.len * 4, policy);
+          bulk_store_hint(d.m + it.e, S.m, it.len * 4, policy);
+          bulk_store_hint(d.v + it.e, S.v, it.len * 4, policy);
+          if (d.param != nullptr) bulk_store_hint(d.param + it.e, S.param, it.len * 2, policy);
+        } else {
+          bulk_store(d.master + it.e, S.master, it.len * 4);
+          bulk_store(d.m + it.e, S.m, it.len * 4);
+          bulk_store(d.v + it.e, S.v, it.len * 4);
+          if (d.param != nullptr) bulk_store(d.param + it.e, S.param, it.len * 2);
+        }
+        bulk_commit();
+        if (prev >= 0) {
+          bulk_wait_read<1>();  // the previous stage's store has read its smem
+          mbar_arrive(&empty[prev]);
+        }
+        prev = pos.st;
+        pos.next<kStages>();
+      }
+      bulk_wait_all();
     }
-    if (++st == kStages) {
-      st = 0;
-      phase ^= 1u;
+  } else {
+    // ------------------------------------------------------ consumers --
+    RingPos pos;
+    for (int64_t k = 0; kDynamic || k < my_items; ++k) {
+      mbar_wait(&full[pos.st], pos.ph);
+      if (kDynamic && meta[pos.st].c < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[pos.st]);  // lets the storer see the end
+        break;
+      }
+      const int len = meta[pos.st].len;
+      TmaStage<kTile>& S = stage[pos.st];
+      const int e = tid * 4;
+      if (e < len) {  // always, except in a chunk's last tile
+        float4 p = *reinterpret_cast<float4*>(&S.master[e]);
+        float4 m = *reinterpret_cast<float4*>(&S.m[e]);
+        float4 v = *reinterpret_cast<float4*>(&S.v[e]);
+        const uint2 g2 = *reinterpret_cast<const uint2*>(&S.grad[e]);
+        const float g[4] = {bf_lo(g2.x), bf_hi(g2.x), bf_lo(g2.y), bf_hi(g2.y)};
+        float* pp = &p.x;
+        float* mm = &m.x;
+        float* vv = &v.x;
+        float usq = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float gk = __fmul_rn(g[q], gs);
+          if (kStats) accum_stats(gk, usq, bad);
+          adam_elem(s, gk, pp[q], mm[q], vv[q]);
+        }
+        if (kStats) sq.add(usq);
+        *reinterpret_cast<float4*>(&S.master[e]) = p;
+        *reinterpret_cast<float4*>(&S.m[e]) = m;
+        *reinterpret_cast<float4*>(&S.v[e]) = v;
+        *reinterpret_cast<uint2*>(&S.param[e]) =
+            make_uint2(pack_bf16x2(p.x, p.y), pack_bf16x2(p.z, p.w));
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[pos.st]);
+      pos.next<kStages>();
     }
   }
-  if (tid == 0) bulk_wait_all();
   // the < 8 trailing elements of chunks whose length is not a multiple of 8
   for (int c = blockIdx.x; c < b.n_chunks; c += gridDim.x) {
     const ChunkDesc& d = b.d[c];
@@ -614,30 +746,12 @@ chunk_adam_tma_kernel(ptk_adam_scalars s, const __grid_constant__ ChunkBatch<kCa
       d.m[e] = mm;
       d.v[e] = vv;
       if (d.param != nullptr) d.param[e] = static_cast<uint16_t>(pack_bf16x2(p, 0.0f) & 0xffffu);
-      if (kStats) sq += usq;
+      if (kStats) sq.add(usq);
     }
   }
+  __syncthreads();
   if (kStats) reduce_stats(sq, bad, ws, stats);
 }
-
-// Warp-specialized ring pieces used by the fused kernel below.
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-struct RingPos {
-  int st = 0;
-  uint32_t ph = 0;
-  template <int kStages>
-  __device__ __forceinline__ void next() {
-    if (++st == kStages) {
-      st = 0;
-      ph ^= 1u;
-    }
-  }
-};
-
-constexpr int kRoleThreads = 64;  // producer warp + storer warp
 
 // -------------------------------------------------------------- K2 -------
 
@@ -645,7 +759,7 @@ template <bool kWrite>
 __global__ void __launch_bounds__(kThreads)
 grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
                   float* __restrict__ out, StatsWorkspace* ws, ptk_grad_stats_t* stats) {
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
   const int64_t nvec = n >> 3;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
@@ -659,7 +773,7 @@ grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
       g[k] = __fmul_rn(g[k], scale);
       accum_stats(g[k], usq, bad);
     }
-    sq += usq;
+    sq.add(usq);
     if (kWrite) st8f(out + (i << 3), g);
   }
   const int64_t t0 = nvec << 3;
@@ -668,7 +782,7 @@ grad_stats_kernel(const uint16_t* __restrict__ grad, int64_t n, float scale,
     const float gk = __fmul_rn(GradBf16::load1(grad + e), scale);
     float usq = 0.0f;
     accum_stats(gk, usq, bad);
-    sq += usq;
+    sq.add(usq);
     if (kWrite) out[e] = gk;
   }
   reduce_stats(sq, bad, ws, stats);
@@ -707,7 +821,7 @@ fused_peer_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, St
                   ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev) {
   if (skip_dev != nullptr && *skip_dev != 0) return;
   const float gs = launch_gscale(s, gscale_dev);
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   for (int c = 0; c < list.n_chunks; ++c) {
@@ -739,7 +853,7 @@ fused_peer_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, St
         accum_stats(gk, usq, bad);
         adam_elem(s, gk, p[k], m[k], v[k]);
       }
-      sq += usq;
+      sq.add(usq);
       st8f(d.master + e, p);
       st8f(d.m + e, m);
       st8f(d.v + e, v);
@@ -761,7 +875,7 @@ __global__ void __launch_bounds__(kThreads)
 fused_stats_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, StatsWorkspace* ws,
                    ptk_grad_stats_t* stats) {
   constexpr int U = W <= 2 ? 4 : W <= 4 ? 2 : 1;  // >= 4 x 16 B loads in flight per thread
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   for (int c = 0; c < list.n_chunks; ++c) {
@@ -794,7 +908,7 @@ fused_stats_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list, S
         float usq = 0.0f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) accum_stats(__fmul_rn(g[k], s.gscale), usq, bad);
-        sq += usq;
+        sq.add(usq);
       }
     }
   }
@@ -832,7 +946,7 @@ constexpr int fused_stages() {
   return s > 9 ? 9 : s;
 }
 
-template <int W, int kStages>
+template <int W, int kStages, bool kDynamic>
 __global__ void __launch_bounds__(fused_threads<W>() + kRoleThreads, 1)
 fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list,
                       StatsWorkspace* ws, ptk_grad_stats_t* stats, const float* gscale_dev,
@@ -863,16 +977,27 @@ fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list
   }
   __syncthreads();
 
-  double sq = 0.0;
+  SumSq sq;
   unsigned bad = 0;
   if (warp == kConsumerWarps) {
     // ---------------- producer: local state + every rank's gradient tile --
     if (lane == 0) {
       TileCursor<FusedDesc> cur;
       RingPos pos;
-      for (int64_t k = 0; k < my_items; ++k) {
+      int64_t claimed = kDynamic ? claim_tile(ws) : 0;  // one claim in flight ahead
+      for (int64_t k = 0; kDynamic || k < my_items; ++k) {
         if (k >= kStages) mbar_wait(&empty[pos.st], pos.ph ^ 1u);
-        const int64_t t = blockIdx.x + k * gridDim.x;
+        int64_t t = blockIdx.x + k * gridDim.x;
+        if (kDynamic) {
+          t = claimed;
+          if (t >= T) {  // end of the step: a tile-less stage tells the others
+            meta[pos.st] = ItemMeta{0, -1, 0};
+            mbar_arrive(&full[pos.st]);
+            release_scheduler(ws);
+            break;
+          }
+          claimed = claim_tile(ws);
+        }
         cursor_seek(list, cur, t);
         const FusedDesc& d = cur.d;
         const int64_t e = (t - d.tile0) * kFusedTile;
@@ -897,9 +1022,10 @@ fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list
       TileCursor<FusedDesc> scur;
       RingPos pos;
       int prev = -1;
-      for (int64_t k = 0; k < my_items; ++k) {
+      for (int64_t k = 0; kDynamic || k < my_items; ++k) {
         mbar_wait(&done[pos.st], pos.ph);
         const ItemMeta it = meta[pos.st];
+        if (kDynamic && it.c < 0) break;
         const FusedDesc& d = cursor_at(list, scur, it.c);
         const int64_t off = static_cast<int64_t>(list.rank) * d.shard + it.e;
         FusedStage<W>& S = stage[pos.st];
@@ -921,8 +1047,13 @@ fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list
   } else {
     // ------------------------------------------------------ consumers --
     RingPos pos;
-    for (int64_t k = 0; k < my_items; ++k) {
+    for (int64_t k = 0; kDynamic || k < my_items; ++k) {
       mbar_wait(&full[pos.st], pos.ph);
+      if (kDynamic && meta[pos.st].c < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[pos.st]);  // lets the storer see the end
+        break;
+      }
       const int len = meta[pos.st].len;
       FusedStage<W>& S = stage[pos.st];
       const int e = tid * 4;
@@ -950,7 +1081,7 @@ fused_peer_tma_kernel(ptk_adam_scalars s, const __grid_constant__ FusedList list
           accum_stats(gk, usq, bad);
           adam_elem(s, gk, pp[q], mm[q], vv[q]);
         }
-        sq += usq;
+        sq.add(usq);
         *reinterpret_cast<float4*>(&S.master[e]) = p;
         *reinterpret_cast<float4*>(&S.m[e]) = m;
         *reinterpret_cast<float4*>(&S.v[e]) = v;
@@ -1137,6 +1268,15 @@ int grid_for(K kernel, int64_t work_items) {
   return static_cast<int>(g);
 }
 
+// PTK_TILE_SCHEDULE=static forces the round-robin tile split (A/B runs).
+bool static_schedule() {
+  static const bool v = [] {
+    const char* e = std::getenv("PTK_TILE_SCHEDULE");
+    return e != nullptr && std::string(e) == "static";
+  }();
+  return v;
+}
+
 constexpr int kUnroll = 2;
 
 // TMA ring shapes of the chunk Adam: (name, tile elements, ring stages, CTAs
@@ -1147,10 +1287,8 @@ constexpr int kUnroll = 2;
 #define PTK_TMA_VARIANTS(X)                     \
   X(Tma1536x9t384, 1536, 9, 1, 384, false)      \
   X(Tma2048x6t512, 2048, 6, 1, 512, false)      \
-  X(Tma2048x6t256, 2048, 6, 1, 256, false)      \
   X(Tma2048x6t512h, 2048, 6, 1, 512, true)      \
   X(Tma2560x5t640, 2560, 5, 1, 640, false)      \
-  X(Tma3072x4t384, 3072, 4, 1, 384, false)      \
   X(Tma3072x4t768, 3072, 4, 1, 768, false)      \
   X(Tma1024x13t256, 1024, 13, 1, 256, false)    \
   X(Tma1792x7t448, 1792, 7, 1, 448, false)      \
@@ -1212,15 +1350,18 @@ template <int kTile, int kStages, int kPerSm, int kThr, bool kStats, bool kHint,
 int launch_tma(const ptk_adam_scalars& s, const ChunkBatch<kCap>& b, StatsWorkspace* ws,
                ptk_grad_stats_t* stats, const float* gscale_dev, const int32_t* skip_dev,
                cudaStream_t st) {
-  auto k = chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint, kCap>;
+  const bool dynamic = ws != nullptr && !static_schedule();
+  auto k = dynamic ? chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint, kCap, true>
+                   : chunk_adam_tma_kernel<kTile, kStages, kThr, kStats, kHint, kCap, false>;
   constexpr int kSmem = kStages * static_cast<int>(sizeof(TmaStage<kTile>));
-  static std::atomic<bool> configured[kMaxDevices];
-  const int rc = ensure_smem(k, kSmem, configured, "chunk_adam_tma_kernel smem attribute");
+  static std::atomic<bool> configured[2][kMaxDevices];
+  const int rc = ensure_smem(k, kSmem, configured[dynamic], "chunk_adam_tma_kernel smem attribute");
   if (rc != PTK_OK) return rc;
   int64_t grid = static_cast<int64_t>(sm_count()) * kPerSm;
   if (grid > b.total_tiles) grid = b.total_tiles;
   if (grid < 1) grid = 1;  // tails only
-  k<<<static_cast<int>(grid), kThr, kSmem, st>>>(s, b, ws, stats, gscale_dev, skip_dev);
+  k<<<static_cast<int>(grid), kThr + kRoleThreads, kSmem, st>>>(s, b, ws, stats, gscale_dev,
+                                                                skip_dev);
   launch_counter()++;
   return PTK_OK;
 }
@@ -1366,13 +1507,15 @@ int launch_fused(FusedOp op, const ptk_adam_scalars& s, const FusedList& list, i
   }
   constexpr int kSt = fused_stages<W>();
   constexpr int kSmem = kSt * static_cast<int>(sizeof(FusedStage<W>));
-  auto k = fused_peer_tma_kernel<W, kSt>;
-  static std::atomic<bool> configured[kMaxDevices];
-  const int rc = ensure_smem(k, kSmem, configured, "fused_peer_tma_kernel smem attribute");
-  if (rc != PTK_OK) return rc;
   int64_t grid = sm_count();
   if (grid > list.total_tiles) grid = list.total_tiles;
   if (grid < 1) grid = 1;
+  // the dynamic tile scheduler keeps its counter in the workspace
+  const bool dynamic = ws != nullptr && !static_schedule();
+  auto k = dynamic ? fused_peer_tma_kernel<W, kSt, true> : fused_peer_tma_kernel<W, kSt, false>;
+  static std::atomic<bool> configured[2][kMaxDevices];
+  const int rc = ensure_smem(k, kSmem, configured[dynamic], "fused_peer_tma_kernel smem attribute");
+  if (rc != PTK_OK) return rc;
   k<<<static_cast<int>(grid), fused_threads<W>() + kRoleThreads, kSmem, st>>>(s, list, ws, stats, gscale_dev,
                                                                 skip_dev);
   return PTK_OK;

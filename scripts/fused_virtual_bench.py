@@ -33,6 +33,8 @@ sys.path.insert(0, REPO)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--chunk-mib", type=int, default=512)
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="chunks per step (one table launch per virtual rank walks all of them)")
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
@@ -45,7 +47,7 @@ def main():
     p = args.chunk_mib * (1 << 20) // 2
     rows = []
     for w in map(int, args.worlds.split(",")):
-        sets = [ChunkSet([p], world=w, rank=r, device=dev, mode="fused") for r in range(w)]
+        sets = [ChunkSet([p] * args.chunks, world=w, rank=r, device=dev, mode="fused") for r in range(w)]
         for cs in sets:
             cs.init_synthetic()
             cs.fill_grads(0)
@@ -69,10 +71,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
-        alg = p * (24 + 4 * w)
+        alg = p * args.chunks * (24 + 4 * w)
         gbs = alg / (ms * 1e-3) / 1e9
         row = {"kernel": nat.raw.ptk_fused_kernel_name().decode() + f" W={w}",
-               "virtual_ranks": w, "chunk_params": p,
+               "virtual_ranks": w, "chunk_params": p, "chunks": args.chunks,
                "ms_per_step": round(ms, 4), "algorithmic_bytes_per_step": alg,
                "achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 4),
                "launches_per_step": launches // args.steps,
@@ -82,7 +84,7 @@ def main():
         del g, sets
         torch.cuda.empty_cache()
     os.makedirs(os.path.join(REPO, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(REPO, "gpurun_out", "fused_virtual.jsonl"), "w") as f:
+    with open(os.path.join(REPO, "gpurun_out", "fused_virtual.jsonl"), "a") as f:
         for r in rows:
             f.write(json.dumps(r) + "\n")
 
