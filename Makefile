@@ -22,11 +22,11 @@ PTK_CU   := $(PKG)/csrc/ptk_kernels.cu
 PTK_CPP  := $(PKG)/csrc/ptk_host.cpp $(PKG)/csrc/ptk_comm.cpp $(PKG)/csrc/ptk_cpu_adam.cpp
 PTK_OBJS := $(OBJ)/ptk_kernels.o $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(PTK_CPP))
 
-PLAN_SRC  := model serialize packing costmodel search simulator cli accounting
+PLAN_SRC  := model serialize packing costmodel search simulator policy cli accounting
 PLAN_OBJS := $(addprefix $(OBJ)/planner_,$(addsuffix .o,$(PLAN_SRC)))
 PLANFLAGS := -std=c++20 -O2 -fPIC -pthread -ffp-contract=off -Wall -Wextra -Iinclude -I$(JSON_DIR)
 
-.PHONY: all ptk planner oracle reftests clean
+.PHONY: all ptk planner oracle reftests clean bench-variants
 all: ptk planner oracle
 
 ptk: $(PKG)/libptk.so
@@ -40,7 +40,7 @@ $(OBJ)/%.o: $(PKG)/csrc/%.cpp $(PKG)/csrc/ptk_common.h include/ptk.h
 	$(CXX) $(HOSTFLAGS) -c $< -o $@
 
 # libptk.so = data-plane kernels + C-ABI + the planner + the chunk runtime
-RT_SRC  := executor profile
+RT_SRC  := executor profile policy_abi
 RT_OBJS := $(addprefix $(OBJ)/rt_,$(addsuffix .o,$(RT_SRC)))
 
 $(OBJ)/rt_%.o: $(PKG)/csrc/runtime/%.cpp include/ptk.h include/memplan/execute.hpp $(PKG)/csrc/ptk_common.h
@@ -85,6 +85,14 @@ build/reftests/acceptance: $(REF_TESTS_DIR)/acceptance.cpp build/libmemplan.a
 
 oracle:
 	$(MAKE) -C oracle all
+
+# Shape-sweep build of the data plane (every PTK_TMA_VARIANTS shape compiled
+# in, selected by PTK_ADAM_VARIANT): build/ab/libptk_bench.so, not the product.
+bench-variants: build/ab/libptk_bench.so
+build/ab/libptk_bench.so: $(PTK_CU) $(PTK_OBJS) $(PLAN_OBJS) $(RT_OBJS)
+	@mkdir -p build/ab
+	$(NVCC) $(NVFLAGS) -DPTK_BENCH_VARIANTS -c $(PTK_CU) -o build/ab/ptk_kernels_bench.o 2> build/ab/ptxas.log || (cat build/ab/ptxas.log; false)
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ build/ab/ptk_kernels_bench.o $(filter-out $(OBJ)/ptk_kernels.o,$(PTK_OBJS)) $(PLAN_OBJS) $(RT_OBJS) -lnccl -Xcompiler -fopenmp -lgomp -Xcompiler -pthread
 
 clean:
 	rm -rf build $(PKG)/libptk.so

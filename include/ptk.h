@@ -334,6 +334,42 @@ int ptk_profile_cpu_adam_rate(int64_t n, double* params_per_s);
  * (28 * params updated + bytes copied) / elapsed. Host-synchronising. */
 int ptk_profile_host_memory_bw(int64_t n, int32_t threads, double seconds, double* bytes_per_s);
 
+/* ---- the chunk buffer pool: the runtime's ONE residency policy --------- */
+/* memplan::ChunkBufferPool (include/memplan/policy.hpp) -- the same decisions
+ * the simulator (memplan::simulate, proj/src/sim.cpp:275-343,427-451) and the
+ * device executor (ptk_execute_plan) make -- for a host runtime that moves the
+ * chunk bytes itself (the training loop's chunk pool, offload.py). Chunk ids
+ * are 1-based, chunks 1..n_persist are persistent (never pooled); positions:
+ * forward of chunk c = c, backward = 2N - c + 1. Not thread-safe.
+ *   ptk_pool_grant     a slot for chunk c (away) at position `now`: the
+ *                      lowest free slot, else the slot of the idle resident
+ *                      chunk whose next use is farthest, pinned chunks
+ *                      excluded -- for a prefetch (demand = 0) only a chunk
+ *                      needed strictly later than c; demand != 0 (c is needed
+ *                      now) takes any candidate. *slot = -1 when no slot can
+ *                      be granted now; *evicted = the chunk that gave its slot
+ *                      up (0 = a free slot). c is then arriving.
+ *   ptk_pool_arrived   the chunk's bytes are in its slot (stream-ordered)
+ *   ptk_pool_release   drain: the chunk leaves the device, its slot is free */
+typedef struct ptk_pool ptk_pool;
+int ptk_pool_create(int32_t n_chunk, int32_t n_persist, int32_t n_buffer, ptk_pool** out);
+void ptk_pool_destroy(ptk_pool* pool);
+int ptk_pool_grant(ptk_pool* pool, int32_t c, int32_t now, const int32_t* pinned,
+                   int32_t n_pinned, int32_t demand, int32_t* slot, int32_t* evicted);
+int ptk_pool_arrived(ptk_pool* pool, int32_t c);
+int ptk_pool_release(ptk_pool* pool, int32_t c, int32_t* slot);
+int32_t ptk_pool_slot_of(const ptk_pool* pool, int32_t c);       /* -1: none */
+int32_t ptk_pool_chunk_in_slot(const ptk_pool* pool, int32_t s);  /* 0: free */
+int32_t ptk_pool_residency(const ptk_pool* pool, int32_t c);      /* 0 away, 1 arriving,
+                                                                     2 resident, 3 draining */
+
+/* ---- the planner in process ------------------------------------------- */
+/* memplan::run_cli (proj/include/memplan/cli.hpp:20-35) with argv = the memplan
+ * command line without the program name; returns its exit code (0 ok, 1 domain
+ * error, 2 usage error) and malloc'ed stdout / stderr text (free with ptk_free). */
+int ptk_memplan_run(int32_t argc, const char* const* argv, char** out, char** err);
+void ptk_free(void* p);
+
 /* ---- streams / events / timing helpers used by the host runtime ------- */
 int ptk_stream_create(void** out, int32_t high_priority);
 int ptk_stream_destroy(void* stream);

@@ -145,7 +145,22 @@ _SIGNATURES = {
     "ptk_stream_synchronize": (c_int32, [c_void_p]),
     "ptk_device_synchronize": (c_int32, []),
     "ptk_kernel_launch_count": (c_int64, []),
+    "ptk_pool_create": (c_int32, [c_int32, c_int32, c_int32, POINTER(c_void_p)]),
+    "ptk_pool_destroy": (None, [c_void_p]),
+    "ptk_pool_grant": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_int32), c_int32, c_int32,
+                                 POINTER(c_int32), POINTER(c_int32)]),
+    "ptk_pool_arrived": (c_int32, [c_void_p, c_int32]),
+    "ptk_pool_release": (c_int32, [c_void_p, c_int32, POINTER(c_int32)]),
+    "ptk_pool_slot_of": (c_int32, [c_void_p, c_int32]),
+    "ptk_pool_chunk_in_slot": (c_int32, [c_void_p, c_int32]),
+    "ptk_pool_residency": (c_int32, [c_void_p, c_int32]),
+    "ptk_memplan_run": (c_int32, [c_int32, POINTER(c_char_p), POINTER(c_void_p),
+                                  POINTER(c_void_p)]),
+    "ptk_free": (None, [c_void_p]),
 }
+# int32-returning functions whose result is a value, not a status
+_VALUE_RESULTS = {"ptk_pool_slot_of", "ptk_pool_chunk_in_slot", "ptk_pool_residency",
+                  "ptk_memplan_run"}
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -176,7 +191,7 @@ class _Lib:
 
     def __getattr__(self, name):
         fn = getattr(_lib, name)
-        if _SIGNATURES[name][0] is c_int32:
+        if _SIGNATURES[name][0] is c_int32 and name not in _VALUE_RESULTS:
             def call(*args, _fn=fn, _name=name):
                 rc = _fn(*args)
                 check(rc, _name)
@@ -207,3 +222,65 @@ def shard_elems(n: int, world: int) -> int:
 
 def launch_count() -> int:
     return int(_lib.ptk_kernel_launch_count())
+
+
+class BufferPool:
+    """The runtime's chunk residency policy (memplan::ChunkBufferPool through
+    ptk_pool_*): slot grants, farthest-next-use eviction, arrival and release.
+    Chunk ids are 0-based here (1-based in C); positions are the C ones
+    (forward of 0-based chunk c = c + 1, backward = 2N - c)."""
+
+    def __init__(self, n_chunk: int, n_persist: int, n_buffer: int):
+        h = c_void_p()
+        lib.ptk_pool_create(n_chunk, n_persist, n_buffer, ctypes.byref(h))
+        self._h = h
+        self.n_chunk, self.n_persist, self.n_buffer = n_chunk, n_persist, n_buffer
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ptk_pool_destroy(self._h)
+            self._h = None
+
+    def grant(self, c: int, now: int, pinned=(), demand: bool = False
+              ) -> tuple[int, int | None] | None:
+        """(slot, evicted 0-based chunk or None), or None when no slot can be
+        granted for c at position `now` (demand: c is needed right now)."""
+        pin = (c_int32 * max(1, len(pinned)))(*[p + 1 for p in pinned])
+        slot, ev = c_int32(), c_int32()
+        lib.ptk_pool_grant(self._h, c + 1, now, pin, len(pinned), int(demand),
+                           ctypes.byref(slot), ctypes.byref(ev))
+        if slot.value < 0:
+            return None
+        return slot.value, (ev.value - 1 if ev.value else None)
+
+    def arrived(self, c: int) -> None:
+        lib.ptk_pool_arrived(self._h, c + 1)
+
+    def release(self, c: int) -> int:
+        slot = c_int32()
+        lib.ptk_pool_release(self._h, c + 1, ctypes.byref(slot))
+        return slot.value
+
+    def slot_of(self, c: int) -> int:
+        return int(_lib.ptk_pool_slot_of(self._h, c + 1))
+
+    def chunk_in_slot(self, s: int) -> int | None:
+        c = int(_lib.ptk_pool_chunk_in_slot(self._h, s))
+        return c - 1 if c else None
+
+    def residency(self, c: int) -> int:
+        return int(_lib.ptk_pool_residency(self._h, c + 1))
+
+
+def memplan_run(args: list[str]) -> tuple[int, str, str]:
+    """The planner CLI in process (ptk_memplan_run): (exit code, stdout, stderr)."""
+    argv = (c_char_p * max(1, len(args)))(*[a.encode() for a in args])
+    out, err = c_void_p(), c_void_p()
+    rc = int(_lib.ptk_memplan_run(len(args), argv, ctypes.byref(out), ctypes.byref(err)))
+    try:
+        so = ctypes.string_at(out).decode() if out.value else ""
+        se = ctypes.string_at(err).decode() if err.value else ""
+    finally:
+        _lib.ptk_free(out)
+        _lib.ptk_free(err)
+    return rc, so, se

@@ -1,8 +1,9 @@
 // The chunk runtime: executes one training iteration of a plan on the
 // device with the simulator's decisions and measured times (execute.hpp).
 //
-// Policy (identical decisions to the simulator, csrc/planner/simulator.cpp,
-// which restates proj/src/sim.cpp:99-685):
+// Policy: the shared chunk-runtime policy (include/memplan/policy.hpp), the
+// same code the simulator (csrc/planner/simulator.cpp) and the training-time
+// chunk pool run -- proj/src/sim.cpp's semantics:
 //   * positions: forward of chunk c at c, backward at 2N-c+1, optimizer 2N+1
 //   * fetch queue filled one position ahead of the GPU; ONE fetch in flight
 //   * a fetch needs a free slot of the n_buffer pool, else evicts the idle
@@ -26,12 +27,14 @@
 #include <limits>
 #include <map>
 #include <mutex>
+#include <optional>
 #include <stdexcept>
 #include <thread>
 
 #include "memplan/accounting.hpp"
 #include "memplan/errors.hpp"
 #include "memplan/execute.hpp"
+#include "memplan/policy.hpp"
 #include "ptk.h"
 
 namespace memplan {
@@ -50,8 +53,6 @@ std::int64_t host_ns() {
              std::chrono::steady_clock::now().time_since_epoch())
       .count();
 }
-
-enum class Where { Away, Arriving, Here, Leaving };
 
 struct DeviceBuf {
   void* p = nullptr;
@@ -199,15 +200,6 @@ class Runtime {
   }
 
  private:
-  enum class Kind { Fwd, Bwd, Recompute, Optim };
-  struct Job {
-    Kind kind;
-    int op;
-    int block;
-    int chunk;
-    double seconds;
-    int slot;
-  };
   // an asynchronous device operation whose completion the loop waits for
   struct Pending {
     enum What { Gpu, Upload, Gather, Reduce, Offload, SwapOut, SwapIn } what;
@@ -309,48 +301,25 @@ class Runtime {
   }
 
   // ------------------------------------------------------- one iteration --
+  using Job = IterationCore::Job;
   SimulationResult iterate();
   void prepare_iteration();
-  int fwd_slot(int c) const { return c; }
-  int bwd_slot(int c) const { return 2 * nc_ - c + 1; }
-  int chunk_in_slot(int p) const { return p <= nc_ ? p : 2 * nc_ - p + 1; }
-  int slot_now() const { return next_ < jobs_.size() ? jobs_[next_].slot : 2 * nc_ + 2; }
-  int next_use(int c) const {
-    const int p = slot_now();
-    if (fwd_slot(c) >= p) return fwd_slot(c);
-    if (bwd_slot(c) >= p) return bwd_slot(c);
-    return std::numeric_limits<int>::max();
-  }
-  BlockStrategy policy(const OperatorRecord& op) const {
-    return op.block_id ? sch_.strategies[*op.block_id] : BlockStrategy::None;
-  }
   void note(const char* res, const std::string& ev, const std::string& subj, std::int64_t t) {
     log_.push_back({t, res, ev, subj});
-  }
-  void alloc(std::int64_t d, std::int64_t t) {
-    held_ += d;
-    if (held_ < 0) throw LedgerUnderflow("allocated bytes went negative");
-    high_ = std::max(high_, held_);
-    if (!mem_.empty() && mem_.back().time_ns == t)
-      mem_.back().bytes = held_;
-    else
-      mem_.push_back({t, held_});
   }
   std::int64_t dev_ns(void* ev) const {
     float ms = 0;
     must(ptk_event_elapsed_ms(base_, ev, &ms), "elapsed");
     return static_cast<std::int64_t>(static_cast<double>(ms) * 1e6);
   }
-  void* chunk_dev_params(int c) {
-    ChunkStore& st = store_[c];
-    return st.persistent ? st.d_param.p : slots_[slot_of_[c]].p;
-  }
-  void* chunk_dev_grads(int c) {
+  void* chunk_slot(int c) {
     // non-persistent chunks reuse the gathered slot for gradients (quirk Q5:
     // the model charges a buffer only for the working copy)
-    ChunkStore& st = store_[c];
-    return st.persistent ? st.d_grad.p : slots_[slot_of_[c]].p;
+    const ChunkStore& st = store_[c];
+    return st.persistent ? nullptr : slots_[core_->pool().slot_of(c)].p;
   }
+  void* chunk_dev_params(int c) { return store_[c].persistent ? store_[c].d_param.p : chunk_slot(c); }
+  void* chunk_dev_grads(int c) { return store_[c].persistent ? store_[c].d_grad.p : chunk_slot(c); }
 
   Pending& launch(Pending::What what, void* stream, int chunk, int block, int op) {
     pending_.push_back({what, chunk, block, op, new_event(), new_event()});
@@ -359,14 +328,12 @@ class Runtime {
   }
   void finish_launch(Pending& p, void* stream) { must(ptk_event_record(p.end, stream), "record"); }
 
-  void enqueue_until(int slot);
   bool issue_prefetch(std::int64_t t);
   void swap_out_from(int b, int i, std::int64_t t);
   void swap_in_from(int b, int i, std::int64_t t);
   void release_swap_ins(std::int64_t t);
   void drain(int c, std::int64_t t);
   void reduced(int c, std::int64_t t);
-  bool ready(const Job& j) const;
   bool start_gpu(std::int64_t t);
   void finish_gpu(std::int64_t t);
   bool start_cpu(std::int64_t t);
@@ -388,39 +355,22 @@ class Runtime {
   int nops_ = 0, nc_ = 0, nblk_ = 0;
   std::vector<ChunkStore> store_;
   std::vector<DeviceBuf> slots_;
-  std::vector<int> free_slot_ids_;
-  std::vector<int> slot_of_;
   DeviceBuf swap_dev_, ws_, stats_dev_;
   HostBuf swap_host_;
   std::vector<void*> act_dev_, act_host_;
   std::int64_t device_bytes_ = 0, host_bytes_ = 0;
   ExecutionStats stats_;
 
-  // iteration state (mirrors the simulator)
-  std::vector<Job> jobs_;
-  std::size_t next_ = 0;         // oldest unfinished GPU job (the simulator's next_task)
+  // iteration state: every decision is the shared policy's (policy.hpp)
+  std::optional<IterationCore> core_;
   std::size_t next_launch_ = 0;  // next GPU job to put on the compute stream
   static constexpr std::size_t kRunAhead = 4;  // GPU jobs queued ahead (hides launch gaps)
-  std::vector<Where> where_;
-  std::vector<int> bwd_left_;
-  std::vector<char> reduce_done_;
-  std::deque<int> fetch_queue_;
-  int fetching_ = 0;
   int fetch_parts_left_ = 0;
-  int enqueued_ = 0;
-  std::vector<std::int64_t> blk_act_;
-  std::vector<int> blk_first_, blk_last_;
-  std::vector<double> blk_fwd_;
-  std::vector<char> out_done_, in_issued_, act_back_;
-  int lowest_entered_ = std::numeric_limits<int>::max();
-  bool in_backward_ = false;
   bool gpu_busy_ = false;
   std::deque<int> host_queue_;
   bool cpu_busy_ = false;
   std::int64_t cpu_first_ = -1, cpu_last_ = 0;
   std::int64_t fwd_end_ = 0, bwd_end_ = 0, gpu_end_ = 0;
-  std::int64_t held_ = 0, high_ = 0;
-  std::vector<MemSample> mem_;
   std::vector<TimelineEvent> log_;
   std::deque<Pending> pending_;
   std::int64_t t0_host_ = 0;
@@ -428,107 +378,28 @@ class Runtime {
 };
 
 void Runtime::prepare_iteration() {
-  jobs_.clear();
-  next_ = 0;
+  // the optimizer jobs' time is measured, not modelled (rate 0)
+  core_.emplace(tr_, lay_, sch_, cfg_, 0.0);
   next_launch_ = 0;
   log_.clear();
-  mem_.clear();
-  held_ = high_ = 0;
-  const std::size_t nb = static_cast<std::size_t>(std::max(1, nblk_));
-  blk_act_.assign(nb, 0);
-  blk_first_.assign(nb, -1);
-  blk_last_.assign(nb, -1);
-  blk_fwd_.assign(nb, 0.0);
-  for (const OperatorRecord& op : tr_.ops) {
-    if (!op.block_id) continue;
-    const int b = *op.block_id;
-    blk_act_[b] += op.act_bytes;
-    if (blk_first_[b] < 0) blk_first_[b] = op.index;
-    blk_last_[b] = op.index;
-    blk_fwd_[b] += op.t_fwd;
-  }
-  std::vector<int> op_chunk(nops_);
-  for (int i = 0; i < nops_; ++i) op_chunk[i] = lay_.chunk_of_op(i);
-  for (int i = 0; i < nops_; ++i)
-    jobs_.push_back({Kind::Fwd, i, tr_.ops[i].block_id.value_or(-1), op_chunk[i], tr_.ops[i].t_fwd,
-                     fwd_slot(op_chunk[i])});
-  for (int i = nops_ - 1; i >= 0; --i) {
-    const OperatorRecord& op = tr_.ops[i];
-    if (op.block_id && policy(op) == BlockStrategy::Checkpoint && i == blk_last_[*op.block_id])
-      jobs_.push_back({Kind::Recompute, -1, *op.block_id, op_chunk[i], blk_fwd_[*op.block_id],
-                       bwd_slot(op_chunk[i])});
-    jobs_.push_back({Kind::Bwd, i, op.block_id.value_or(-1), op_chunk[i], op.t_bwd,
-                     bwd_slot(op_chunk[i])});
-  }
-  for (int c = 1; c <= cfg_.n_persist; ++c) jobs_.push_back({Kind::Optim, -1, -1, c, 0.0, 2 * nc_ + 1});
-  where_.assign(nc_ + 1, Where::Away);
-  for (int c = 1; c <= cfg_.n_persist; ++c) where_[c] = Where::Here;
-  bwd_left_.assign(nc_ + 1, 0);
-  for (const Job& j : jobs_)
-    if (j.kind == Kind::Bwd || j.kind == Kind::Recompute) ++bwd_left_[j.chunk];
-  reduce_done_.assign(nc_ + 1, 0);
-  fetch_queue_.clear();
-  fetching_ = 0;
-  enqueued_ = 0;
-  out_done_.assign(nb, 0);
-  in_issued_.assign(nb, 0);
-  act_back_.assign(nops_, 0);
-  lowest_entered_ = std::numeric_limits<int>::max();
-  in_backward_ = false;
+  fetch_parts_left_ = 0;
   gpu_busy_ = cpu_busy_ = false;
   host_queue_.clear();
   cpu_first_ = -1;
   cpu_last_ = fwd_end_ = bwd_end_ = gpu_end_ = 0;
-  slot_of_.assign(nc_ + 1, -1);
-  free_slot_ids_.clear();
-  for (int i = cfg_.n_buffer - 1; i >= 0; --i) free_slot_ids_.push_back(i);
-}
-
-void Runtime::enqueue_until(int slot) {
-  const int upto = std::min(slot, 2 * nc_);
-  for (int p = enqueued_ + 1; p <= upto; ++p) {
-    const int c = chunk_in_slot(p);
-    if (where_[c] == Where::Away &&
-        std::find(fetch_queue_.begin(), fetch_queue_.end(), c) == fetch_queue_.end())
-      fetch_queue_.push_back(c);
-  }
-  enqueued_ = std::max(enqueued_, upto);
 }
 
 bool Runtime::issue_prefetch(std::int64_t t) {
-  if (fetching_ != 0 || fetch_queue_.empty()) return false;
-  const int c = fetch_queue_.front();
-  if (where_[c] != Where::Away) {
-    fetch_queue_.pop_front();
-    return true;
-  }
-  if (free_slot_ids_.empty()) {
-    // never evict a chunk a queued or next-to-queue GPU job uses
-    const auto pinned = [&](int v) {
-      for (std::size_t k = next_; k <= next_launch_ && k < jobs_.size(); ++k)
-        if (jobs_[k].chunk == v) return true;
-      return false;
-    };
-    int victim = 0, victim_use = -1;
-    for (int v = cfg_.n_persist + 1; v <= nc_; ++v) {
-      if (where_[v] != Where::Here || pinned(v)) continue;
-      const int use = next_use(v);
-      if (use > victim_use) {
-        victim_use = use;
-        victim = v;
-      }
-    }
-    if (victim == 0 || victim_use <= next_use(c)) return false;
-    where_[victim] = Where::Away;
-    free_slot_ids_.push_back(slot_of_[victim]);
-    slot_of_[victim] = -1;
-    note("gpu", "evict", "chunk=" + std::to_string(victim), t);
-  }
-  fetch_queue_.pop_front();
-  slot_of_[c] = free_slot_ids_.back();
-  free_slot_ids_.pop_back();
-  where_[c] = Where::Arriving;
-  fetching_ = c;
+  // the chunks of every GPU job already on the stream (and the next one) stay
+  std::vector<int> pinned;
+  const auto& jobs = core_->jobs();
+  for (std::size_t k = core_->cursor(); k <= next_launch_ && k < jobs.size(); ++k)
+    pinned.push_back(jobs[k].chunk);
+  const auto d = core_->pool().next_fetch(core_->position(), pinned);
+  if (d.step == ChunkBufferPool::FetchStep::Nothing) return false;
+  if (d.step == ChunkBufferPool::FetchStep::Skipped) return true;
+  if (d.grant.evicted != 0) note("gpu", "evict", "chunk=" + std::to_string(d.grant.evicted), t);
+  const int c = d.grant.chunk;
   ChunkStore& st = store_[c];
   // upload this rank's shard into its place in the slot, then all-gather
   char* dst = static_cast<char*>(chunk_dev_params(c)) + 2 * st.shard * opt_.rank;
@@ -554,47 +425,35 @@ bool Runtime::issue_prefetch(std::int64_t t) {
 }
 
 void Runtime::swap_out_from(int b, int i, std::int64_t t) {
-  while (i <= blk_last_[b] && tr_.ops[i].act_bytes == 0) ++i;
-  if (i > blk_last_[b]) {
-    out_done_[b] = 1;
+  const int op = core_->swap_out_next(b, i);
+  if (op < 0) {
     note("d2h", "swap_out_done", "block=" + std::to_string(b), t);
     return;
   }
-  Pending& p = launch(Pending::SwapOut, s_d2h_, 0, b, i);
-  must(ptk_memcpy_d2h_async(act_host_[i], act_dev_[i], tr_.ops[i].act_bytes, s_d2h_), "swap out");
+  Pending& p = launch(Pending::SwapOut, s_d2h_, 0, b, op);
+  must(ptk_memcpy_d2h_async(act_host_[op], act_dev_[op], tr_.ops[op].act_bytes, s_d2h_), "swap out");
   finish_launch(p, s_d2h_);
-  stats_.d2h_bytes += tr_.ops[i].act_bytes;
-  note("d2h", "swap_out_start", "block=" + std::to_string(b) + " op=" + std::to_string(i), t);
+  stats_.d2h_bytes += tr_.ops[op].act_bytes;
+  note("d2h", "swap_out_start", "block=" + std::to_string(b) + " op=" + std::to_string(op), t);
   p.start_note = static_cast<int>(log_.size()) - 1;
 }
 
 void Runtime::swap_in_from(int b, int i, std::int64_t t) {
-  for (; i >= blk_first_[b] && tr_.ops[i].act_bytes == 0; --i) act_back_[i] = 1;
-  if (i < blk_first_[b]) {
+  const int op = core_->swap_in_next(b, i);
+  if (op < 0) {
     note("h2d", "swap_in_done", "block=" + std::to_string(b), t);
     return;
   }
-  Pending& p = launch(Pending::SwapIn, s_h2d_, 0, b, i);
-  must(ptk_memcpy_h2d_async(act_dev_[i], act_host_[i], tr_.ops[i].act_bytes, s_h2d_), "swap in");
+  Pending& p = launch(Pending::SwapIn, s_h2d_, 0, b, op);
+  must(ptk_memcpy_h2d_async(act_dev_[op], act_host_[op], tr_.ops[op].act_bytes, s_h2d_), "swap in");
   finish_launch(p, s_h2d_);
-  stats_.h2d_bytes += tr_.ops[i].act_bytes;
-  note("h2d", "swap_in_start", "block=" + std::to_string(b) + " op=" + std::to_string(i), t);
+  stats_.h2d_bytes += tr_.ops[op].act_bytes;
+  note("h2d", "swap_in_start", "block=" + std::to_string(b) + " op=" + std::to_string(op), t);
   p.start_note = static_cast<int>(log_.size()) - 1;
 }
 
 void Runtime::release_swap_ins(std::int64_t t) {
-  for (int b = 0; b < nblk_; ++b) {
-    if (sch_.strategies[b] != BlockStrategy::Swap || in_issued_[b] || !out_done_[b]) continue;
-    const int entered =
-        in_backward_ ? std::min(lowest_entered_, nblk_) : std::numeric_limits<int>::max();
-    const bool near = entered <= b + cfg_.n_interval;
-    const bool room = (high_ - held_) >= blk_act_[b];
-    const bool needed = next_ < jobs_.size() && jobs_[next_].kind == Kind::Bwd && jobs_[next_].block == b;
-    if ((near && room) || needed) {
-      in_issued_[b] = 1;
-      swap_in_from(b, blk_last_[b], t);
-    }
-  }
+  for (const int b : core_->swap_ins_due()) swap_in_from(b, core_->block_last(b), t);
 }
 
 void Runtime::drain(int c, std::int64_t t) {
@@ -618,11 +477,8 @@ void Runtime::drain(int c, std::int64_t t) {
 }
 
 void Runtime::reduced(int c, std::int64_t t) {
+  if (!core_->reduced(c)) return;  // persistent: its device optimizer job is now ready
   ChunkStore& st = store_[c];
-  if (st.persistent) {
-    reduce_done_[c] = 1;
-    return;
-  }
   void* after = new_event();
   must(ptk_event_record(after, w_ > 1 ? s_coll_ : s_gpu_), "record");
   must(ptk_stream_wait_event(s_d2h_, after), "wait");
@@ -636,60 +492,35 @@ void Runtime::reduced(int c, std::int64_t t) {
   off.start_note = static_cast<int>(log_.size()) - 1;
 }
 
-bool Runtime::ready(const Job& j) const {
-  const auto present = [&](int c) { return where_[c] == Where::Here || where_[c] == Where::Leaving; };
-  switch (j.kind) {
-    case Kind::Fwd:
-    case Kind::Recompute:
-      return present(j.chunk);
-    case Kind::Bwd:
-      if (!present(j.chunk)) return false;
-      return !(j.block >= 0 && sch_.strategies[j.block] == BlockStrategy::Swap &&
-               tr_.ops[j.op].act_bytes > 0 && !act_back_[j.op]);
-    case Kind::Optim:
-      return reduce_done_[j.chunk] != 0;
-  }
-  return false;
-}
-
 // Queues the next GPU job if it is ready. Up to kRunAhead jobs sit on the
 // compute stream at once (stream order keeps them serial, as the simulator's
 // single GPU queue); readiness can only be lost by eviction, and queued jobs'
 // chunks are pinned against eviction.
 bool Runtime::start_gpu(std::int64_t t) {
-  if (next_launch_ >= jobs_.size() || next_launch_ - next_ >= kRunAhead) return false;
-  const Job& j = jobs_[next_launch_];
-  if (!ready(j)) return false;
+  const auto& jobs = core_->jobs();
+  if (next_launch_ >= jobs.size() || next_launch_ - core_->cursor() >= kRunAhead) return false;
+  const Job& j = jobs[next_launch_];
+  if (!core_->ready(j)) return false;
   ++next_launch_;
-  enqueue_until(j.slot + 1);
-  if (j.kind == Kind::Bwd || j.kind == Kind::Recompute) {
-    in_backward_ = true;
-    if (j.block >= 0) lowest_entered_ = std::min(lowest_entered_, j.block);
-  }
+  core_->start(j, t);
   Pending& p = launch(Pending::Gpu, s_gpu_, j.chunk, j.block, j.op);
   const auto busy = [&](double sec) {
     must(ptk_busy_wait(static_cast<std::int64_t>(sec * opt_.compute_scale * 1e9), s_gpu_), "busy");
   };
   switch (j.kind) {
-    case Kind::Recompute:
-      alloc(blk_act_[j.block] - tr_.ops[blk_first_[j.block]].act_bytes, t);
+    case Job::Recompute:
       note("gpu", "recompute_start", "block=" + std::to_string(j.block), t);
       busy(j.seconds);
       break;
-    case Kind::Bwd: {
-      const OperatorRecord& op = tr_.ops[j.op];
-      high_ = std::max(high_, held_ + op.d_peak_prior);
-      if (op.d_cur_prior != 0) alloc(op.d_cur_prior, t);
-      high_ = std::max(high_, held_ + op.d_peak_op);
+    case Job::Backward:
       note("gpu", "bwd_start", "op=" + std::to_string(j.op), t);
       busy(j.seconds);
       break;
-    }
-    case Kind::Fwd:
+    case Job::Forward:
       note("gpu", "fwd_start", "op=" + std::to_string(j.op), t);
       busy(j.seconds);
       break;
-    case Kind::Optim: {
+    case Job::Optimizer: {
       note("gpu", "optim_start", "chunk=" + std::to_string(j.chunk), t);
       ChunkStore& st = store_[j.chunk];
       const ptk_adam_config a = adam(1.0 / w_);
@@ -712,47 +543,29 @@ bool Runtime::start_gpu(std::int64_t t) {
 }
 
 void Runtime::finish_gpu(std::int64_t t) {
-  const Job j = jobs_[next_];
-  ++next_;
-  gpu_busy_ = next_ < next_launch_;
+  const IterationCore::Finished f = core_->finish(t);
+  gpu_busy_ = core_->cursor() < next_launch_;
   gpu_end_ = t;
-  const auto chunk_done = [&](int c) {
-    if (--bwd_left_[c] != 0) return;
-    if (c > cfg_.n_persist) where_[c] = Where::Leaving;
-    drain(c, t);
-  };
+  const Job& j = f.job;
   switch (j.kind) {
-    case Kind::Fwd: {
-      const OperatorRecord& op = tr_.ops[j.op];
-      const BlockStrategy pol = policy(op);
-      const bool first = op.block_id && j.op == blk_first_[*op.block_id];
-      const bool keep = pol == BlockStrategy::None || pol == BlockStrategy::Swap ||
-                        (pol == BlockStrategy::Checkpoint && first);
-      if (keep && op.act_bytes > 0) alloc(op.act_bytes, t);
-      if (op.block_id && j.op == blk_last_[*op.block_id] && pol == BlockStrategy::Swap)
-        swap_out_from(*op.block_id, blk_first_[*op.block_id], t);
+    case Job::Forward:
+      if (f.swap_out_block >= 0) swap_out_from(f.swap_out_block, core_->block_first(f.swap_out_block), t);
       note("gpu", "fwd_end", "op=" + std::to_string(j.op), t);
       fwd_end_ = t;
       break;
-    }
-    case Kind::Bwd: {
-      const OperatorRecord& op = tr_.ops[j.op];
-      if (op.d_cur_op != 0) alloc(op.d_cur_op, t);
-      if (op.act_bytes > 0) alloc(-op.act_bytes, t);
+    case Job::Backward:
       note("gpu", "bwd_end", "op=" + std::to_string(j.op), t);
       bwd_end_ = t;
-      chunk_done(j.chunk);
       break;
-    }
-    case Kind::Recompute:
+    case Job::Recompute:
       note("gpu", "recompute_end", "block=" + std::to_string(j.block), t);
       bwd_end_ = t;
-      chunk_done(j.chunk);
       break;
-    case Kind::Optim:
+    case Job::Optimizer:
       note("gpu", "optim_end", "chunk=" + std::to_string(j.chunk), t);
       break;
   }
+  if (f.drain_chunk != 0) drain(f.drain_chunk, t);
 }
 
 bool Runtime::start_cpu(std::int64_t t) {
@@ -777,10 +590,7 @@ void Runtime::complete(const Pending& p, std::int64_t t) {
     case Pending::Gather:
       note(p.what == Pending::Upload ? "h2d" : "coll",
            p.what == Pending::Upload ? "upload_end" : "gather_end", tag, t);
-      if (--fetch_parts_left_ == 0) {
-        where_[p.chunk] = Where::Here;
-        if (fetching_ == p.chunk) fetching_ = 0;
-      }
+      if (--fetch_parts_left_ == 0) core_->pool().arrived(p.chunk);
       break;
     case Pending::Reduce:
       note("coll", "reduce_end", tag, t);
@@ -788,19 +598,16 @@ void Runtime::complete(const Pending& p, std::int64_t t) {
       break;
     case Pending::Offload:
       note("d2h", "offload_end", tag, t);
-      where_[p.chunk] = Where::Away;
-      free_slot_ids_.push_back(slot_of_[p.chunk]);
-      slot_of_[p.chunk] = -1;
+      core_->offloaded(p.chunk);  // the slot is free again
       host_queue_.push_back(p.chunk);
       break;
     case Pending::SwapOut:
-      alloc(-tr_.ops[p.op].act_bytes, t);
+      core_->swapped_out(p.op, t);
       note("d2h", "swap_out_end", "block=" + std::to_string(p.block) + " op=" + std::to_string(p.op), t);
       swap_out_from(p.block, p.op + 1, t);
       break;
     case Pending::SwapIn:
-      alloc(tr_.ops[p.op].act_bytes, t);
-      act_back_[p.op] = 1;
+      core_->swapped_in(p.op, t);
       note("h2d", "swap_in_end", "block=" + std::to_string(p.block) + " op=" + std::to_string(p.op), t);
       swap_in_from(p.block, p.op - 1, t);
       break;
@@ -814,10 +621,6 @@ SimulationResult Runtime::iterate() {
   must(ptk_event_record(base_, s_gpu_), "record");
   must(ptk_stream_synchronize(s_gpu_), "sync");
   t0_host_ = host_ns();
-  // model states + residual floor
-  alloc(device_state_bytes(cfg_) + tr_.m_fwd,
-        0);
-  enqueue_until(1);
   std::int64_t now = 0;
   for (;;) {
     for (bool moved = true; moved;) {
@@ -827,7 +630,7 @@ SimulationResult Runtime::iterate() {
       moved |= issue_prefetch(now);
       release_swap_ins(now);
     }
-    const bool work_left = next_ < jobs_.size() || !host_queue_.empty() || cpu_busy_ ||
+    const bool work_left = !core_->finished() || !host_queue_.empty() || cpu_busy_ ||
                            !pending_.empty();
     if (!work_left) break;
     if (pending_.empty() && !cpu_busy_)
@@ -865,7 +668,8 @@ SimulationResult Runtime::iterate() {
         Pending p = pending_[best_i];
         pending_.erase(pending_.begin() + static_cast<std::ptrdiff_t>(best_i));
         now = std::max(now, best_t);
-        if (p.what == Pending::Gpu && tr_.ops.size() && jobs_[next_].kind == Kind::Optim)
+        if (p.what == Pending::Gpu && !core_->finished() &&
+            core_->jobs()[core_->cursor()].kind == Job::Optimizer)
           stats_.gpu_optim_ns += dev_ns(p.end) - dev_ns(p.start);
         if (p.start_note >= 0) log_[p.start_note].time_ns = dev_ns(p.start);
         complete(p, best_t);
@@ -882,11 +686,11 @@ SimulationResult Runtime::iterate() {
   r.t_bwd = static_cast<double>(std::max<std::int64_t>(0, bwd_end_ - fwd_end_)) * 1e-9;
   r.t_iter = static_cast<double>(std::max(gpu_end_, cpu_last_)) * 1e-9;
   r.t_cpu_optim_span = cpu_first_ >= 0 ? static_cast<double>(cpu_last_ - cpu_first_) * 1e-9 : 0.0;
-  r.m_peak = high_;
+  r.m_peak = core_->ledger().high();
   std::stable_sort(log_.begin(), log_.end(),
                    [](const TimelineEvent& a, const TimelineEvent& b) { return a.time_ns < b.time_ns; });
   r.timeline = log_;
-  r.mem_trace = mem_;
+  r.mem_trace = core_->ledger().samples();
   return r;
 }
 

@@ -1,7 +1,10 @@
 """Non-persistent chunks inside the training model: host-resident shards, a
-pool of device buffers, fetch-before-use and drain-after-backward — the
-chunk runtime's policy (csrc/runtime/executor.cpp, which restates
-proj/src/sim.cpp:275-451) driven by autograd instead of a trace.
+pool of device buffers, fetch-before-use and drain-after-backward, driven by
+autograd instead of a trace. Every residency decision (which slot, which
+chunk to evict, when a slot frees up) is made by the runtime's ONE policy
+implementation, memplan::ChunkBufferPool in libptk.so (ptk_pool_*; the same
+code the simulator and the device executor run, proj/src/sim.cpp:275-451's
+rules); this module moves the bytes.
 
 * storage: chunk c >= n_persist keeps its rank shard in pinned host memory
   (fp32 master/m/v, bf16 params, bf16 grads); `n_buffer` device slots hold
@@ -10,10 +13,11 @@ proj/src/sim.cpp:275-451) driven by autograd instead of a trace.
   shard into its slot position on the h2d stream (+ NCCL all-gather, w > 1),
   the compute stream waits on that event; one prefetch ahead (the next chunk
   in forward, the previous one in backward);
-* eviction: the resident pool chunk whose next use (forward position c,
-  backward position 2N-c+1) is farthest, never the chunk being acquired or
-  in use; the h2d stream waits for all compute issued so far before it
-  overwrites the slot;
+* eviction (policy): the resident pool chunk whose next use (forward
+  position c, backward position 2N-c+1) is farthest, never the chunk being
+  acquired or in use; a prefetch is issued only if that chunk is needed
+  strictly later than the prefetched one (the simulator's rule). The h2d
+  stream waits for all compute issued so far before it overwrites the slot;
 * autograd: a chunk's parameters are outputs of `ChunkGather` (one node per
   use in forward); tensors autograd saves that live in a slot are saved as
   (chunk, offset, shape) and re-acquired on unpack, so a chunk evicted between
@@ -80,8 +84,8 @@ class ChunkPool:
                       for _ in range(n_buffer)]
         self.device_bytes = 2 * n_pad_max * n_buffer
         self.host_bytes = sum(16 * s for s in self.shard.values())
-        self.slot_of: dict[int, int] = {}
-        self.free = list(range(n_buffer - 1, -1, -1))
+        # chunks 0..first-1 are persistent (resident, never pooled)
+        self.policy = nat.BufferPool(len(numels), first, n_buffer)
         self.slot_released: list = [None] * n_buffer  # compute event at the slot's release
         self.ready: dict[int, torch.cuda.Event] = {}
         self.h2d, self.d2h = torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)
@@ -112,13 +116,8 @@ class ChunkPool:
         self.h_v[c].zero_()
 
     # -------------------------------------------------------------- policy --
-    def _next_use(self, c: int) -> int:
-        fwd, bwd = c + 1, 2 * self.n_total - c
-        if fwd >= self.position:
-            return fwd
-        if bwd >= self.position:
-            return bwd
-        return 1 << 30
+    def resident(self, c: int) -> bool:
+        return self.policy.slot_of(c) >= 0
 
     def _pieces(self, c: int):
         s = self.shard[c]
@@ -130,23 +129,26 @@ class ChunkPool:
         chunk's pending host update: it is skipped and retried later. A
         blocking fetch of a chunk whose update is still running uploads it
         piece by piece as the host finishes each piece."""
-        if c in self.slot_of:
+        if self.resident(c):
             return True
         fut = self.updates.get(c)
         if fut is not None and not blocking and not fut.done():
             self.counters["prefetch_deferred"] = self.counters.get("prefetch_deferred", 0) + 1
             return False
-        if self.free:
-            k = self.free.pop()
+        # acquiring c itself is a demand fetch (it is needed now); a prefetch
+        # follows the simulator's rule (evict only a chunk needed later than c)
+        granted = self.policy.grant(c, self.position, pinned=(c, keep), demand=c == keep)
+        if granted is None:
+            if c == keep:
+                raise RuntimeError("chunk pool exhausted: every buffer is in use")
+            self.counters["prefetch_refused"] = self.counters.get("prefetch_refused", 0) + 1
+            return False
+        k, v = granted
+        if v is None:
             # compute that used the slot before it was freed must be done
             if self.slot_released[k] is not None:
                 self.h2d.wait_event(self.slot_released[k])
         else:
-            victims = [(self._next_use(v), v) for v in self.slot_of if v not in (c, keep)]
-            if not victims:
-                raise RuntimeError("chunk pool exhausted: every buffer is in use")
-            _, v = max(victims)
-            k = self.slot_of.pop(v)
             self.ready.pop(v, None)
             self.counters["evict"] += 1
             if self.timeline is not None:
@@ -154,7 +156,6 @@ class ChunkPool:
                                   f"chunk={v + 1}")
             # the evicted chunk may still be read by compute already issued
             self.h2d.wait_stream(torch.cuda.current_stream(self.device))
-        self.slot_of[c] = k
         s = self.shard[c]
         dst = self.slots[k][self.rank * s:(self.rank + 1) * s]
         done = self.piece_done.get(c) if fut is not None else None
@@ -180,6 +181,7 @@ class ChunkPool:
         ev = torch.cuda.Event()
         ev.record(self.h2d)
         self.ready[c] = ev
+        self.policy.arrived(c)  # stream-ordered: users wait on ready[c]
         self.counters["fetch"] += 1
         return True
 
@@ -190,12 +192,12 @@ class ChunkPool:
             self.position = position
             self._fetch(c, c)
             torch.cuda.current_stream(self.device).wait_event(self.ready[c])
-            view = self.slots[self.slot_of[c]][: self.shard[c] * self.world]
-            if prefetch is not None and prefetch in self.numel and prefetch not in self.slot_of:
-                if self.free or len(self.slot_of) > 1:
-                    # w > 1: the prefetch's all-gather must be issued in the same
-                    # order on every rank, so it may not depend on host timing
-                    self._fetch(prefetch, c, blocking=self.world > 1)
+            view = self.slots[self.policy.slot_of(c)][: self.shard[c] * self.world]
+            if prefetch is not None and prefetch in self.numel and not self.resident(prefetch):
+                # w > 1: the prefetch's all-gather must be issued in the same
+                # order on every rank, so it may not depend on host timing (the
+                # policy's decision depends on positions only)
+                self._fetch(prefetch, c, blocking=self.world > 1)
             return view
 
     # --------------------------------------------------------------- drain --
@@ -240,12 +242,11 @@ class ChunkPool:
         cfg = self.hyper.config(self.step, self.world)
         # the device copy is stale once the host update runs: release the slot
         # (a later fetch into it waits for the compute issued until now)
-        if c in self.slot_of:
-            k = self.slot_of.pop(c)
+        if self.resident(c):
+            k = self.policy.release(c)
             released = torch.cuda.Event()
             released.record(cur)
             self.slot_released[k] = released
-            self.free.append(k)
             self.ready.pop(c, None)
         self.piece_done[c] = [threading.Event() for _ in landed]
         self.updates[c] = self.worker.submit(self._host_adam, c, landed, cfg)
@@ -282,7 +283,7 @@ class ChunkPool:
         if k is None:
             return ("t", t)
         with self._lock:
-            c = next(ch for ch, kk in self.slot_of.items() if kk == k)
+            c = self.policy.chunk_in_slot(k)
         return ("ref", c, t.storage_offset(), tuple(t.shape), tuple(t.stride()))
 
     def unpack(self, packed):

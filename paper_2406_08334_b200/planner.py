@@ -1,7 +1,9 @@
 """Python access to the chunk planner (layouts for the data plane).
 
-The planner is the C++ drop-in of the reference API (include/memplan/*.hpp,
-built as build/memplan); `layout_for` returns the `pack` JSON of a named
+The planner is the C++ drop-in of the reference API (include/memplan/*.hpp),
+linked into libptk.so and called IN PROCESS through the C-ABI
+(ptk_memplan_run = memplan::run_cli, proj/include/memplan/cli.hpp:20-35): no
+subprocess, no binary on PATH. `layout_for` returns the `pack` JSON of a named
 workload trace: {"s_chunk", "n_chunk", "waste_bytes", "chunks": [...],
 "bytes_per_param"}.
 """
@@ -9,12 +11,10 @@ from __future__ import annotations
 
 import json
 import os
-import subprocess
 import tempfile
 
 from . import REPO_DIR
 
-MEMPLAN_BIN = os.path.join(REPO_DIR, "build", "memplan")
 GOLDEN_DIR = os.path.join(REPO_DIR, "tests", "golden")
 
 # named traces: gen-trace arguments
@@ -27,12 +27,12 @@ TRACE_ARGS = {
 
 
 def run_memplan(args: list[str]) -> str:
-    if not os.path.exists(MEMPLAN_BIN):
-        raise FileNotFoundError(f"{MEMPLAN_BIN} not built: run `make planner`")
-    r = subprocess.run([MEMPLAN_BIN] + args, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"memplan {' '.join(args)} failed ({r.returncode}): {r.stderr.strip()}")
-    return r.stdout
+    """One memplan command in process; raises with its stderr on a nonzero exit."""
+    from . import _native
+    rc, out, err = _native.memplan_run(args)
+    if rc != 0:
+        raise RuntimeError(f"memplan {' '.join(args)} failed ({rc}): {err.strip()}")
+    return out
 
 
 def trace_file(args: list[str], path: str) -> str:
@@ -62,6 +62,6 @@ def pack(trace_path: str, grid: str | None = None) -> dict:
 
 
 def layout_for(name: str) -> dict:
-    """Chunk layout of a named trace, produced by the clean-room planner
-    (raises if build/memplan is missing: no fallback to stored layouts)."""
+    """Chunk layout of a named trace, produced by the planner in libptk.so
+    (raises if the library is missing: no fallback to stored layouts)."""
     return _with_trace(name, pack)

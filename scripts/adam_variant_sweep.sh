@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 for N in ${NS:-268435456 16777216 522593600}; do
   REPS=$(( N < 50000000 ? 200 : 20 ))
   for round in 1 2; do
-    for v in ${VARIANTS:-tma1536x9t384 tma2048x6t512 tma2048x6t256 tma2048x6t512h tma2560x5t640 tma3072x4t384 tma3072x4t768 tma1024x13t256 tma1792x7t448 tma1024x6x2t256}; do
+    for v in ${VARIANTS:-tma1536x9t384 tma2048x6t512 tma2048x6t512h tma2560x5t640 tma3072x4t768 tma1024x13t256 tma1792x7t448 tma1024x6x2t256}; do
       echo -n "$v "; PTK_ADAM_VARIANT=$v timeout 120 python scripts/ab_adam.py build/ab/libptk_bench.so $N $REPS
     done
     [ -f build/ab/libptk_old.so ] && { echo -n "r01 "; python scripts/ab_adam.py build/ab/libptk_old.so $N $REPS; }
