@@ -161,11 +161,11 @@ int ptk_clip_coef(const ptk_grad_stats_t* stats, double max_norm,
  * GPU optimizer task (proj/src/cost.cpp:206-219) and gather
  * (proj/src/hardware.cpp:29-34) of one chunk with ONE kernel: by default a
  * TMA ring (cp.async.bulk of the local state and of every rank's gradient
- * tile into shared memory, bulk stores of the bf16 tile into every rank)
- * when every peer buffer is on the calling device, the register-staged
- * variant (128-bit peer loads / stores) when one is on another GPU;
- * PTK_FUSED_KERNEL=tma|ldg forces one. Both are bit-identical. shard must be
- * a multiple of 8 elements. */
+ * tile into shared memory, bulk stores of the bf16 tile into every rank,
+ * tiles claimed dynamically by the CTAs when a workspace is given);
+ * PTK_FUSED_KERNEL=ldg selects the register-staged variant (128-bit peer
+ * loads / stores). Both are bit-identical. shard must be a multiple of 8
+ * elements. */
 int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad_peers,
                          uint16_t* const* param_peers, int32_t world, int32_t rank,
                          int64_t shard, float* master, float* exp_avg,
@@ -174,9 +174,8 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
 
 /* Table form of the fused step: every chunk of a rank in ONE launch (the
  * ring stays full across chunks). kernel: PTK_FUSED_AUTO (PTK_FUSED_KERNEL
- * env if set, else TMA when every peer buffer is on the calling device and
- * the register-staged kernel otherwise -- decided once, here), PTK_FUSED_TMA
- * or PTK_FUSED_LDG. gscale_dev / skip_dev as for ptk_chunk_adam (a device
+ * env if set, else the TMA ring -- decided once, here), PTK_FUSED_TMA or
+ * PTK_FUSED_LDG (register-staged 128-bit peer loads / stores). gscale_dev / skip_dev as for ptk_chunk_adam (a device
  * clip coefficient / overflow flag from ptk_stats_collect).
  * ptk_fused_grad_stats_table is phase 1 of a clipped or overflow-checked
  * step: the statistics of this rank's reduced, scaled gradient shards (the

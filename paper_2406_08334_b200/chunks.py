@@ -501,15 +501,15 @@ PTK_MAX = nat.PTK_MAX_PEERS
 
 def fused_kernel_choice(same_device: bool) -> int:
     """The fused kernel for a peer table: PTK_FUSED_KERNEL=tma|ldg if set,
-    else the TMA ring when every rank's buffers are on this GPU (virtual
-    ranks, same-device cudaIpc) and the register-staged kernel (plain
-    128-bit peer loads / stores) across GPUs. Chosen once per table."""
+    else the TMA ring (dynamic tile schedule, 1.03-1.05 of the measured HBM
+    peak with virtual ranks) wherever the peer buffers live -- bulk copies
+    address cudaIpc / peer mappings like any global memory. The
+    register-staged kernel (plain 128-bit peer loads / stores) stays
+    selectable. Chosen once per table."""
     env = os.environ.get("PTK_FUSED_KERNEL", "")
-    if env == "tma":
-        return nat.PTK_FUSED_TMA
     if env == "ldg":
         return nat.PTK_FUSED_LDG
-    return nat.PTK_FUSED_TMA if same_device else nat.PTK_FUSED_LDG
+    return nat.PTK_FUSED_TMA
 
 
 def fused_group_step(sets: list[ChunkSet], hyper: AdamHyper, stream=None, with_stats: bool = True,

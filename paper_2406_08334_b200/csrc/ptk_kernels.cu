@@ -1466,14 +1466,6 @@ int fused_env_override() {
   return mode;
 }
 
-bool on_device(const void* p, int dev) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice && a.device == dev;
-}
 
 int fused_tile_for(int world) {
   switch (world) {
@@ -1592,9 +1584,9 @@ const char* ptk_fused_kernel_name(void) {
     case PTK_FUSED_LDG:
       return "fused_peer_kernel (ldg, forced by PTK_FUSED_KERNEL=ldg)";
     default:
-      return "per table: fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for "
-             "W>=5; threads = tile/4; stages = min(9, 220 KB / stage)) when every peer buffer is "
-             "on this device, fused_peer_kernel (ldg) across devices";
+      return "fused_peer_tma_kernel (tile 2048 for W=2, 1536 for W=1,3,4, 1024 for W>=5; "
+             "threads = tile/4 + producer/storer warps; stages = min(9, 220 KB / stage); dynamic "
+             "tile schedule)";
   }
 }
 
@@ -1746,7 +1738,6 @@ int ptk_fused_table_create(const ptk_fused_desc* descs, int32_t n_chunks, int32_
   t->rank = rank;
   t->device = current_device();
   const int tile = fused_tile_for(world);
-  bool all_local = true;
   int64_t tile0 = 0;
   for (int32_t c = 0; c < n_chunks; ++c) {
     const ptk_fused_desc& d = descs[c];
@@ -1762,9 +1753,6 @@ int ptk_fused_table_create(const ptk_fused_desc* descs, int32_t n_chunks, int32_
         bad = "peer buffers must be non-null and 16-byte aligned";
       f.grad[r] = d.grad_peers[r];
       f.param[r] = d.param_peers[r];
-      if (!bad && kernel == PTK_FUSED_AUTO)
-        all_local = all_local && on_device(d.grad_peers[r], t->device) &&
-                    on_device(d.param_peers[r], t->device);
     }
     if (bad) {
       delete t;
@@ -1781,11 +1769,12 @@ int ptk_fused_table_create(const ptk_fused_desc* descs, int32_t n_chunks, int32_
   }
   t->total_tiles = tile0;
   // Kernel choice, once per table: the caller's, else PTK_FUSED_KERNEL, else
-  // the TMA ring when every peer buffer is on this device (virtual ranks,
-  // same-GPU cudaIpc mappings) and the register-staged kernel across GPUs.
+  // the TMA ring. Bulk copies address peer memory like any global memory (a
+  // cudaIpc / peer mapping is a global address), as TMA loads from peer GPUs
+  // do in distributed GEMMs; the register-staged kernel stays selectable.
   int k = kernel;
   if (k == PTK_FUSED_AUTO) k = fused_env_override();
-  if (k == PTK_FUSED_AUTO) k = all_local ? PTK_FUSED_TMA : PTK_FUSED_LDG;
+  if (k == PTK_FUSED_AUTO) k = PTK_FUSED_TMA;
   t->kernel = k;
   if (n_chunks > 0) {
     const size_t bytes = sizeof(FusedDesc) * t->host.size();
@@ -1872,14 +1861,8 @@ int ptk_fused_rs_adam_ag(const ptk_adam_config* cfg, const uint16_t* const* grad
   if (!aligned16(master) || !aligned16(exp_avg) || !aligned16(exp_avg_sq))
     return fail(PTK_EINVAL, "ptk_fused_rs_adam_ag: state buffers must be 16-byte aligned");
   if (shard == 0) return PTK_OK;
-  const int dev = current_device();
   int k = fused_env_override();
-  if (k == PTK_FUSED_AUTO) {
-    bool local = true;
-    for (int r = 0; r < world && local; ++r)
-      local = on_device(grad_peers[r], dev) && on_device(param_peers[r], dev);
-    k = local ? PTK_FUSED_TMA : PTK_FUSED_LDG;
-  }
+  if (k == PTK_FUSED_AUTO) k = PTK_FUSED_TMA;
   list.table = nullptr;
   list.one.master = master;
   list.one.m = exp_avg;

@@ -291,54 +291,70 @@ FULL_SIZE = {  # workload -> (parameters, chunks): SURVEY §8(a) golden layouts
     "gpt2-1b_b2": (985_376_256, 4),
     "gpt2-1.5b_b8": (1_557_608_000, 3),
     "gpt2-10b_b8": (9_876_279_296, 49),   # 158 GB of chunk state on one B200
+    "flat512": (268_435_456, 1),           # one flat 512 MiB chunk (cfg5's largest point)
 }
+PARITY_STEPS = 10  # 10 steps, fresh gradients (seed 1 + rank + step) each step
+HYPERS = {"adam": dict(), "adamw_wd0.01": dict(weight_decay=0.01, adamw=True)}
 
 
+def _sample_fill(fill, n_idx, seed, scale, idx):
+    return np.array([fill(1, seed, scale, int(i))[0] for i in idx],
+                    np.float32 if fill is ol.fill_f32 else np.uint16)
+
+
+@pytest.mark.parametrize("variant", sorted(HYPERS))
 @pytest.mark.parametrize("workload", sorted(FULL_SIZE))
-def test_full_size_layout_sampled_parity(cuda_device, workload):
-    """cfg1 / cfg2 / cfg3 at full size on one GPU (cfg3: 49 chunks, 9.9 B
-    params, fp32 master/m/v + bf16 param/grad = 158 GB resident): 2 steps,
-    then sampled elements (head, tail, random) of every chunk are recomputed
-    by the oracle from their global index and must match bit-exactly; the
-    statistics must equal the full-chunk sum of squares within 1e-6 (the
-    oracle's on the host up to 2 B params, torch fp64 on the device above)."""
+def test_full_size_layout_sampled_parity(cuda_device, workload, variant):
+    """cfg1 / cfg2 / cfg3 / flat 512 MiB at full size on one GPU (cfg3: 49
+    chunks, 9.9 B params, fp32 master/m/v + bf16 param/grad = 158 GB
+    resident): 10 steps with FRESH gradients every step (Adam, and AdamW
+    with weight decay 0.01), then sampled elements (head, tail, random) of
+    every chunk are recomputed by the oracle from their global index over the
+    same 10 steps and must match bit-exactly (master, m, v, bf16 param);
+    the last step's statistics must equal the full-chunk sum of squares
+    within 1e-6 (the oracle's on the host up to 2 B params, torch fp64 on the
+    device above); padding elements stay exactly zero."""
     nat, ch = _modules()
-    from paper_2406_08334_b200 import planner
-    layout = planner.layout_for(workload)
-    numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
+    if workload == "flat512":
+        numels = [FULL_SIZE[workload][0]]
+    else:
+        from paper_2406_08334_b200 import planner
+        layout = planner.layout_for(workload)
+        numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
     assert (sum(numels), len(numels)) == FULL_SIZE[workload]
     host_sum = sum(numels) <= 2_000_000_000
     cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device)
     cs.init_synthetic()
-    cs.fill_grads(0)
-    hyper = ch.AdamHyper()
-    cs.step(hyper)
-    cs.step(hyper)
+    hyper = ch.AdamHyper(**HYPERS[variant])
+    for step in range(1, PARITY_STEPS + 1):
+        cs.fill_grads(step - 1)
+        cs.step(hyper)
     torch.cuda.synchronize()
     sumsq, bad = cs.grad_stats()
     assert bad == 0
     rng = np.random.default_rng(0)
     total_sq = 0.0
+    last = PARITY_STEPS - 1
     for ci, n in enumerate(numels):
         c = cs.chunks[ci]
         idx = np.unique(np.concatenate([np.arange(0, 64), np.arange(n - 64, n),
-                                        rng.integers(0, n, 4096 if host_sum else 512)]))
-        mst = np.array([ol.fill_f32(1, ch.master_seed(ci), ch.MASTER_SCALE, int(i))[0]
-                        for i in idx], np.float32)
-        g = np.array([ol.fill_bf16(1, ch.grad_seed(ci, 0, 0), ch.GRAD_SCALE, int(i))[0]
-                      for i in idx], np.uint16)
+                                        rng.integers(0, n, 2048 if host_sum else 256)]))
+        mst = _sample_fill(ol.fill_f32, idx.size, ch.master_seed(ci), ch.MASTER_SCALE, idx)
         m = np.zeros(idx.size, np.float32)
         v = np.zeros(idx.size, np.float32)
         out = np.zeros(idx.size, np.uint16)
-        for step in (1, 2):
-            ol.adam_step(ol.scalars(step=step), mst, m, v, g, out)
+        for step in range(1, PARITY_STEPS + 1):
+            g = _sample_fill(ol.fill_bf16, idx.size, ch.grad_seed(ci, 0, step - 1),
+                             ch.GRAD_SCALE, idx)
+            ol.adam_step(ol.scalars(step=step, **HYPERS[variant]), mst, m, v, g, out)
         ti = torch.from_numpy(idx).to(cuda_device)
         np.testing.assert_array_equal(_bits(c.master[ti]), mst.view(np.uint32))
+        np.testing.assert_array_equal(_bits(c.exp_avg[ti]), m.view(np.uint32))
         np.testing.assert_array_equal(_bits(c.exp_avg_sq[ti]), v.view(np.uint32))
         np.testing.assert_array_equal(_bf16_bits(c.param[ti]), out)
-        # full-chunk grad statistics (the 2nd step's, grads unchanged)
+        # full-chunk grad statistics of the last step
         if host_sum:
-            gf = ol.bf16_to_f32(ol.fill_bf16(n, ch.grad_seed(ci, 0, 0), ch.GRAD_SCALE))
+            gf = ol.bf16_to_f32(ol.fill_bf16(n, ch.grad_seed(ci, 0, last), ch.GRAD_SCALE))
             total_sq += float(np.dot(gf.astype(np.float64), gf.astype(np.float64)))
         else:
             for lo in range(0, n, 1 << 27):

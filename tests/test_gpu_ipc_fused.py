@@ -1,13 +1,16 @@
 """The multi-process fused exchange (ptk_fused_rs_adam_ag over cudaIpc peer
 mappings + ptk_peer_barrier) with REAL separate processes.
 
-The GPU tiers here have one GPU, so both ranks live on cuda:0: each process
-maps the other's gradient / parameter chunks and signal slots through
-cudaIpc handles exactly as on an NVLink node (same code path:
+The GPU tiers here have one GPU, so the `shared` tests put every rank on
+cuda:0: each process maps the other's gradient / parameter chunks and signal
+slots through cudaIpc handles exactly as on an NVLink node (same code path:
 ChunkSet.attach_ipc_peers -> ptk_ipc_open_handle), exchanging the handles
 over a gloo group. Only the wire differs (same-device memory instead of
-NVLink). The results must equal the oracle bit for bit, like the
-virtual-rank test in test_gpu_chunkset.py.
+NVLink). The `spread` tests put rank r on cuda:r -- the real NVLink path,
+both fused kernels (TMA ring and register-staged) -- and run whenever the
+box has enough GPUs (skipped, with the reason, on one-GPU boxes). The
+results must equal the oracle bit for bit, like the virtual-rank test in
+test_gpu_chunkset.py.
 """
 import os
 import socket
@@ -30,13 +33,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, out_dir, max_norm=0.0):
+def _rank_main(rank, world, port, out_dir, max_norm=0.0, spread=False, kernel=""):
     import torch.distributed as dist
     os.environ["PTK_PEER_BARRIER_TIMEOUT_MS"] = "20000"
+    if kernel:
+        os.environ["PTK_FUSED_KERNEL"] = kernel
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     from paper_2406_08334_b200 import chunks as ch
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", rank if spread else 0)
     torch.cuda.set_device(dev)
     cs = ch.ChunkSet(NUMELS, world=world, rank=rank, device=dev, mode="fused")
     cs.init_synthetic()
@@ -64,11 +69,12 @@ def _rank_main(rank, world, port, out_dir, max_norm=0.0):
     dist.destroy_process_group()
 
 
-def _spawn(world, tmp_path, max_norm=0.0):
+def _spawn(world, tmp_path, max_norm=0.0, spread=False, kernel=""):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, str(tmp_path), max_norm))
+    procs = [ctx.Process(target=_rank_main,
+                         args=(r, world, port, str(tmp_path), max_norm, spread, kernel))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -81,11 +87,14 @@ def _spawn(world, tmp_path, max_norm=0.0):
     return [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_fused_exchange_across_processes_bit_exact(cuda_device, world, tmp_path):
+def _need_gpus(n):
+    have = torch.cuda.device_count()
+    if have < n:
+        pytest.skip(f"needs {n} GPUs (NVLink peers), this box has {have}")
+
+
+def _check_fused(res, world):
     from paper_2406_08334_b200 import chunks as ch
-    res = _spawn(world, tmp_path)
-    assert all(str(r["kernel"][0]) == "tma" for r in res)  # same physical GPU -> TMA ring
     for ci, n in enumerate(NUMELS):
         shard = ol.shard_elems(n, world)
         n_pad = shard * world
@@ -112,6 +121,44 @@ def test_fused_exchange_across_processes_bit_exact(cuda_device, world, tmp_path)
             params.append(out)
         gathered = ol.allgather(params)
         for r in range(world):
+            np.testing.assert_array_equal(res[r][f"param{ci}"], gathered)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_across_processes_bit_exact(cuda_device, world, tmp_path):
+    res = _spawn(world, tmp_path)
+    assert all(str(r["kernel"][0]) == "tma" for r in res)  # the default: the TMA ring
+    _check_fused(res, world)
+
+
+@pytest.mark.parametrize("kernel", ["tma", "ldg"])
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_exchange_across_gpus_bit_exact(cuda_device, world, kernel, tmp_path):
+    """Rank r on cuda:r: the fused RS -> Adam -> AG reads every peer's
+    gradient shard and writes every peer's parameter chunk over NVLink (TMA
+    bulk copies or 128-bit loads / stores of peer memory), bit-exact."""
+    _need_gpus(world)
+    res = _spawn(world, tmp_path, spread=True, kernel=kernel)
+    assert all(str(r["kernel"][0]) == kernel for r in res)
+    _check_fused(res, world)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_fused_clipping_across_gpus(cuda_device, world, tmp_path):
+    """Global-norm clipping over NVLink: statistics mailboxes on other GPUs."""
+    _need_gpus(world)
+    max_norm = 0.01
+    res = _spawn(world, tmp_path, max_norm, spread=True)
+    coefs = [tuple(r["coef"].tolist()) for r in res]
+    assert len(set(coefs)) == 1, coefs
+    state, norms = _oracle_clipped(world, max_norm, list(coefs[0]))
+    for dev_c, want in zip(coefs[0], norms):
+        assert want < 1.0 and abs(dev_c - want) <= 1e-6 * want
+    for ci in range(len(NUMELS)):
+        gathered = ol.allgather([state[ci, r][3] for r in range(world)])
+        for r in range(world):
+            np.testing.assert_array_equal(res[r][f"master{ci}"].view(np.uint32),
+                                          state[ci, r][0].view(np.uint32))
             np.testing.assert_array_equal(res[r][f"param{ci}"], gathered)
 
 
