@@ -134,7 +134,7 @@ def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_
             model.chunks.step(hyper, max_grad_norm=max_norm)
         else:
             loss = train_step(model, xs, ys, hyper)
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
     torch.cuda.synchronize()
     out = _state(model, numels)
     out["losses"] = np.array(losses, np.float64)
@@ -182,7 +182,7 @@ def _virtual(tmp_path, dev, world, max_norm):
         for r, m in enumerate(models):
             loss = m.loss(x[r * b:(r + 1) * b], y[r * b:(r + 1) * b])
             loss.backward()
-            losses[r].append(float(loss))
+            losses[r].append(float(loss.detach()))
         fused_group_step(sets, _hyper(), max_grad_norm=max_norm)
     torch.cuda.synchronize()
     res = []
