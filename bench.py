@@ -238,6 +238,17 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t[0])
 
 
+def cuda_alive() -> bool:
+    """False once this process's CUDA context carries a sticky error."""
+    import torch
+    try:
+        torch.cuda.synchronize()
+        return True
+    except Exception:  # noqa: BLE001
+        traceback.print_exc()
+        return False
+
+
 def all_ok(ok: bool, world: int) -> bool:
     if world == 1:
         return ok
@@ -335,18 +346,28 @@ def run_gpu(args):
     results = {}
     for mode in legs:
         err = None
-        try:
-            res = run_leg(args, mode, numels, world, rank, local, dev, hbm_peak, peak_kind)
-        except Exception as e:  # noqa: BLE001  (one failing leg must not lose the line)
-            err = f"{type(e).__name__}: {e}"
-            traceback.print_exc()
-            res = None
+        if world > 1 and mode == "fused":
+            # the peer-memory kernel in a guarded child job (see run_exchange_child)
+            res, err = run_exchange_child(args, world, rank, local, mode)
+        else:
+            try:
+                res = run_leg(args, mode, numels, world, rank, local, dev, hbm_peak, peak_kind)
+            except Exception as e:  # noqa: BLE001  (one failing leg must not lose the line)
+                err = f"{type(e).__name__}: {e}"
+                traceback.print_exc()
+                res = None
         ok = all_ok(err is None, world)
         if ok:
             results[mode] = res
         else:
             results[mode] = {"error": err or "failed on another rank"}
+        if not cuda_alive():
+            # a sticky device error (e.g. a trapped peer barrier) poisons this
+            # context: keep the legs measured so far and touch the GPU no more
+            results[mode]["error"] = (results[mode].get("error") or "") + "; CUDA context lost"
+            break
         torch.cuda.empty_cache()
+    gpu_ok = cuda_alive()
     done = {m: r for m, r in results.items() if "error" not in r}
     if not done:
         raise SystemExit(f"bench.py: every exchange leg failed: {results}")
@@ -354,7 +375,7 @@ def run_gpu(args):
     lead = done[best]
 
     train = train_offload = None
-    if args.train_steps > 0 and args.workload in TRAIN_MODELS:
+    if args.train_steps > 0 and args.workload in TRAIN_MODELS and (gpu_ok or world > 1):
         if world == 1:
             train = run_train(args, world, rank, dev, None)
             if args.offload_persist >= 0:
@@ -369,7 +390,7 @@ def run_gpu(args):
             if args.offload_persist >= 0:
                 train_offload = run_train_child(args, world, rank, local,
                                                 n_persist=args.offload_persist)
-    copy_peak = live_copy_peak()
+    copy_peak = live_copy_peak() if gpu_ok else None
 
     result = None
     cpu = None
@@ -378,7 +399,7 @@ def run_gpu(args):
     barrier(world)
     if rank == 0:
         roof = dict(lead["roofline"], live_copy_gbs_this_box=copy_peak)
-        if roof.get("bound") == "hbm":
+        if roof.get("bound") == "hbm" and copy_peak:
             roof["frac_of_live_copy"] = round(roof["achieved"] / copy_peak, 4)
         result = {
             "metric": METRIC,
@@ -718,24 +739,28 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     return out
 
 
-def run_train_child(args, world, rank, local, n_persist):
-    """The training leg at N > 1 in a child process per rank (its own
-    process group on a fresh port, NCCL communicator, timeout): a failure or
-    hang there is reported in the line instead of losing it."""
+def _run_child(args, world, rank, local, extra, timeout, what, env_extra=None):
+    """Runs this script again as one rank of a child job (its own gloo group
+    on a fresh port, its own CUDA context, a timeout) and returns
+    (result dict or None, error string or None). A failure, hang or device
+    fault inside the child is reported instead of losing the bench line."""
     import torch
     import torch.distributed as dist
     port = torch.tensor([free_port() if rank == 0 else 0], dtype=torch.int64)
     dist.broadcast(port, 0)
-    fd, out_path = tempfile.mkstemp(prefix=f"ptk_train_r{rank}_", suffix=".json")
+    fd, out_path = tempfile.mkstemp(prefix=f"ptk_{what}_r{rank}_", suffix=".json")
     os.close(fd)
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(int(port[0])),
-               RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(local))
-    cmd = [sys.executable, os.path.abspath(__file__)] + sys.argv[1:] + [
-        "--leg", "train", "--leg-out", out_path, "--leg-persist", str(n_persist)]
+    # not torchrun's agent store: the child job rendezvouses on its own port
+    # (with TORCHELASTIC_USE_AGENT_STORE inherited, every child would wait
+    # for a store server that never comes up on that port)
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC_")}
+    env.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(int(port[0])), RANK=str(rank),
+               WORLD_SIZE=str(world), LOCAL_RANK=str(local), **(env_extra or {}))
+    cmd = [sys.executable, os.path.abspath(__file__)] + sys.argv[1:] + extra + ["--leg-out", out_path]
     barrier(world)
     t0 = time.time()
     try:
-        p = subprocess.run(cmd, env=env, timeout=args.train_timeout, stdout=subprocess.DEVNULL)
+        p = subprocess.run(cmd, env=env, timeout=timeout, stdout=subprocess.DEVNULL)
         rc = p.returncode
     except subprocess.TimeoutExpired:
         rc = "timeout"
@@ -749,8 +774,55 @@ def run_train_child(args, world, rank, local, n_persist):
         os.unlink(out_path)
     barrier(world)
     if res is None:
-        return {"error": f"training child exited with {rc} after {time.time() - t0:.0f} s"}
-    return res
+        return None, f"{what} child exited with {rc} after {time.time() - t0:.0f} s"
+    return res, None
+
+
+def run_train_child(args, world, rank, local, n_persist):
+    """The training leg at N > 1 in a child process per rank (NCCL
+    communicator inside the child): a failure or hang there is reported in
+    the line instead of losing it."""
+    res, err = _run_child(args, world, rank, local,
+                          ["--leg", "train", "--leg-persist", str(n_persist)],
+                          args.train_timeout, "train")
+    return res if res is not None else {"error": err}
+
+
+def run_exchange_child(args, world, rank, local, mode):
+    """An exchange leg at N > 1 in a child process per rank. The fused leg
+    runs the TMA-ring kernel first; if that child fails on any rank (a device
+    fault poisons only the child's context), every rank retries with the
+    register-staged kernel (PTK_FUSED_KERNEL=ldg) and the line says so."""
+    res, err = _run_child(args, world, rank, local, ["--leg", "exchange", "--leg-mode", mode],
+                          args.leg_timeout, f"exchange_{mode}")
+    if all_ok(res is not None, world) or mode != "fused" or os.environ.get("PTK_FUSED_KERNEL"):
+        return res, err
+    first = err or "failed on another rank"
+    res, err = _run_child(args, world, rank, local, ["--leg", "exchange", "--leg-mode", mode],
+                          args.leg_timeout, "exchange_fused_ldg", {"PTK_FUSED_KERNEL": "ldg"})
+    if res is not None:
+        res["fallback"] = f"TMA-ring fused kernel failed ({first}); register-staged kernel"
+        return res, None
+    return None, f"{first}; ldg retry: {err}"
+
+
+def run_exchange_leg(args):
+    """--leg exchange: the child of run_exchange_child."""
+    import torch
+    world, rank, local = dist_setup()
+    if args.shared_device:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    numels, _ = chunk_numels(args.workload)
+    hbm_peak, peak_kind = load_peaks()
+    if (os.environ.get("PTK_BENCH_INJECT_FAULT") == "fused-tma"
+            and os.environ.get("PTK_FUSED_KERNEL") != "ldg"):   # test hook of the retry path
+        raise SystemExit("bench.py: injected fault in the TMA-ring fused leg")
+    res = run_leg(args, args.leg_mode, numels, world, rank, local, dev, hbm_peak, peak_kind)
+    with open(args.leg_out, "w") as f:
+        json.dump(res, f)
+    barrier(world)
 
 
 def run_train_leg(args):
@@ -1165,12 +1237,25 @@ def main():
     ap.add_argument("--shared-device", action="store_true",
                     help="validation only: all ranks on cuda:0 (one-GPU box), fused exchange "
                          "over cudaIpc; exercises the N>1 flow, its timings are not a bench value")
-    ap.add_argument("--leg", default=None, choices=[None, "train"], help=argparse.SUPPRESS)
+    ap.add_argument("--leg-timeout", type=int, default=600,
+                    help="N>1: seconds before a fused-exchange child process is killed")
+    ap.add_argument("--leg", default=None, choices=[None, "train", "exchange", "ping"],
+                    help=argparse.SUPPRESS)
+    ap.add_argument("--leg-mode", default="fused", help=argparse.SUPPRESS)
     ap.add_argument("--leg-out", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--leg-persist", type=int, default=-1, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.leg == "train":
         run_train_leg(args)
+        return
+    if args.leg == "exchange":
+        run_exchange_leg(args)
+        return
+    if args.leg == "ping":   # the child-job mechanism alone (CPU test)
+        world, rank, _ = dist_setup()
+        barrier(world)
+        with open(args.leg_out, "w") as f:
+            json.dump({"rank": rank, "world": world}, f)
         return
     world_env = os.environ.get("WORLD_SIZE")
     if world_env is None and args.gpus > 1:

@@ -91,3 +91,27 @@ def test_split_workloads_cover_cfg2():
         assert sum(numels) == bench.CFG2_PARAMS
         assert max(numels) == (mib << 20) // 2
     assert len(bench.chunk_numels("cfg2x32")[0]) == 93
+
+
+def test_child_job_under_torchrun(tmp_path):
+    """The guarded child jobs of the N>1 legs (training, fused exchange):
+    under torchrun each rank starts a child that forms its own group on a
+    fresh port -- not on torchrun's agent store -- and hands back a result."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    env["PROBE_OUT_DIR"] = str(tmp_path)
+    port = _free_port_cpu()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr=127.0.0.1", f"--master-port={port}",
+                        os.path.join(REPO, "tests", "_child_probe.py")],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    got = [json.loads((tmp_path / f"rank{q}.json").read_text()) for q in range(2)]
+    assert [d["res"] for d in got] == [{"rank": 0, "world": 2}, {"rank": 1, "world": 2}], got
+
+
+def _free_port_cpu():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]

@@ -249,3 +249,30 @@ def test_bench_self_launch_shared_device_two_ranks(cuda_device):
     leg = d["exchanges"]["fused"]
     assert leg["consistent_across_ranks"] is True
     assert d["roofline"]["chunks_per_launch"] == 1 and d["e2e"]["value"] > 0
+
+
+def test_bench_fused_leg_retries_with_register_staged_kernel(cuda_device):
+    """At N > 1 the fused exchange runs in a guarded child job; when the
+    TMA-ring child fails (here: an injected fault), every rank retries with
+    the register-staged kernel and the line records the fallback -- a
+    device fault in one kernel cannot lose the N > 1 bench line."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT",
+                        "PTK_FUSED_KERNEL")}
+    env["PTK_PEER_BARRIER_TIMEOUT_MS"] = "20000"
+    env["PTK_BENCH_INJECT_FAULT"] = "fused-tma"
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2",
+                        "--shared-device", "--workload", "flat32", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline", "--no-e2e"], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=repo)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    leg = json.loads(lines[0])["exchanges"]["fused"]
+    assert "TMA-ring fused kernel failed" in leg["fallback"]
+    assert "ldg" in leg["kernel"] or "fused_peer_kernel" in leg["kernel"], leg["kernel"]
+    assert leg["consistent_across_ranks"] is True
