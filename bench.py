@@ -346,8 +346,9 @@ def run_gpu(args):
     results = {}
     for mode in legs:
         err = None
-        if world > 1 and mode == "fused":
-            # the peer-memory kernel in a guarded child job (see run_exchange_child)
+        if world > 1:
+            # N > 1: each exchange in a guarded child job (run_exchange_child),
+            # so a hang or device fault in one leg cannot lose the other
             res, err = run_exchange_child(args, world, rank, local, mode)
         else:
             try:
