@@ -292,6 +292,9 @@ FULL_SIZE = {  # workload -> (parameters, chunks): SURVEY §8(a) golden layouts
     "gpt2-1.5b_b8": (1_557_608_000, 3),
     "gpt2-10b_b8": (9_876_279_296, 49),   # 158 GB of chunk state on one B200
     "flat512": (268_435_456, 1),           # one flat 512 MiB chunk (cfg5's largest point)
+    # maximum size: one chunk of 2^31 + 4101 parameters (element offsets beyond
+    # int32, fp32 state beyond 2^33 bytes, a ragged count padded to 8)
+    "flat_2g": (2_147_487_749, 1),
 }
 PARITY_STEPS = 10  # 10 steps, fresh gradients (seed 1 + rank + step) each step
 HYPERS = {"adam": dict(), "adamw_wd0.01": dict(weight_decay=0.01, adamw=True)}
@@ -305,7 +308,7 @@ def _sample_fill(fill, n_idx, seed, scale, idx):
 @pytest.mark.parametrize("variant", sorted(HYPERS))
 @pytest.mark.parametrize("workload", sorted(FULL_SIZE))
 def test_full_size_layout_sampled_parity(cuda_device, workload, variant):
-    """cfg1 / cfg2 / cfg3 / flat 512 MiB at full size on one GPU (cfg3: 49
+    """cfg1 / cfg2 / cfg3 / flat 512 MiB / one 2^31+ element chunk at full size on one GPU (cfg3: 49
     chunks, 9.9 B params, fp32 master/m/v + bf16 param/grad = 158 GB
     resident): 10 steps with FRESH gradients every step (Adam, and AdamW
     with weight decay 0.01), then sampled elements (head, tail, random) of
@@ -315,7 +318,7 @@ def test_full_size_layout_sampled_parity(cuda_device, workload, variant):
     within 1e-6 (the oracle's on the host up to 2 B params, torch fp64 on the
     device above); padding elements stay exactly zero."""
     nat, ch = _modules()
-    if workload == "flat512":
+    if workload.startswith("flat"):
         numels = [FULL_SIZE[workload][0]]
     else:
         from paper_2406_08334_b200 import planner
