@@ -444,7 +444,9 @@ def run_leg(args, mode, numels, world, rank, local, dev, hbm_peak, peak_kind):
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet
 
     comm = make_comm(world, rank) if (mode == "nccl" and world > 1) else None
-    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode=mode, comm=comm)
+    symmetric = comm is not None and args.nccl_symmetric
+    cs = ChunkSet(numels, world=world, rank=rank, device=dev, mode=mode, comm=comm,
+                  symmetric=symmetric)
     try:
         stream = torch.cuda.current_stream()
         cs.init_synthetic()
@@ -519,6 +521,9 @@ def run_leg(args, mode, numels, world, rank, local, dev, hbm_peak, peak_kind):
                               "scope": "this rank's shards" if world > 1 else "all chunks"},
                "consistent_across_ranks": consistent, "e2e": e2e,
                "kernel": kern["kernel"]}
+        if comm is not None:
+            out["nccl_buffers"] = ("NCCL symmetric windows (ncclMemAlloc + ncclCommWindowRegister)"
+                                   if symmetric else "cudaMalloc (caching allocator)")
         if not consistent:
             raise RuntimeError("gathered parameter chunks differ across ranks")
         return out
@@ -796,7 +801,19 @@ def run_exchange_child(args, world, rank, local, mode):
     register-staged kernel (PTK_FUSED_KERNEL=ldg) and the line says so."""
     res, err = _run_child(args, world, rank, local, ["--leg", "exchange", "--leg-mode", mode],
                           args.leg_timeout, f"exchange_{mode}")
-    if all_ok(res is not None, world) or mode != "fused" or os.environ.get("PTK_FUSED_KERNEL"):
+    if all_ok(res is not None, world):
+        return res, err
+    if mode == "nccl" and args.nccl_symmetric:
+        # symmetric windows need NCCL/driver support: retry on plain buffers
+        first = err or "failed on another rank"
+        res, err = _run_child(args, world, rank, local, ["--leg", "exchange", "--leg-mode", mode,
+                                                         "--no-nccl-symmetric"],
+                              args.leg_timeout, "exchange_nccl_plain")
+        if res is not None:
+            res["fallback"] = f"NCCL symmetric-window leg failed ({first}); plain buffers"
+            return res, None
+        return None, f"{first}; plain-buffer retry: {err}"
+    if mode != "fused" or os.environ.get("PTK_FUSED_KERNEL"):
         return res, err
     first = err or "failed on another rank"
     res, err = _run_child(args, world, rank, local, ["--leg", "exchange", "--leg-mode", mode],
@@ -1238,6 +1255,9 @@ def main():
     ap.add_argument("--shared-device", action="store_true",
                     help="validation only: all ranks on cuda:0 (one-GPU box), fused exchange "
                          "over cudaIpc; exercises the N>1 flow, its timings are not a bench value")
+    ap.add_argument("--nccl-symmetric", action=argparse.BooleanOptionalAction, default=True,
+                    help="N>1 NCCL leg: chunk buffers in NCCL symmetric windows (ncclMemAlloc + "
+                         "ncclCommWindowRegister), retried on plain buffers if that fails")
     ap.add_argument("--leg-timeout", type=int, default=600,
                     help="N>1: seconds before a fused-exchange child process is killed")
     ap.add_argument("--leg", default=None, choices=[None, "train", "exchange", "ping"],

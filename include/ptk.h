@@ -262,6 +262,22 @@ int ptk_comm_wait(ptk_comm* comm, void* stream, int64_t timeout_ms);
 int ptk_comm_async_error(ptk_comm* comm);
 int ptk_comm_abort(ptk_comm* comm);
 
+/* NCCL symmetric memory for the library baseline's chunk buffers. The
+ * NVLink-optimised NCCL kernels for all-gather / reduce-scatter engage when
+ * the send / receive buffers lie in a window registered with
+ * NCCL_WIN_COLL_SYMMETRIC on every rank; such windows must come from
+ * ncclMemAlloc (cuMem, multicast-capable granularity).
+ * ptk_comm_mem_alloc / _free: ncclMemAlloc / ncclMemFree of `bytes`.
+ * ptk_comm_window_register: COLLECTIVE over the communicator (every rank, same
+ * order, same size); *win_out is an opaque handle for _deregister (also
+ * collective). Replaces nothing in the reference (its coll_bw is a modelled
+ * constant, proj/src/hardware.cpp:29-38); it makes the NCCL comparison leg
+ * the strongest NCCL path. */
+int ptk_comm_mem_alloc(void** ptr_out, int64_t bytes);
+int ptk_comm_mem_free(void* ptr);
+int ptk_comm_window_register(ptk_comm* comm, void* buf, int64_t bytes, void** win_out);
+int ptk_comm_window_deregister(ptk_comm* comm, void* win);
+
 /* ---- NVLink peer memory for the fused path ---------------------------- */
 #define PTK_IPC_HANDLE_BYTES 64
 /* Handle of the allocation containing dev_ptr; *offset_out = dev_ptr - base

@@ -117,6 +117,10 @@ _SIGNATURES = {
     "ptk_comm_wait": (c_int32, [c_void_p, c_void_p, c_int64]),
     "ptk_comm_async_error": (c_int32, [c_void_p]),
     "ptk_comm_abort": (c_int32, [c_void_p]),
+    "ptk_comm_mem_alloc": (c_int32, [POINTER(c_void_p), c_int64]),
+    "ptk_comm_mem_free": (c_int32, [c_void_p]),
+    "ptk_comm_window_register": (c_int32, [c_void_p, c_void_p, c_int64, POINTER(c_void_p)]),
+    "ptk_comm_window_deregister": (c_int32, [c_void_p, c_void_p]),
     "ptk_ipc_get_handle": (c_int32, [c_void_p, POINTER(c_uint8), POINTER(c_int64)]),
     "ptk_ipc_open_handle": (c_int32, [POINTER(c_uint8), POINTER(c_void_p)]),
     "ptk_ipc_close_handle": (c_int32, [c_void_p]),

@@ -124,24 +124,49 @@ class ChunkSet:
     per chunk). `comm` is a ptk_comm handle (mode "nccl", world > 1);
     `peers` is a list of per-rank ChunkSets (mode "fused" with virtual ranks
     on one device) or a PeerMap of NVLink-mapped pointers.
+
+    `symmetric=True` (mode "nccl" with a communicator): the bf16 param / grad
+    chunk buffers come from ncclMemAlloc and are registered as NCCL
+    symmetric windows (collective, in chunk order on every rank), so NCCL's
+    all-gather / reduce-scatter run their symmetric-memory NVLink kernels;
+    `close()` deregisters them (collective: call it on every rank).
     """
 
     def __init__(self, chunk_numels, world: int = 1, rank: int = 0, device=None,
-                 mode: str = "nccl", comm=None):
+                 mode: str = "nccl", comm=None, symmetric: bool = False):
         if mode not in ("nccl", "fused"):
             raise ValueError(f"unknown exchange mode {mode!r}")
         if mode == "nccl" and world > 1 and comm is None:
             raise ValueError("world > 1 in nccl mode needs a ptk_comm communicator")
+        if symmetric and (mode != "nccl" or comm is None):
+            raise ValueError("symmetric windows need mode='nccl' and a ptk_comm communicator")
         self.world, self.rank, self.mode, self.comm = world, rank, mode, comm
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.chunks: list[ChunkShard] = []
+        self._nccl_mem: list[ctypes.c_void_p] = []    # ncclMemAlloc'd buffers (symmetric)
+        self._windows: list[ctypes.c_void_p] = []     # their registered windows
+
+        def flat_bf16(n_pad: int) -> torch.Tensor:
+            if not symmetric:
+                return torch.zeros(n_pad, dtype=BF16, device=self.device)
+            ptr = ctypes.c_void_p()
+            with torch.cuda.device(self.device):
+                nat.lib.ptk_comm_mem_alloc(ctypes.byref(ptr), 2 * n_pad)
+                self._nccl_mem.append(ptr)
+                t = _wrap_device(ptr.value, n_pad, self.device).view(BF16)
+                t.zero_()
+                win = ctypes.c_void_p()
+                nat.lib.ptk_comm_window_register(comm, ptr, 2 * n_pad, ctypes.byref(win))
+                self._windows.append(win)
+            return t
+
         for c, n in enumerate(chunk_numels):
             shard = nat.shard_elems(int(n), world)
             n_pad = shard * world
             self.chunks.append(ChunkShard(
                 c, int(n), world, rank, shard,
-                param=torch.zeros(n_pad, dtype=BF16, device=self.device),
-                grad=torch.zeros(n_pad, dtype=BF16, device=self.device),
+                param=flat_bf16(n_pad),
+                grad=flat_bf16(n_pad),
                 master=torch.zeros(shard, dtype=F32, device=self.device),
                 exp_avg=torch.zeros(shard, dtype=F32, device=self.device),
                 exp_avg_sq=torch.zeros(shard, dtype=F32, device=self.device)))
@@ -171,18 +196,31 @@ class ChunkSet:
         with torch.cuda.device(self.device):
             nat.lib.ptk_chunk_table_create(descs, len(self.chunks), ctypes.byref(self.table))
 
-    def close(self) -> None:
-        """Releases the native chunk tables (also done on garbage collection)."""
+    def close(self, collective: bool = True) -> None:
+        """Releases the native chunk tables (also done on garbage collection)
+        and, with `collective` (every rank calls close), the symmetric windows
+        and their ncclMemAlloc buffers. Garbage collection never runs the
+        collective deregistration (ranks collect at different times): an
+        unclosed symmetric set keeps its buffers until the process exits."""
         for name, fn in (("table", "ptk_chunk_table_destroy"),
                          ("fused_table", "ptk_fused_table_destroy")):
             t = getattr(self, name, None)
             if t is not None and t.value:
                 getattr(nat.raw, fn)(t)
             setattr(self, name, None)
+        if collective and getattr(self, "_nccl_mem", None):
+            torch.cuda.synchronize(self.device)
+            for c in self.chunks:   # drop the views before the memory goes
+                c.param = c.grad = None
+            for win in self._windows:
+                nat.lib.ptk_comm_window_deregister(self.comm, win)
+            for ptr in self._nccl_mem:
+                nat.lib.ptk_comm_mem_free(ptr)
+            self._windows, self._nccl_mem = [], []
 
     def __del__(self):
         try:
-            self.close()
+            self.close(collective=False)
         except Exception:  # noqa: BLE001  (interpreter shutdown)
             pass
 
@@ -497,6 +535,19 @@ class ChunkSet:
 
 
 PTK_MAX = nat.PTK_MAX_PEERS
+
+
+class _CudaArray:
+    """A raw device range seen through __cuda_array_interface__ (no ownership)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False),
+                                         "strides": None, "version": 3}
+
+
+def _wrap_device(ptr: int, n: int, device: torch.device) -> torch.Tensor:
+    """int16 tensor view of n elements at device pointer `ptr` (memory owned elsewhere)."""
+    return torch.as_tensor(_CudaArray(ptr, n), device=device)
 
 
 def fused_kernel_choice(same_device: bool) -> int:

@@ -152,6 +152,37 @@ int ptk_comm_wait(ptk_comm* c, void* stream, int64_t timeout_ms) {
   }
 }
 
+int ptk_comm_mem_alloc(void** ptr_out, int64_t bytes) {
+  if (!ptr_out || bytes <= 0) return ptk::fail(PTK_EINVAL, "ptk_comm_mem_alloc: bad arguments");
+  *ptr_out = nullptr;
+  PTK_TRY_NCCL(ncclMemAlloc(ptr_out, static_cast<size_t>(bytes)));
+  return PTK_OK;
+}
+
+int ptk_comm_mem_free(void* ptr) {
+  if (!ptr) return PTK_OK;
+  PTK_TRY_NCCL(ncclMemFree(ptr));
+  return PTK_OK;
+}
+
+int ptk_comm_window_register(ptk_comm* c, void* buf, int64_t bytes, void** win_out) {
+  PTK_TRY_USABLE(c, "ptk_comm_window_register");
+  if (!buf || bytes <= 0 || !win_out)
+    return ptk::fail(PTK_EINVAL, "ptk_comm_window_register: bad arguments");
+  ncclWindow_t win = nullptr;
+  PTK_TRY_NCCL(ncclCommWindowRegister(c->comm, buf, static_cast<size_t>(bytes), &win,
+                                      NCCL_WIN_COLL_SYMMETRIC));
+  *win_out = static_cast<void*>(win);
+  return PTK_OK;
+}
+
+int ptk_comm_window_deregister(ptk_comm* c, void* win) {
+  PTK_TRY_USABLE(c, "ptk_comm_window_deregister");
+  if (!win) return PTK_OK;
+  PTK_TRY_NCCL(ncclCommWindowDeregister(c->comm, static_cast<ncclWindow_t>(win)));
+  return PTK_OK;
+}
+
 int ptk_chunk_allgather(ptk_comm* c, void* buf, int64_t shard_elems, int32_t dtype,
                         void* stream) {
   PTK_TRY_USABLE(c, "ptk_chunk_allgather");

@@ -206,12 +206,17 @@ def _world1_comm(nat):
     return comm
 
 
-@pytest.mark.parametrize("with_comm", [False, True])
-def test_nccl_mode_single_rank_matches_oracle(cuda_device, with_comm):
+@pytest.mark.parametrize("with_comm,symmetric", [(False, False), (True, False), (True, True)])
+def test_nccl_mode_single_rank_matches_oracle(cuda_device, with_comm, symmetric):
+    """symmetric: the chunk buffers are ncclMemAlloc'd and registered as NCCL
+    symmetric windows (the NCCL baseline's strongest path); same bits."""
     nat, ch = _modules()
     numels = [123_457, 65_536]
     comm = _world1_comm(nat) if with_comm else None
-    cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device, mode="nccl", comm=comm)
+    cs = ch.ChunkSet(numels, world=1, rank=0, device=cuda_device, mode="nccl", comm=comm,
+                     symmetric=symmetric)
+    if symmetric:
+        assert len(cs._windows) == 2 * len(numels)
     cs.init_synthetic()
     cs.fill_grads(0)
     hyper = ch.AdamHyper()
@@ -238,6 +243,8 @@ def test_nccl_mode_single_rank_matches_oracle(cuda_device, with_comm):
         assert cs.grad_stats()[1] == 0
         nat.lib.ptk_comm_barrier(comm, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         torch.cuda.synchronize()
+        cs.close()   # deregisters the symmetric windows (collective) before the comm goes
+        assert cs._windows == []
         nat.lib.ptk_comm_destroy(comm)
 
 

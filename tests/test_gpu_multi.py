@@ -44,7 +44,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _nccl_rank(rank, world, port, out_dir):
+def _nccl_rank(rank, world, port, out_dir, symmetric=False):
     import torch.distributed as dist
     sys.path.insert(0, REPO)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
@@ -61,7 +61,8 @@ def _nccl_rank(rank, world, port, out_dir):
     uid = (ctypes.c_uint8 * nat.PTK_UNIQUE_ID_BYTES)(*t.tolist())
     comm = ctypes.c_void_p()
     nat.lib.ptk_comm_init(ctypes.byref(comm), world, rank, uid)
-    cs = ch.ChunkSet(NUMELS, world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    cs = ch.ChunkSet(NUMELS, world=world, rank=rank, device=dev, mode="nccl", comm=comm,
+                     symmetric=symmetric)
     cs.init_synthetic()
     hyper = ch.AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True)
     s = torch.cuda.current_stream()
@@ -79,15 +80,16 @@ def _nccl_rank(rank, world, port, out_dir):
         out[f"param{c.chunk_id}"] = c.param.view(torch.int16).cpu().numpy().view(np.uint16)
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **out)
     dist.barrier()
+    cs.close()   # collective: symmetric windows are deregistered on every rank
     nat.lib.ptk_comm_destroy(comm)
     dist.destroy_process_group()
 
 
-def _spawn(world, tmp_path):
+def _spawn(world, tmp_path, symmetric=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_nccl_rank, args=(r, world, port, str(tmp_path)))
+    procs = [ctx.Process(target=_nccl_rank, args=(r, world, port, str(tmp_path), symmetric))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -100,11 +102,14 @@ def _spawn(world, tmp_path):
     return [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
 
 
+@pytest.mark.parametrize("symmetric", [False, True])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_nccl_rs_adam_ag_across_gpus(cuda_device, world, tmp_path):
+def test_nccl_rs_adam_ag_across_gpus(cuda_device, world, symmetric, tmp_path):
+    """symmetric: chunk buffers in NCCL symmetric windows (ncclMemAlloc +
+    ncclCommWindowRegister), the same stated bound."""
     from paper_2406_08334_b200 import chunks as ch
     _need_gpus(world)
-    res = _spawn(world, tmp_path)
+    res = _spawn(world, tmp_path, symmetric)
     for ci, n in enumerate(NUMELS):
         shard = ol.shard_elems(n, world)
         n_pad = shard * world
