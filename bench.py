@@ -862,6 +862,33 @@ def run_train_leg(args):
         nat.lib.ptk_comm_destroy(comm)
 
 
+def e2e_pieces(n: int, piece: int, ramp_up: bool, ramp_down: bool, first: int = 1 << 20):
+    """(offset, length) pieces covering [0, n): `piece`-sized in the middle,
+    doubling from `first` at the start (ramp_up) and halving to `first` at
+    the end (ramp_down). Every boundary is a multiple of 8 elements."""
+    ramp = []
+    k = first
+    while k < piece:
+        ramp.append(k)
+        k *= 2
+    head = ramp if ramp_up else []
+    tail = ramp[::-1] if ramp_down else []
+    if sum(head) + sum(tail) >= n:   # too small to ramp: plain pieces
+        head, tail = [], []
+    sizes = list(head)
+    mid = n - sum(head) - sum(tail)
+    sizes += [piece] * (mid // piece)
+    if mid % piece:
+        sizes.append(mid % piece)
+    sizes += tail
+    out, lo = [], 0
+    for m in sizes:
+        out.append((lo, m))
+        lo += m
+    assert lo == n
+    return out
+
+
 def run_e2e(cs, hyper, args, world, numels, comm):
     """Same step through the C-ABI with HOST buffers: per chunk piece, pinned
     H2D of the gradients (h2d stream) -> fused Adam (compute stream) -> pinned
@@ -928,12 +955,16 @@ def run_e2e(cs, hyper, args, world, numels, comm):
         cs.step_count += 1
         cfg = hyper.config(cs.step_count, world)
         nat.lib.ptk_stats_reset(vp(cs.stats), sc)
+        last = len(cs.chunks) - 1
         for c, hg, hp in zip(cs.chunks, host_g, host_p):
             # at least ~8 pieces per chunk so copies overlap the update even
-            # for small chunks (multiple of 12288 elements: whole TMA tiles)
+            # for small chunks (multiple of 12288 elements: whole TMA tiles);
+            # the step's first pieces grow and its last ones shrink
+            # geometrically, so the pipeline fill (first H2D) and drain (last
+            # D2H) cost one small piece instead of one full piece each
             pc = min(piece, max(1 << 20, -(-c.shard // 8 // 12288) * 12288))
-            for lo in range(0, c.shard, pc):
-                n = min(pc, c.shard - lo)
+            for lo, n in e2e_pieces(c.shard, pc, ramp_up=c.chunk_id == 0,
+                                    ramp_down=c.chunk_id == last):
                 g_dev = c.grad_shard()[lo:lo + n]
                 p_dev = c.param_shard()[lo:lo + n]
                 e_in, e_up = torch.cuda.Event(), torch.cuda.Event()

@@ -115,3 +115,18 @@ def _free_port_cpu():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("n,piece,up,down", [(512_420_800, 1 << 25, True, True),
+                                             (522_593_600, 1 << 25, False, True),
+                                             (1 << 21, 1 << 25, True, True),
+                                             (3 << 20, 1 << 20, True, False)])
+def test_e2e_pieces_cover_the_chunk(n, piece, up, down):
+    got = bench.e2e_pieces(n, piece, up, down)
+    assert got[0][0] == 0 and sum(m for _, m in got) == n
+    assert all(lo % 8 == 0 for lo, _ in got)
+    assert all(a[0] + a[1] == b[0] for a, b in zip(got, got[1:]))
+    if up and n > 4 * piece:
+        assert got[0][1] == 1 << 20
+    if down and n > 4 * piece:
+        assert got[-1][1] == 1 << 20
