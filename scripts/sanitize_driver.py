@@ -2,8 +2,11 @@
 """Launch every libptk kernel once at small, ragged sizes (for
 compute-sanitizer racecheck / synccheck / initcheck, scripts/sanitize.sh):
 each chunk-Adam shape (TMA ring variants incl. the partial last tile, LDG),
-the f32-grad variant, grad stats / prep, clip coefficient, the fused
-RS->Adam->AG kernel (TMA ring) over 2, 4 and 8 virtual ranks, the peer barrier, fills."""
+the f32-grad variant, grad stats / prep, clip coefficient, the chunk-TABLE
+launch (dynamic tile scheduler, several ragged chunks, back-to-back launches
+re-arming the scheduler), the fused RS->Adam->AG kernel (TMA ring and
+register-staged) over 2, 4 and 8 virtual ranks, the clipped fused step
+(statistics pass, mailbox publish / collect), the peer barrier, fills."""
 import ctypes
 import os
 import sys
@@ -19,7 +22,7 @@ def main():
     from paper_2406_08334_b200.chunks import AdamHyper, ChunkSet, vp
     dev = torch.device("cuda", 0)
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    n = 3 * 148 * 1536 + 777          # several tiles per CTA plus a partial tile
+    n = 3 * 148 * 2048 + 777          # several tiles per CTA plus a partial tile
     master = torch.empty(n, dtype=torch.float32, device=dev)
     m = torch.zeros_like(master)
     v = torch.zeros_like(master)
@@ -65,6 +68,40 @@ def main():
         for cs in sets_w:
             cs.step(AdamHyper(lr=1e-3))
     print("fused kernel in use:", nat.raw.ptk_fused_kernel_name().decode())
+
+    # chunk-table launch: ragged chunks, tiles claimed dynamically, 3 launches
+    # back to back (the last CTA re-arms the scheduler for the next launch)
+    cs_t = ChunkSet([2048 * 150 + 8, 5000, 8, 2048 * 300 + 4096], device=dev)
+    cs_t.init_synthetic()
+    cs_t.fill_grads(0)
+    for _ in range(3):
+        cs_t.step(AdamHyper(lr=1e-3, weight_decay=0.01, adamw=True))
+    cs_t.step(AdamHyper(lr=1e-3), max_grad_norm=0.5, skip_nonfinite=True)
+
+    # clipped fused step over virtual ranks: statistics pass, mailboxes, update
+    from paper_2406_08334_b200.chunks import fused_group_step
+    for w in (2, 4):
+        sets_c = [ChunkSet([w * 2048 * 7 + 8 * w * 3, 4096], world=w, rank=r, device=dev,
+                           mode="fused") for r in range(w)]
+        for cs in sets_c:
+            cs.init_synthetic()
+            cs.fill_grads(0)
+            cs.attach_virtual_peers(sets_c)
+        fused_group_step(sets_c, AdamHyper(lr=1e-3), max_grad_norm=0.01, skip_nonfinite=True)
+        fused_group_step(sets_c, AdamHyper(lr=1e-3))
+
+    # the register-staged fused kernel
+    os.environ["PTK_FUSED_KERNEL"] = "ldg"
+    sets_l = [ChunkSet([3 * 8 * 148 * 256 + 24], world=3, rank=r, device=dev, mode="fused")
+              for r in range(3)]
+    for cs in sets_l:
+        cs.init_synthetic()
+        cs.fill_grads(0)
+        cs.attach_virtual_peers(sets_l)
+    assert sets_l[0].fused_kernel == "ldg"
+    for cs in sets_l:
+        cs.step(AdamHyper(lr=1e-3))
+    os.environ.pop("PTK_FUSED_KERNEL")
     sig = torch.zeros(nat.PTK_MAX_PEERS, dtype=torch.int32, device=dev)
     arr = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(sig.data_ptr())
     nat.lib.ptk_peer_barrier(arr, 1, 0, 1, s)
