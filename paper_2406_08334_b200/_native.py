@@ -173,6 +173,13 @@ if not os.path.exists(LIB_PATH):
         f"libptk.so not found at {LIB_PATH}: build it with `make ptk` (or "
         "`python -c 'import __graft_entry__ as g; g.build()'`). There is no fallback path.")
 
+# libptk.so and torch both need `libnccl.so.2`; whichever loads first binds
+# the soname for the process. torch's bundled NCCL (2.28) is a superset of the
+# system one (2.27) that libptk was linked against, so torch goes first: with
+# libptk first, importing torch later fails (libtorch_cuda: undefined symbol
+# ncclDevCommCreate).
+import torch  # noqa: E402,F401
+
 _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
 for _name, (_res, _args) in _SIGNATURES.items():
     _fn = getattr(_lib, _name)

@@ -124,3 +124,19 @@ def test_host_profile_probe_and_argument_checks():
     assert nat.raw.ptk_profile_cpu_adam_rate(0, ctypes.byref(rate)) != nat.PTK_OK
     assert "ptk_profile_cpu_adam_rate" in nat.last_error()
     assert nat.raw.ptk_profile_collective(None, 2, 1 << 20, None, None) != nat.PTK_OK
+
+
+def test_planner_first_then_torch_in_a_fresh_process():
+    """The first thing a process touches may be the planner (libptk.so) and
+    only later torch: torch's NCCL must still be the one the process binds
+    (a regression of the reference arm: `import torch` after libptk failed
+    with `undefined symbol: ncclDevCommCreate`)."""
+    import subprocess
+    import sys
+    code = ("from paper_2406_08334_b200 import planner\n"
+            "planner.layout_for('gpt2-1b_b2')\n"
+            "import torch, torch.distributed\n"
+            "print(torch.zeros(2).sum().item())\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=REPO,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
