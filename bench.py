@@ -1271,7 +1271,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
-    ap.add_argument("--train-timeout", type=int, default=900,
+    ap.add_argument("--train-timeout", type=int, default=400,
                     help="N>1: seconds before a training child process is killed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train-graph", action=argparse.BooleanOptionalAction, default=True,
