@@ -766,7 +766,9 @@ def _run_child(args, world, rank, local, extra, timeout, what, env_extra=None):
     barrier(world)
     t0 = time.time()
     try:
-        p = subprocess.run(cmd, env=env, timeout=timeout, stdout=subprocess.DEVNULL)
+        # the child's stdout (NCCL_DEBUG=INFO init lines: "comm ... nRanks N") goes to
+        # this rank's stderr: visible to the driver, never mixed into the JSON line
+        p = subprocess.run(cmd, env=env, timeout=timeout, stdout=sys.stderr.fileno())
         rc = p.returncode
     except subprocess.TimeoutExpired:
         rc = "timeout"
