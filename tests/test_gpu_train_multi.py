@@ -2,7 +2,7 @@
 chunk shards), each rank on its slice of one global batch, the
 gradient exchange inside the training step.
 
-* fused exchange, two PROCESSES on one GPU (runs on every box): each rank's
+* fused exchange, two or four PROCESSES on one GPU (runs on every box): each rank's
   parameters are views of its own chunk buffers; after the backward, the
   fused RS -> Adam -> AG kernel reads every rank's gradient chunk and writes
   every rank's parameter chunk through cudaIpc mappings (the NVLink code path
@@ -216,9 +216,8 @@ def _follows_w1(res, w1):
     assert mean[-1] < mean[0]
 
 
-@pytest.mark.parametrize("max_norm", [0.0, 0.05])
-def test_fused_training_two_processes_equals_virtual_ranks(tmp_path, cuda_device, max_norm):
-    world = 2
+@pytest.mark.parametrize("world,max_norm", [(2, 0.0), (2, 0.05), (4, 0.0)])
+def test_fused_training_processes_equal_virtual_ranks(tmp_path, cuda_device, world, max_norm):
     res = _spawn(world, tmp_path, "fused", max_norm=max_norm)
     ref = _virtual(tmp_path, cuda_device, world, max_norm)
     for r in range(world):
@@ -227,9 +226,10 @@ def test_fused_training_two_processes_equals_virtual_ranks(tmp_path, cuda_device
     _replicas_identical(res)
     if max_norm > 0:
         assert res[0]["coef"][0] < 1.0   # the clip engaged (same coefficient on every rank)
-        assert res[0]["coef"][0] == res[1]["coef"][0]
+        assert all(r["coef"][0] == res[0]["coef"][0] for r in res)
     else:
         _follows_w1(res, _w1_losses(tmp_path, cuda_device))
+        assert res[0]["losses"].size == STEPS
 
 
 def test_nccl_training_across_gpus(tmp_path, cuda_device):
