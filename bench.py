@@ -337,7 +337,8 @@ def run_gpu(args):
         # so only the fused exchange runs and the timings are not a bench value
         legs = ["fused"]
         local = 0
-        args.train_steps = 0
+        args.offload_persist = -1   # the pool's exchange is NCCL
+        args.train_exchange = "fused"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     numels, desc = chunk_numels(args.workload)
@@ -679,12 +680,19 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     layout = planner.layout_for(name)
     numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
     np_ = len(numels) if n_persist is None else n_persist
-    cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode="nccl", comm=comm)
+    # N > 1, every chunk persistent: the fused RS->Adam->AG kernel over NVLink
+    # peer memory is the training step's exchange (--train-exchange nccl: the
+    # library path); non-persistent chunks (ChunkPool) exchange through NCCL
+    mode = train_exchange_mode(args, world, np_ == len(numels))
+    cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode=mode,
+                  comm=comm if mode == "nccl" else None)
     pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev)
             if np_ < len(numels) else None)
     shape = GPT2Shape.from_trace(trace)
     model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(seed=0)
+    if mode == "fused":
+        cs.attach_ipc_peers()
     batch = int(trace["meta"]["batch_size"])
     n_iter = args.warmup + args.train_steps
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -694,7 +702,7 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     hyper = AdamHyper(lr=1e-4, weight_decay=0.01, adamw=True)
     stream = torch.cuda.current_stream()
     losses = []
-    overlap = args.train_overlap
+    overlap = args.train_overlap and mode == "nccl"
     graphed = None
     if args.train_graph and pool is None:
         from paper_2406_08334_b200.train import GraphedTrainStep
@@ -733,16 +741,28 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
                                 else "host-launched"),
            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
     if world > 1:
-        out["exchange"] = "NCCL RS / AG per chunk (ChunkSet nccl mode, ChunkPool)"
+        out["exchange"] = ("fused RS->Adam->AG table kernel over NVLink peer memory"
+                           if mode == "fused" else
+                           "NCCL RS / AG per chunk (ChunkSet nccl mode, ChunkPool)")
     if pool is not None:
         out["offload"] = {"pinned_host_GB": round(pool.host_bytes / 1e9, 3),
                           "buffer_GB": round(pool.device_bytes / 1e9, 3),
                           "fetches": pool.counters["fetch"], "evictions": pool.counters["evict"],
                           "h2d_GB": round(pool.counters["h2d_bytes"] / 1e9, 2),
                           "d2h_GB": round(pool.counters["d2h_bytes"] / 1e9, 2)}
+    if mode == "fused":
+        torch.cuda.synchronize()
+        barrier(world)   # no rank unmaps while a peer may still store into it
+        cs.close_ipc_peers()
     del model, cs, pool
     torch.cuda.empty_cache()
     return out
+
+
+def train_exchange_mode(args, world, all_persistent) -> str:
+    if world > 1 and all_persistent and args.train_exchange == "fused":
+        return "fused"
+    return "nccl"
 
 
 def _run_child(args, world, rank, local, extra, timeout, what, env_extra=None):
@@ -787,13 +807,21 @@ def _run_child(args, world, rank, local, extra, timeout, what, env_extra=None):
 
 
 def run_train_child(args, world, rank, local, n_persist):
-    """The training leg at N > 1 in a child process per rank (NCCL
-    communicator inside the child): a failure or hang there is reported in
-    the line instead of losing it."""
-    res, err = _run_child(args, world, rank, local,
-                          ["--leg", "train", "--leg-persist", str(n_persist)],
-                          args.train_timeout, "train")
-    return res if res is not None else {"error": err}
+    """The training leg at N > 1 in a child process per rank: a failure or
+    hang there is reported in the line instead of losing it. All-persistent
+    training runs the fused exchange first and, if that child fails on any
+    rank, is retried with NCCL (the line says so)."""
+    extra = ["--leg", "train", "--leg-persist", str(n_persist)]
+    res, err = _run_child(args, world, rank, local, extra, args.train_timeout, "train")
+    fused_first = train_exchange_mode(args, world, n_persist < 0) == "fused"
+    if all_ok(res is not None, world) or not fused_first or args.shared_device:
+        return res if res is not None else {"error": err}
+    res, err2 = _run_child(args, world, rank, local, extra + ["--train-exchange", "nccl"],
+                           args.train_timeout, "train_nccl")
+    if res is not None:
+        res["fallback"] = f"fused-exchange training failed ({err}); NCCL"
+        return res
+    return {"error": f"{err}; NCCL retry: {err2}"}
 
 
 def run_exchange_child(args, world, rank, local, mode):
@@ -849,10 +877,13 @@ def run_train_leg(args):
     """--leg train: the child of run_train_child."""
     import torch
     world, rank, local = dist_setup()
+    if args.shared_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    comm = make_comm(world, rank)
     n_persist = None if args.leg_persist < 0 else args.leg_persist
+    fused = train_exchange_mode(args, world, n_persist is None) == "fused"
+    comm = None if fused else make_comm(world, rank)
     res = run_train(args, world, rank, dev, comm, n_persist=n_persist,
                     n_buffer=args.offload_buffers if n_persist is not None else 0)
     torch.cuda.synchronize()
@@ -1275,6 +1306,9 @@ def main():
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
     ap.add_argument("--train-timeout", type=int, default=400,
                     help="N>1: seconds before a training child process is killed")
+    ap.add_argument("--train-exchange", default="fused", choices=["fused", "nccl"],
+                    help="N>1 all-persistent training: the fused RS->Adam->AG kernel over NVLink "
+                         "peer memory (default, NCCL retry on failure) or NCCL RS/AG")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train-graph", action=argparse.BooleanOptionalAction, default=True,
                     help="training (all chunks persistent): forward + backward as one CUDA-graph "
