@@ -286,8 +286,8 @@ def main():
     ap.add_argument("--model", default="llama-13b")
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--profile-blocks", type=int, default=4)
-    ap.add_argument("--iters", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--host-frac", type=float, default=0.7,
                     help="refuse a plan whose pinned host bytes exceed this fraction of the "
                          "host memory available now (protects the box)")

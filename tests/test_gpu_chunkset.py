@@ -377,6 +377,64 @@ def test_full_size_layout_sampled_parity(cuda_device, workload, variant):
     assert abs(sumsq - total_sq) <= 1e-6 * total_sq
 
 
+@pytest.mark.parametrize("variant", sorted(HYPERS))
+@pytest.mark.parametrize("world", [2, 8])
+def test_full_size_fused_virtual_ranks_sampled_parity(cuda_device, world, variant):
+    """cfg2 (GPT-2 1.5B, 3 x 1 GiB chunks) at full size through the fused
+    RS -> Adam -> AG exchange over W virtual ranks on this device (W = 8:
+    8 ranks' bf16 param + grad chunks and the sharded fp32 state, 68 GB):
+    10 steps with FRESH gradients on every rank every step (Adam, and AdamW
+    with weight decay 0.01); then sampled elements (head, tail, every shard
+    boundary, random) are recomputed by the oracle from their global index
+    -- rank-order fp32 sum of the W ranks' bf16 gradients, Adam with grad
+    scale 1/W -- and must match bit-exactly in the owner's master / m / v
+    and in EVERY rank's gathered bf16 chunk."""
+    nat, ch = _modules()
+    from paper_2406_08334_b200 import planner
+    layout = planner.layout_for("gpt2-1.5b_b8")
+    numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
+    sets = [ch.ChunkSet(numels, world=world, rank=r, device=cuda_device, mode="fused")
+            for r in range(world)]
+    for cs in sets:
+        cs.init_synthetic()
+        cs.attach_virtual_peers(sets)
+    hyper = ch.AdamHyper(**HYPERS[variant])
+    for step in range(1, PARITY_STEPS + 1):
+        for cs in sets:
+            cs.fill_grads(step - 1)
+        ch.fused_group_step(sets, hyper)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    for ci, n in enumerate(numels):
+        shard = sets[0].chunks[ci].shard
+        bounds = np.concatenate([np.arange(r * shard - 4, r * shard + 4) for r in range(1, world)])
+        idx = np.unique(np.concatenate([np.arange(0, 32), np.arange(n - 32, n), bounds,
+                                        rng.integers(0, n, 384)]))
+        mst = _sample_fill(ol.fill_f32, idx.size, ch.master_seed(ci), ch.MASTER_SCALE, idx)
+        m = np.zeros(idx.size, np.float32)
+        v = np.zeros(idx.size, np.float32)
+        out = np.zeros(idx.size, np.uint16)
+        for step in range(1, PARITY_STEPS + 1):
+            grads = [_sample_fill(ol.fill_bf16, idx.size, ch.grad_seed(ci, q, step - 1),
+                                  ch.GRAD_SCALE, idx) for q in range(world)]
+            red = ol.reduce_scatter(grads, 0, idx.size, fp32=True)   # rank-order fp32 sum
+            ol.adam_step(ol.scalars(step=step, grad_scale=1.0 / world, **HYPERS[variant]),
+                         mst, m, v, red, out)
+        owner = idx // shard
+        for r in range(world):
+            mine = owner == r
+            if mine.any():
+                c = sets[r].chunks[ci]
+                ti = torch.from_numpy(idx[mine] - r * shard).to(cuda_device)
+                np.testing.assert_array_equal(_bits(c.master[ti]), mst[mine].view(np.uint32))
+                np.testing.assert_array_equal(_bits(c.exp_avg[ti]), m[mine].view(np.uint32))
+                np.testing.assert_array_equal(_bits(c.exp_avg_sq[ti]), v[mine].view(np.uint32))
+            tg = torch.from_numpy(idx).to(cuda_device)
+            np.testing.assert_array_equal(_bf16_bits(sets[r].chunks[ci].param[tg]), out)
+    for cs in sets:
+        cs.close()
+
+
 def test_global_norm_clipping_matches_oracle(cuda_device):
     """max_grad_norm: global norm over all chunks -> device clip coefficient ->
     every chunk's Adam reads it from device memory. Checked against the
