@@ -296,6 +296,25 @@ int ptk_ipc_close_handle(void* dev_ptr);
 int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank,
                      int32_t epoch, void* stream);
 
+/* ---- K3 / K4 over peer memory for NON-persistent chunks --------------
+ * The offload path's exchange without a library collective (the gather
+ * before a block's use and the reduce after its backward, proj/src/
+ * sim.cpp:335-350,426-436; modelled as gather_time / reduce_time,
+ * proj/src/hardware.cpp:29-38). Both are collective over the ranks and are
+ * bracketed by ptk_peer_barrier on the calling stream (one signal array per
+ * stream that issues them).
+ * ptk_peer_reduce_scatter_f32: out[i] = sum over r = 0..world-1, in that
+ *   order, of bf16 grad_peers[r][rank * shard + i] in fp32 (shard elements,
+ *   16-byte aligned): the same sum ptk_fused_step_table feeds its Adam, kept
+ *   in fp32 for the host Adam (ptk_cpu_adam_f32grad).
+ * ptk_peer_allgather: for every q != rank, copies bytes
+ *   [q * shard_bytes, (q+1) * shard_bytes) of buf_peers[q] to the same range
+ *   of buf_peers[rank] (copy-engine peer transfers over NVLink on `stream`). */
+int ptk_peer_reduce_scatter_f32(const uint16_t* const* grad_peers, int32_t world, int32_t rank,
+                                int64_t shard, float* out, void* stream);
+int ptk_peer_allgather(void* const* buf_peers, int32_t world, int32_t rank, int64_t shard_bytes,
+                       void* stream);
+
 /* ---- K5: pinned host <-> device chunk copies on side streams ---------- */
 int ptk_host_alloc_pinned(void** out, size_t bytes);
 int ptk_host_free_pinned(void* ptr);
@@ -310,6 +329,11 @@ int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
                  float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
                  int64_t n, int32_t n_threads, double* sumsq_out,
                  int64_t* nonfinite_out);
+/* fp32 gradients (a reduce-scattered sum kept in fp32, ptk_peer_reduce_scatter_f32) */
+int ptk_cpu_adam_f32grad(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                         float* exp_avg_sq, const float* grad, uint16_t* param_out,
+                         int64_t n, int32_t n_threads, double* sumsq_out,
+                         int64_t* nonfinite_out);
 
 /* ---- the chunk runtime (memplan::execute) and the profiler re-feed ----- */
 /* Executes `iterations` iterations of a plan (plan JSON as written by

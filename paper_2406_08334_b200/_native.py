@@ -131,6 +131,12 @@ _SIGNATURES = {
     "ptk_memcpy_d2h_async": (c_int32, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "ptk_cpu_adam": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p, c_int64, c_int32, POINTER(c_double), POINTER(c_int64)]),
+    "ptk_cpu_adam_f32grad": (c_int32, [POINTER(AdamConfig), c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_int64, c_int32, POINTER(c_double),
+                                       POINTER(c_int64)]),
+    "ptk_peer_reduce_scatter_f32": (c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int64,
+                                              c_void_p, c_void_p]),
+    "ptk_peer_allgather": (c_int32, [POINTER(c_void_p), c_int32, c_int32, c_int64, c_void_p]),
     "ptk_execute_plan": (c_int32, [c_char_p, c_char_p, c_char_p, c_void_p, c_int32, c_double,
                                    c_int32, c_char_p, c_char_p]),
     "ptk_measure_profile": (c_int32, [c_char_p, c_void_p, c_int32, c_char_p]),

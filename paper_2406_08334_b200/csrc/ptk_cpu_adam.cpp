@@ -34,15 +34,19 @@ inline uint16_t f32_to_bf16(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+inline float grad_f32(uint16_t g) { return bf16_to_f32(g); }
+inline float grad_f32(float g) { return g; }
+
 // The element loop, branch-free inside so it vectorises (IEEE vdivps /
-// vsqrtps keep it bit-exact with the GPU rule; no FMA contraction).
-template <bool kL2, bool kDecay, bool kOut>
+// vsqrtps keep it bit-exact with the GPU rule; no FMA contraction). G is the
+// gradient type: bf16 bits, or fp32 (a reduce-scattered sum kept in fp32).
+template <bool kL2, bool kDecay, bool kOut, class G>
 inline __attribute__((always_inline)) void update_run(const ptk_adam_scalars& s, float* __restrict__ pm,
                                                        float* __restrict__ mm, float* __restrict__ vm,
-                                                       const uint16_t* __restrict__ gr,
+                                                       const G* __restrict__ gr,
                                                        uint16_t* __restrict__ out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) {
-    float g = bf16_to_f32(gr[i]) * s.gscale;
+    float g = grad_f32(gr[i]) * s.gscale;
     float p = pm[i];
     if (kL2) g = g + s.wd * p;
     if (kDecay) p = p * s.decay;
@@ -61,8 +65,9 @@ inline __attribute__((always_inline)) void update_run(const ptk_adam_scalars& s,
 
 // One block of the shard, compiled for AVX-512, AVX2 and baseline x86-64
 // (resolved once at load time), so the library runs on any host CPU.
-__attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
-    const ptk_adam_scalars& s, float* pm, float* mm, float* vm, const uint16_t* gr, uint16_t* out,
+template <class G>
+inline __attribute__((always_inline)) void update_block_body(
+    const ptk_adam_scalars& s, float* pm, float* mm, float* vm, const G* gr, uint16_t* out,
     int64_t n) {
   const bool l2 = s.wd != 0.0f, decay = s.adamw != 0, has_out = out != nullptr;
   if (l2) {
@@ -77,16 +82,38 @@ __attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
   }
 }
 
+__attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
+    const ptk_adam_scalars& s, float* pm, float* mm, float* vm, const uint16_t* gr, uint16_t* out,
+    int64_t n) {
+  update_block_body(s, pm, mm, vm, gr, out, n);
+}
+
+__attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
+    const ptk_adam_scalars& s, float* pm, float* mm, float* vm, const float* gr, uint16_t* out,
+    int64_t n) {
+  update_block_body(s, pm, mm, vm, gr, out, n);
+}
+
 // AVX-512 variant with the bf16 parameter output written by non-temporal
 // stores: the output is write-only, so streaming it saves the read-for-
 // ownership of its cache lines (2 of ~30 host DRAM bytes per parameter --
 // host DRAM is what the offloaded iteration is bound by). The arithmetic is
 // the same sequence of IEEE single operations as update_run (no FMA), so the
 // result is bit-identical; the rounding to bf16 is f32_to_bf16's.
-template <bool kL2, bool kDecay>
+template <class G>
+__attribute__((target("avx512f,avx512bw"))) inline __m512 load_grad16(const G* gr) {
+  if constexpr (sizeof(G) == 2) {
+    const __m256i gb = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(gr));
+    return _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(gb), 16));
+  } else {
+    return _mm512_loadu_ps(reinterpret_cast<const float*>(gr));
+  }
+}
+
+template <bool kL2, bool kDecay, class G>
 __attribute__((target("avx512f,avx512bw"))) void update_run_nt(
     const ptk_adam_scalars& s, float* __restrict__ pm, float* __restrict__ mm,
-    float* __restrict__ vm, const uint16_t* __restrict__ gr, uint16_t* __restrict__ out,
+    float* __restrict__ vm, const G* __restrict__ gr, uint16_t* __restrict__ out,
     int64_t n) {
   int64_t i = 0;
   // scalar head until the output is 32-byte aligned (stream stores need it)
@@ -103,9 +130,7 @@ __attribute__((target("avx512f,avx512bw"))) void update_run_nt(
                 round = _mm512_set1_epi32(0x7fff), one = _mm512_set1_epi32(1),
                 qnan = _mm512_set1_epi32(0x7fff);
   for (; i + 16 <= n; i += 16) {
-    const __m256i gb = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(gr + i));
-    __m512 g = _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(gb), 16));
-    g = _mm512_mul_ps(g, gscale);
+    __m512 g = _mm512_mul_ps(load_grad16(gr + i), gscale);
     __m512 p = _mm512_loadu_ps(pm + i);
     if (kL2) g = _mm512_add_ps(g, _mm512_mul_ps(wd, p));
     if (kDecay) p = _mm512_mul_ps(p, decay);
@@ -140,8 +165,9 @@ bool use_nt_path() {
   return ok;
 }
 
+template <class G>
 void update_block_dispatch(const ptk_adam_scalars& s, float* pm, float* mm, float* vm,
-                           const uint16_t* gr, uint16_t* out, int64_t n) {
+                           const G* gr, uint16_t* out, int64_t n) {
   if (out != nullptr && use_nt_path()) {
     if (s.wd != 0.0f) update_run_nt<true, false>(s, pm, mm, vm, gr, out, n);
     else if (s.adamw != 0) update_run_nt<false, true>(s, pm, mm, vm, gr, out, n);
@@ -153,15 +179,13 @@ void update_block_dispatch(const ptk_adam_scalars& s, float* pm, float* mm, floa
 
 constexpr int64_t kBlock = 1 << 16;
 
-}  // namespace
-
-extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
-                            float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
-                            int64_t n, int32_t n_threads, double* sumsq_out,
-                            int64_t* nonfinite_out) {
+template <class G>
+int cpu_adam(const char* what, const ptk_adam_config* cfg, float* master, float* exp_avg,
+             float* exp_avg_sq, const G* grad, uint16_t* param_out, int64_t n,
+             int32_t n_threads, double* sumsq_out, int64_t* nonfinite_out) {
   if (!cfg || !master || !exp_avg || !exp_avg_sq || !grad || n < 0)
-    return ptk::fail(PTK_EINVAL, "ptk_cpu_adam: bad arguments");
-  if (cfg->step < 1) return ptk::fail(PTK_EINVAL, "ptk_cpu_adam: step must be >= 1");
+    return ptk::fail(PTK_EINVAL, std::string(what) + ": bad arguments");
+  if (cfg->step < 1) return ptk::fail(PTK_EINVAL, std::string(what) + ": step must be >= 1");
   const ptk_adam_scalars s = ptk::derive_scalars(*cfg);
   const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
   const bool stats = sumsq_out != nullptr || nonfinite_out != nullptr;
@@ -184,7 +208,7 @@ extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* ex
       double sq = 0.0;
       int64_t bad = 0;
       for (int64_t i = lo; i < lo + len; ++i) {
-        const float g = bf16_to_f32(grad[i]) * s.gscale;
+        const float g = grad_f32(grad[i]) * s.gscale;
         sq += static_cast<double>(g) * static_cast<double>(g);
         bad += std::isfinite(g) ? 0 : 1;
       }
@@ -210,4 +234,22 @@ extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* ex
   if (sumsq_out) *sumsq_out = sq;
   if (nonfinite_out) *nonfinite_out = bad;
   return PTK_OK;
+}
+
+}  // namespace
+
+extern "C" int ptk_cpu_adam(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                            float* exp_avg_sq, const uint16_t* grad, uint16_t* param_out,
+                            int64_t n, int32_t n_threads, double* sumsq_out,
+                            int64_t* nonfinite_out) {
+  return cpu_adam("ptk_cpu_adam", cfg, master, exp_avg, exp_avg_sq, grad, param_out, n,
+                  n_threads, sumsq_out, nonfinite_out);
+}
+
+extern "C" int ptk_cpu_adam_f32grad(const ptk_adam_config* cfg, float* master, float* exp_avg,
+                                    float* exp_avg_sq, const float* grad, uint16_t* param_out,
+                                    int64_t n, int32_t n_threads, double* sumsq_out,
+                                    int64_t* nonfinite_out) {
+  return cpu_adam("ptk_cpu_adam_f32grad", cfg, master, exp_avg, exp_avg_sq, grad, param_out, n,
+                  n_threads, sumsq_out, nonfinite_out);
 }

@@ -1192,6 +1192,48 @@ __global__ void busy_wait_kernel(int64_t ns) {
   } while (static_cast<int64_t>(t - t0) < ns);
 }
 
+// ------------------------------------------- K4 for non-persistent chunks --
+// Reduce-scatter over peer memory for a chunk that leaves the device after its
+// backward (the offload path): the owned shard of every rank's bf16 gradient
+// chunk, summed in fp32 in rank order 0..W-1 -- the same sum the fused
+// persistent step feeds its Adam -- written as fp32 (the host Adam consumes
+// it unrounded, so an offloaded chunk's update is bit-identical to a
+// persistent one's). Pure streaming over NVLink: register-staged 128-bit
+// loads, every peer's 8-element unit issued before any add.
+struct PeerGrads {
+  const uint16_t* g[PTK_MAX_PEERS];  // rank r's gradient chunk + this rank's shard offset
+};
+
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+peer_reduce_f32_kernel(PeerGrads p, int64_t n, float* __restrict__ out) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t nvec = n >> 3;
+  for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < nvec;
+       u += stride) {
+    uint4 raw[W];
+#pragma unroll
+    for (int r = 0; r < W; ++r) raw[r] = __ldcs(reinterpret_cast<const uint4*>(p.g[r]) + u);
+    float acc[8], f[8];
+    unpack8(raw[0], acc);
+#pragma unroll
+    for (int r = 1; r < W; ++r) {
+      unpack8(raw[r], f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+    }
+    st8f(out + 8 * u, acc);
+  }
+  // n % 8 trailing elements (unpadded shards only)
+  for (int64_t i = 8 * nvec + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    float acc = GradBf16::load1(p.g[0] + i);
+#pragma unroll
+    for (int r = 1; r < W; ++r) acc = __fadd_rn(acc, GradBf16::load1(p.g[r] + i));
+    out[i] = acc;
+  }
+}
+
 // ----------------------------------------------------------- synthetic ----
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -1944,6 +1986,59 @@ int ptk_fill_uniform_f32(float* out, int64_t n, uint64_t seed, int64_t index0, f
   fill_f32_kernel<<<grid, 256, 0, as_stream(stream)>>>(out, n, seed, index0, scale);
   launch_counter()++;
   return check_cuda(cudaGetLastError(), "fill_f32_kernel launch");
+}
+
+int ptk_peer_reduce_scatter_f32(const uint16_t* const* grad_peers, int32_t world, int32_t rank,
+                                int64_t shard, float* out, void* stream) {
+  if (!grad_peers || !out || world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world ||
+      shard < 0)
+    return fail(PTK_EINVAL, "ptk_peer_reduce_scatter_f32: bad arguments");
+  if (shard == 0) return PTK_OK;
+  PeerGrads p{};
+  for (int r = 0; r < world; ++r) {
+    if (!grad_peers[r]) return fail(PTK_EINVAL, "ptk_peer_reduce_scatter_f32: null peer");
+    p.g[r] = grad_peers[r] + static_cast<int64_t>(rank) * shard;
+    if ((reinterpret_cast<uintptr_t>(p.g[r]) & 15u) != 0)
+      return fail(PTK_EINVAL, "ptk_peer_reduce_scatter_f32: shards must be 16-byte aligned");
+  }
+  if ((reinterpret_cast<uintptr_t>(out) & 15u) != 0)
+    return fail(PTK_EINVAL, "ptk_peer_reduce_scatter_f32: out must be 16-byte aligned");
+  cudaStream_t st = as_stream(stream);
+  int grid = 1;
+  switch (world) {
+#define PTK_RS_CASE(W)                                                             \
+  case W:                                                                          \
+    grid = grid_for(peer_reduce_f32_kernel<W>, (shard + 7) / 8);                   \
+    peer_reduce_f32_kernel<W><<<grid, kThreads, 0, st>>>(p, shard, out);           \
+    break;
+    PTK_RS_CASE(1) PTK_RS_CASE(2) PTK_RS_CASE(3) PTK_RS_CASE(4)
+    PTK_RS_CASE(5) PTK_RS_CASE(6) PTK_RS_CASE(7) PTK_RS_CASE(8)
+#undef PTK_RS_CASE
+    default:
+      return fail(PTK_EINVAL, "ptk_peer_reduce_scatter_f32: world > 8");
+  }
+  launch_counter()++;
+  return check_cuda(cudaGetLastError(), "peer_reduce_f32_kernel launch");
+}
+
+int ptk_peer_allgather(void* const* buf_peers, int32_t world, int32_t rank, int64_t shard_bytes,
+                       void* stream) {
+  if (!buf_peers || world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world ||
+      shard_bytes < 0)
+    return fail(PTK_EINVAL, "ptk_peer_allgather: bad arguments");
+  char* local = static_cast<char*>(buf_peers[rank]);
+  if (!local) return fail(PTK_EINVAL, "ptk_peer_allgather: null local buffer");
+  cudaStream_t st = as_stream(stream);
+  // pull: every peer's own shard, rank order from the next rank on (spreads
+  // the W-1 readers of one rank over time); copy-engine transfers, no SMs
+  for (int k = 1; k < world; ++k) {
+    const int q = (rank + k) % world;
+    if (!buf_peers[q]) return fail(PTK_EINVAL, "ptk_peer_allgather: null peer buffer");
+    const int64_t off = static_cast<int64_t>(q) * shard_bytes;
+    PTK_TRY_CUDA(cudaMemcpyAsync(local + off, static_cast<const char*>(buf_peers[q]) + off,
+                                 static_cast<size_t>(shard_bytes), cudaMemcpyDeviceToDevice, st));
+  }
+  return PTK_OK;
 }
 
 int ptk_fill_uniform_bf16(uint16_t* out, int64_t n, uint64_t seed, int64_t index0, float scale,

@@ -107,6 +107,40 @@ def test_host_adam_all_modes_unaligned_bit_exact(mode, offset):
     np.testing.assert_array_equal(pa, pb)
 
 
+@pytest.mark.parametrize("mode", ["adam", "adamw", "l2"])
+@pytest.mark.parametrize("offset", [0, 3])
+def test_host_adam_f32grad_bit_exact(mode, offset):
+    """ptk_cpu_adam_f32grad (the offloaded chunk's update from a fp32
+    reduce-scattered sum, the offload path's peer reduce-scatter): every rule,
+    unaligned output, a NaN in the gradients, statistics -- bit-identical to
+    the oracle's fp32-gradient step."""
+    from paper_2406_08334_b200 import _native as nat
+    n = 50_021
+    wd, adamw = {"adam": (0.0, False), "adamw": (0.01, True), "l2": (0.01, False)}[mode]
+    master = ol.fill_f32(n, 5, 0.05)
+    g = ol.fill_f32(n, 6, 2e-3)
+    g[11] = np.nan
+    a = [master.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    b = [master.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)]
+    buf = np.zeros(n + 8, np.uint16)
+    pa = buf[offset:offset + n]
+    pb = np.zeros(n, np.uint16)
+    for step in (1, 2):
+        cfg = nat.adam_config(step=step, weight_decay=wd, adamw=adamw, grad_scale=0.25)
+        sq, bad = ctypes.c_double(), ctypes.c_int64()
+        nat.lib.ptk_cpu_adam_f32grad(ctypes.byref(cfg),
+                                     *[ctypes.c_void_p(x.ctypes.data) for x in a],
+                                     ctypes.c_void_p(g.ctypes.data),
+                                     ctypes.c_void_p(pa.ctypes.data), n, 2, ctypes.byref(sq),
+                                     ctypes.byref(bad))
+        osq, obad = ol.adam_step(ol.scalars(step=step, weight_decay=wd, adamw=adamw,
+                                            grad_scale=0.25), *b, g, pb)
+        assert bad.value == obad == 1
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x.view(np.uint32), y.view(np.uint32))
+    np.testing.assert_array_equal(pa, pb)
+
+
 def test_errors_are_reported():
     from paper_2406_08334_b200 import _native as nat
     rc = nat.raw.ptk_cpu_adam(None, None, None, None, None, None, 0, 0, None, None)
