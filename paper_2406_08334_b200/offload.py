@@ -56,13 +56,29 @@ def _sh(stream: torch.cuda.Stream) -> ctypes.c_void_p:
 
 
 class ChunkPool:
+    """`exchange` (w > 1): "nccl" -- NCCL all-gather on fetch and in-place
+    bf16 reduce-scatter on drain (needs `comm`); "peer" -- the same two steps
+    over NVLink peer memory without a library collective (attach_ipc_peers):
+    the fetch pulls every peer's shard out of the peer's slot with
+    copy-engine transfers (ptk_peer_allgather), the drain sums the owned
+    shard of every rank's gradient in fp32 in rank order
+    (ptk_peer_reduce_scatter_f32) and the host Adam consumes that fp32 sum
+    (ptk_cpu_adam_f32grad) -- exactly the numbers the fused persistent step
+    computes, so an offloaded chunk trains bit-identically to a persistent
+    one at any w. Both bracket their transfers with peer barriers (one
+    signal array for the h2d stream's gathers, one for the compute stream's
+    reduces)."""
+
     def __init__(self, numels: list[int], first: int, n_buffer: int, world: int = 1, rank: int = 0,
                  comm=None, device=None, cpu_threads: int | None = None,
-                 piece: int = 32 * 1024 * 1024):
+                 piece: int = 32 * 1024 * 1024, exchange: str = "nccl"):
         if n_buffer < 1:
             raise ValueError("non-persistent chunks need at least one buffer")
-        if world > 1 and comm is None:
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        if world > 1 and exchange == "nccl" and comm is None:
             raise ValueError("world > 1 needs a ptk_comm communicator")
+        self.exchange = exchange
         # the host Adam must not starve the threads that launch the GPU work
         # (Python main thread + autograd's device thread): leave two cores per
         # rank, and split the host between the ranks of this node
@@ -76,7 +92,10 @@ class ChunkPool:
         n_pad_max = max(self.shard[c] * world for c in self.numel)
         pin = dict(device="cpu", pin_memory=True)
         self.h_param = {c: torch.zeros(s, dtype=BF16, **pin) for c, s in self.shard.items()}
-        self.h_grad = {c: torch.zeros(s, dtype=BF16, **pin) for c, s in self.shard.items()}
+        # the offloaded gradient: bf16 (NCCL's in-place reduce-scatter), or the
+        # fp32 rank-order sum of the peer exchange
+        gdt = torch.float32 if exchange == "peer" else BF16
+        self.h_grad = {c: torch.zeros(s, dtype=gdt, **pin) for c, s in self.shard.items()}
         self.h_master = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
         self.h_m = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
         self.h_v = {c: torch.zeros(s, dtype=torch.float32, **pin) for c, s in self.shard.items()}
@@ -102,6 +121,85 @@ class ChunkPool:
         self.timeline = None   # timeline.Timeline: events in the simulator's schema
         self._lock = threading.RLock()
         self._slot_ptr = {t.untyped_storage().data_ptr(): k for k, t in enumerate(self.slots)}
+        if exchange == "peer":
+            shard_max = max(self.shard.values())
+            # the drained chunk's local gradient, read by every peer's reduce
+            self.staging = torch.zeros(n_pad_max, dtype=BF16, device=self.device)
+            # this rank's reduced fp32 shard, two buffers so a D2H can still
+            # be reading one while the next drain reduces into the other
+            self.reduced = [torch.zeros(shard_max, dtype=torch.float32, device=self.device)
+                            for _ in range(2)]
+            self.reduced_free: list = [None, None]   # d2h event: the buffer's last D2H done
+            self.n_drains = 0
+            self.slot_peers = self.staging_peers = None
+            self.sig_gather = self.sig_reduce = None
+            self.g_epoch = self.r_epoch = 0
+            if world == 1:   # nothing to exchange: the local buffers are the peer table
+                self._set_peer_tables([[t.data_ptr() for t in self.slots] + [self.staging.data_ptr()]])
+
+    # ------------------------------------------------ peer exchange setup --
+    def _set_peer_tables(self, ptrs) -> None:
+        """ptrs[r] = rank r's [slot 0 .. slot n_buffer-1, staging, (signals...)]
+        as mapped in this process."""
+        arr = ctypes.c_void_p * nat.PTK_MAX_PEERS
+        nb = len(self.slots)
+        self.slot_peers = [arr(*[ptrs[r][k] for r in range(self.world)]) for k in range(nb)]
+        self.staging_peers = arr(*[ptrs[r][nb] for r in range(self.world)])
+        if len(ptrs[0]) > nb + 1:
+            self.sig_gather = arr(*[ptrs[r][nb + 1] for r in range(self.world)])
+            self.sig_reduce = arr(*[ptrs[r][nb + 2] for r in range(self.world)])
+
+    def attach_ipc_peers(self, group=None) -> None:
+        """exchange="peer", w > 1: map every peer's slots, gradient staging
+        buffer and the two signal arrays into this process (cudaIpc handles
+        exchanged through torch.distributed -- plumbing only). Collective."""
+        import torch.distributed as dist
+        if self.exchange != "peer":
+            raise ValueError("attach_ipc_peers needs exchange='peer'")
+        if self.world == 1:
+            return
+        self._signals = [torch.zeros(nat.PTK_MAX_PEERS, dtype=torch.int32, device=self.device)
+                         for _ in range(2)]
+        bufs = list(self.slots) + [self.staging] + self._signals
+        mine = []
+        for t in bufs:
+            h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
+            off = ctypes.c_int64()
+            nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
+            mine.append((bytes(h), off.value))
+        torch.cuda.synchronize(self.device)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._opened = []
+        ptrs = []
+        for r in range(self.world):
+            row = []
+            for k, (hb, off) in enumerate(everyone[r]):
+                if r == self.rank:
+                    row.append(bufs[k].data_ptr())
+                    continue
+                base = ctypes.c_void_p()
+                nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
+                                            ctypes.byref(base))
+                self._opened.append(base)
+                row.append(base.value + off)
+            ptrs.append(row)
+        self._set_peer_tables(ptrs)
+        dist.barrier(group=group)
+
+    def close_ipc_peers(self) -> None:
+        for base in getattr(self, "_opened", []):
+            nat.lib.ptk_ipc_close_handle(base)
+        self._opened = []
+
+    def _barrier(self, sig, stream) -> None:
+        if sig is self.sig_gather:
+            self.g_epoch += 1
+            epoch = self.g_epoch
+        else:
+            self.r_epoch += 1
+            epoch = self.r_epoch
+        nat.lib.ptk_peer_barrier(sig, self.world, self.rank, epoch, _sh(stream))
 
     # ------------------------------------------------------------ storage --
     def load_initial(self, c: int, full_chunk: torch.Tensor) -> None:
@@ -174,7 +272,16 @@ class ChunkPool:
             self.updates.pop(c, None)
             self.counters["host_wait_s"] = self.counters.get("host_wait_s", 0.0) + waited
         self.counters["h2d_bytes"] += 2 * s
-        if self.comm is not None:
+        if self.exchange == "peer" and self.world > 1:
+            if self.sig_gather is None:
+                raise RuntimeError("exchange='peer' needs attach_ipc_peers() before use")
+            # every rank's own shard is in its slot k -> pull the others' ->
+            # nobody reuses slot k before every peer has finished pulling
+            self._barrier(self.sig_gather, self.h2d)
+            nat.lib.ptk_peer_allgather(self.slot_peers[k], self.world, self.rank, 2 * s,
+                                       _sh(self.h2d))
+            self._barrier(self.sig_gather, self.h2d)
+        elif self.comm is not None:
             nat.lib.ptk_chunk_allgather(self.comm, vp(self.slots[k]), s, 0, _sh(self.h2d))
         if self.timeline is not None:
             self.timeline.gpu(self.h2d, "h2d", "upload_end", f"chunk={c + 1}")
@@ -218,27 +325,56 @@ class ChunkPool:
             if self.pending_uses[c] == 0:
                 self._drain(c, self.partial.pop(c))
 
+    def _reduce_peer(self, c: int, grad: torch.Tensor, cur) -> torch.Tensor:
+        """exchange="peer": this rank's fp32 reduced shard of chunk c, on cur."""
+        s = self.shard[c]
+        b = self.n_drains % 2
+        self.n_drains += 1
+        if self.reduced_free[b] is not None:    # its previous D2H has read it
+            cur.wait_event(self.reduced_free[b])
+        out = self.reduced[b]
+        if self.world == 1:
+            nat.lib.ptk_peer_reduce_scatter_f32(self.staging_peers, 1, 0, s, vp(out), _sh(cur))
+            return out
+        if self.sig_reduce is None:
+            raise RuntimeError("exchange='peer' needs attach_ipc_peers() before use")
+        self.staging[:grad.numel()].copy_(grad)
+        self._barrier(self.sig_reduce, cur)      # every rank's gradient is staged
+        nat.lib.ptk_peer_reduce_scatter_f32(self.staging_peers, self.world, self.rank, s,
+                                            vp(out), _sh(cur))
+        self._barrier(self.sig_reduce, cur)      # nobody restages before all have read
+        return out
+
     def _drain(self, c: int, grad: torch.Tensor) -> None:
         s = self.shard[c]
         cur = torch.cuda.current_stream(self.device)
         staged = grad   # already padded to shard*world: reduce-scatter / D2H in place
-        if self.comm is not None:
+        peer = self.exchange == "peer"
+        if peer:
+            if self.world == 1:
+                self.staging_peers[0] = grad.data_ptr()
+            reduced = self._reduce_peer(c, grad, cur)
+        elif self.comm is not None:
             nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
         self.d2h.wait_stream(cur)
-        src = staged[self.rank * s:]
+        src = reduced if peer else staged[self.rank * s:]
+        esize = src.element_size()
         landed = []
         if self.timeline is not None:
             self.timeline.gpu(self.d2h, "d2h", "offload_start", f"chunk={c + 1}")
         for lo, n in self._pieces(c):
-            nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c][lo:]), vp(src[lo:]), 2 * n,
+            nat.lib.ptk_memcpy_d2h_async(vp(self.h_grad[c][lo:]), vp(src[lo:]), esize * n,
                                          _sh(self.d2h))
             ev = torch.cuda.Event()
             ev.record(self.d2h)
             landed.append(ev)
-        staged.record_stream(self.d2h)
+        if peer:
+            self.reduced_free[(self.n_drains - 1) % 2] = landed[-1] if landed else None
+        else:
+            staged.record_stream(self.d2h)
         if self.timeline is not None:
             self.timeline.gpu(self.d2h, "d2h", "offload_end", f"chunk={c + 1}")
-        self.counters["d2h_bytes"] += 2 * s
+        self.counters["d2h_bytes"] += esize * s
         cfg = self.hyper.config(self.step, self.world)
         # the device copy is stale once the host update runs: release the slot
         # (a later fetch into it waits for the compute issued until now)
@@ -259,10 +395,11 @@ class ChunkPool:
             if i == 0 and tl is not None:
                 tl.host("cpu", "update_start", f"chunk={c + 1}")
             t0 = time.perf_counter()
-            rc = nat.raw.ptk_cpu_adam(ctypes.byref(cfg), vp(self.h_master[c][lo:]),
-                                      vp(self.h_m[c][lo:]), vp(self.h_v[c][lo:]),
-                                      vp(self.h_grad[c][lo:]), vp(self.h_param[c][lo:]), n,
-                                      self.cpu_threads, None, None)
+            adam = (nat.raw.ptk_cpu_adam_f32grad if self.exchange == "peer"
+                    else nat.raw.ptk_cpu_adam)
+            rc = adam(ctypes.byref(cfg), vp(self.h_master[c][lo:]), vp(self.h_m[c][lo:]),
+                      vp(self.h_v[c][lo:]), vp(self.h_grad[c][lo:]), vp(self.h_param[c][lo:]), n,
+                      self.cpu_threads, None, None)
             busy += time.perf_counter() - t0
             done.set()   # set even on failure: a fetch waiting on it re-raises via result()
             if rc != nat.PTK_OK:

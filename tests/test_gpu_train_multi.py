@@ -48,7 +48,8 @@ def _need_gpus(n):
         pytest.skip(f"needs {n} GPUs (one NCCL rank per GPU), this box has {have}")
 
 
-def _build(d: Path, dev, world, rank, mode, comm=None, n_persist=None, n_buffer=0):
+def _build(d: Path, dev, world, rank, mode, comm=None, n_persist=None, n_buffer=0,
+           pool_exchange=None):
     from paper_2406_08334_b200 import planner
     from paper_2406_08334_b200.chunks import ChunkSet
     from paper_2406_08334_b200.offload import ChunkPool
@@ -62,8 +63,11 @@ def _build(d: Path, dev, world, rank, mode, comm=None, n_persist=None, n_buffer=
     numels = [c["used_bytes"] // 2 for c in layout["chunks"]]
     np_ = len(numels) if n_persist is None else n_persist
     cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode=mode, comm=comm)
+    # the fused exchange's pool exchanges over peer memory too (no NCCL)
     pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev,
-                      piece=65_544) if np_ < len(numels) else None)
+                      piece=65_544,
+                      exchange=pool_exchange or ("peer" if mode == "fused" else "nccl"))
+            if np_ < len(numels) else None)
     shape = GPT2Shape.from_trace_meta(trace["meta"], trace["n_blocks"])
     model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(seed=0)
@@ -123,6 +127,8 @@ def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_
                                   n_persist, n_buffer)
     if mode == "fused":
         model.chunks.attach_ipc_peers()
+        if model.pool is not None:
+            model.pool.attach_ipc_peers()
     hyper = _hyper()
     b = GLOBAL_BATCH // world
     losses = []
@@ -143,6 +149,8 @@ def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **out)
     if mode == "fused":
         model.chunks.close_ipc_peers()
+        if model.pool is not None:
+            model.pool.close_ipc_peers()
     if comm is not None:
         nat.lib.ptk_comm_destroy(comm)
     dist.destroy_process_group()
@@ -230,6 +238,46 @@ def test_fused_training_processes_equal_virtual_ranks(tmp_path, cuda_device, wor
     else:
         _follows_w1(res, _w1_losses(tmp_path, cuda_device))
         assert res[0]["losses"].size == STEPS
+
+
+def test_peer_pool_single_rank_equals_persistent(tmp_path, cuda_device):
+    """exchange='peer' at w = 1: the offloaded chunk's gradient goes to the
+    host as fp32 and the host Adam runs on it -- the same numbers as the
+    device Adam on the bf16 gradient, so losses and masters equal the
+    all-persistent run bit for bit."""
+    from paper_2406_08334_b200.train import train_step
+    runs = []
+    for n_persist, n_buffer in ((None, 0), (1, 1)):
+        model, shape, numels = _build(tmp_path / f"w1peer_{n_persist}", cuda_device, 1, 0,
+                                      "nccl", n_persist=n_persist, n_buffer=n_buffer,
+                                      pool_exchange="peer")
+        if model.pool is not None:
+            assert model.pool.h_grad[1].dtype == torch.float32
+        losses = [float(train_step(model, x, y, _hyper()).detach())
+                  for x, y in _batches(shape, cuda_device)]
+        torch.cuda.synchronize()
+        st = _state(model, numels)
+        runs.append((losses, {k: v for k, v in st.items() if k.startswith("master")}))
+    assert runs[0][0] == runs[1][0]
+    for k, v in runs[0][1].items():
+        np.testing.assert_array_equal(runs[1][1][k][:v.size], v, err_msg=k)
+
+
+def test_peer_pool_two_processes_equals_persistent(tmp_path, cuda_device):
+    """w = 2 in two processes on this GPU, NO library collective anywhere:
+    chunk 0 persistent (fused RS->Adam->AG), chunks 1-2 non-persistent in a
+    one-slot pool that gathers over peer memory (copy-engine pulls between
+    peer barriers) and drains through the fp32 peer reduce-scatter into the
+    host Adam. Losses and every master shard equal the all-persistent fused
+    run bit for bit (same fp32 rank-order sums, same update rule)."""
+    world = 2
+    ref = _spawn(world, tmp_path, "fused")
+    res = _spawn(world, tmp_path, "fused", n_persist=1, n_buffer=1)
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["losses"], ref[r]["losses"])
+        for k, v in ref[r].items():
+            if k.startswith("master"):
+                np.testing.assert_array_equal(res[r][k][:v.size], v, err_msg=f"rank {r} {k}")
 
 
 def test_nccl_training_across_gpus(tmp_path, cuda_device):
