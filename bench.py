@@ -337,8 +337,7 @@ def run_gpu(args):
         # so only the fused exchange runs and the timings are not a bench value
         legs = ["fused"]
         local = 0
-        args.offload_persist = -1   # the pool's exchange is NCCL
-        args.train_exchange = "fused"
+        args.train_exchange = "fused"   # NCCL refuses two ranks on one device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     numels, desc = chunk_numels(args.workload)
@@ -680,19 +679,23 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
     layout = planner.layout_for(name)
     numels = [c["used_bytes"] // layout["bytes_per_param"] for c in layout["chunks"]]
     np_ = len(numels) if n_persist is None else n_persist
-    # N > 1, every chunk persistent: the fused RS->Adam->AG kernel over NVLink
-    # peer memory is the training step's exchange (--train-exchange nccl: the
-    # library path); non-persistent chunks (ChunkPool) exchange through NCCL
-    mode = train_exchange_mode(args, world, np_ == len(numels))
+    # N > 1: the persistent chunks' step is the fused RS->Adam->AG kernel over
+    # NVLink peer memory and the non-persistent chunks (ChunkPool) gather and
+    # reduce over peer memory too -- no library collective
+    # (--train-exchange nccl: NCCL for both, the library path)
+    mode = train_exchange_mode(args, world)
     cs = ChunkSet(numels[:np_], world=world, rank=rank, device=dev, mode=mode,
                   comm=comm if mode == "nccl" else None)
-    pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev)
+    pool = (ChunkPool(numels, np_, n_buffer, world=world, rank=rank, comm=comm, device=dev,
+                      exchange="peer" if mode == "fused" else "nccl")
             if np_ < len(numels) else None)
     shape = GPT2Shape.from_trace(trace)
     model = ChunkedGPT2(shape, layout, cs, trace["ops"], pool=pool)
     model.init_weights(seed=0)
     if mode == "fused":
         cs.attach_ipc_peers()
+        if pool is not None:
+            pool.attach_ipc_peers()
     batch = int(trace["meta"]["batch_size"])
     n_iter = args.warmup + args.train_steps
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -742,6 +745,8 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
            "data": "synthetic tokens (uniform ids, target = id + 1), random init"}
     if world > 1:
         out["exchange"] = ("fused RS->Adam->AG table kernel over NVLink peer memory"
+                           + ("; pool: peer all-gather + fp32 peer reduce-scatter"
+                              if pool is not None else "")
                            if mode == "fused" else
                            "NCCL RS / AG per chunk (ChunkSet nccl mode, ChunkPool)")
     if pool is not None:
@@ -754,15 +759,15 @@ def run_train(args, world, rank, dev, comm, n_persist=None, n_buffer=0):
         torch.cuda.synchronize()
         barrier(world)   # no rank unmaps while a peer may still store into it
         cs.close_ipc_peers()
+        if pool is not None:
+            pool.close_ipc_peers()
     del model, cs, pool
     torch.cuda.empty_cache()
     return out
 
 
-def train_exchange_mode(args, world, all_persistent) -> str:
-    if world > 1 and all_persistent and args.train_exchange == "fused":
-        return "fused"
-    return "nccl"
+def train_exchange_mode(args, world) -> str:
+    return "fused" if world > 1 and args.train_exchange == "fused" else "nccl"
 
 
 def _run_child(args, world, rank, local, extra, timeout, what, env_extra=None):
@@ -813,7 +818,7 @@ def run_train_child(args, world, rank, local, n_persist):
     rank, is retried with NCCL (the line says so)."""
     extra = ["--leg", "train", "--leg-persist", str(n_persist)]
     res, err = _run_child(args, world, rank, local, extra, args.train_timeout, "train")
-    fused_first = train_exchange_mode(args, world, n_persist < 0) == "fused"
+    fused_first = train_exchange_mode(args, world) == "fused"
     if all_ok(res is not None, world) or not fused_first or args.shared_device:
         return res if res is not None else {"error": err}
     res, err2 = _run_child(args, world, rank, local, extra + ["--train-exchange", "nccl"],
@@ -882,7 +887,7 @@ def run_train_leg(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n_persist = None if args.leg_persist < 0 else args.leg_persist
-    fused = train_exchange_mode(args, world, n_persist is None) == "fused"
+    fused = train_exchange_mode(args, world) == "fused"
     comm = None if fused else make_comm(world, rank)
     res = run_train(args, world, rank, dev, comm, n_persist=n_persist,
                     n_buffer=args.offload_buffers if n_persist is not None else 0)
@@ -1307,8 +1312,9 @@ def main():
     ap.add_argument("--train-timeout", type=int, default=400,
                     help="N>1: seconds before a training child process is killed")
     ap.add_argument("--train-exchange", default="fused", choices=["fused", "nccl"],
-                    help="N>1 all-persistent training: the fused RS->Adam->AG kernel over NVLink "
-                         "peer memory (default, NCCL retry on failure) or NCCL RS/AG")
+                    help="N>1 training: the fused RS->Adam->AG kernel over NVLink peer memory "
+                         "for persistent chunks + peer all-gather / fp32 peer reduce-scatter for "
+                         "the offloaded pool (default, NCCL retry on failure), or NCCL for both")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--train-graph", action=argparse.BooleanOptionalAction, default=True,
                     help="training (all chunks persistent): forward + backward as one CUDA-graph "
