@@ -90,6 +90,18 @@ def main():
         fused_group_step(sets_c, AdamHyper(lr=1e-3), max_grad_norm=0.01, skip_nonfinite=True)
         fused_group_step(sets_c, AdamHyper(lr=1e-3))
 
+    # the non-persistent chunks' peer exchange: fp32 peer reduce-scatter over
+    # 3 virtual ranks' gradient chunks (ragged shard) + the copy-engine gather
+    w, shard = 3, 2048 * 300 + 8
+    gch = [torch.empty(w * shard, dtype=torch.int16, device=dev) for _ in range(w)]
+    for r, t in enumerate(gch):
+        nat.lib.ptk_fill_uniform_bf16(vp(t), w * shard, 40 + r, 0, ctypes.c_float(1e-3), s)
+    red = torch.empty(shard, dtype=torch.float32, device=dev)
+    gp = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(*[t.data_ptr() for t in gch])
+    for r in range(w):
+        nat.lib.ptk_peer_reduce_scatter_f32(gp, w, r, shard, vp(red), s)
+    nat.lib.ptk_peer_allgather(gp, w, 1, 2 * shard, s)
+
     # the register-staged fused kernel
     os.environ["PTK_FUSED_KERNEL"] = "ldg"
     sets_l = [ChunkSet([3 * 8 * 148 * 256 + 24], world=3, rank=r, device=dev, mode="fused")

@@ -101,7 +101,8 @@ def test_fused_ldg_variant_bit_exact(cuda_device):
                        env=env, capture_output=True, text=True, timeout=900,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "12 passed" in r.stdout, r.stdout[-2000:]
+    # 12 small-size cases + the 4 full-size cfg2 cases of the fused exchange
+    assert "16 passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
 
 
 def _fused_sets(ch, numels, world, dev):
