@@ -508,3 +508,34 @@ def test_pinned_copies_round_trip(cuda_device):
     assert torch.equal(back, src * 2)
     nat.lib.ptk_stream_destroy(s)
     nat.lib.ptk_host_free_pinned(host)
+
+
+@pytest.mark.parametrize("world,shard", [(1, 4101), (2, 2048 * 150 + 8), (3, 1000),
+                                         (8, 8 * 1024 + 8)])
+def test_peer_reduce_scatter_and_allgather_match_oracle(cuda_device, world, shard):
+    """The non-persistent chunks' peer exchange over W virtual ranks' buffers:
+    ptk_peer_reduce_scatter_f32 = the oracle's rank-order fp32 reduce-scatter
+    bit for bit (every rank's shard; W = 1 with an unpadded n % 8 tail), and
+    ptk_peer_allgather assembles every rank's shard into each rank's buffer."""
+    nat, ch = _modules()
+    n_pad = world * shard
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    host = [ol.fill_bf16(n_pad, 70 + r, ch.GRAD_SCALE) for r in range(world)]
+    dev = [torch.from_numpy(h.view(np.int16).copy()).to(cuda_device) for h in host]
+    ptrs = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(*[t.data_ptr() for t in dev])
+    for r in range(world):
+        out = torch.empty(shard, dtype=torch.float32, device=cuda_device)
+        nat.lib.ptk_peer_reduce_scatter_f32(ptrs, world, r, shard, ch.vp(out), s)
+        want = ol.reduce_scatter(host, r, shard, fp32=True)
+        np.testing.assert_array_equal(_bits(out), want.view(np.uint32))
+    # all-gather: each rank's buffer holds only its own shard, then pulls the rest
+    bufs = [torch.zeros(n_pad, dtype=torch.int16, device=cuda_device) for _ in range(world)]
+    for r, b in enumerate(bufs):
+        b[r * shard:(r + 1) * shard] = dev[r][r * shard:(r + 1) * shard]
+    bp = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(*[b.data_ptr() for b in bufs])
+    for r in range(world):
+        nat.lib.ptk_peer_allgather(bp, world, r, 2 * shard, s)
+    torch.cuda.synchronize()
+    want = ol.allgather([h[r * shard:(r + 1) * shard] for r, h in enumerate(host)])
+    for b in bufs:
+        np.testing.assert_array_equal(b.cpu().numpy().view(np.uint16), want)
