@@ -280,6 +280,25 @@ def test_peer_pool_two_processes_equals_persistent(tmp_path, cuda_device):
                 np.testing.assert_array_equal(res[r][k][:v.size], v, err_msg=f"rank {r} {k}")
 
 
+def test_fused_and_peer_pool_training_across_gpus(tmp_path, cuda_device):
+    """The same two checks with one rank per GPU (NVLink peers): fused
+    training equals the virtual-rank run, and the peer pool equals the
+    all-persistent fused run, bit for bit."""
+    world = 2
+    _need_gpus(world)
+    ref = _spawn(world, tmp_path, "fused", spread=True)
+    virt = _virtual(tmp_path, cuda_device, world, 0.0)
+    for r in range(world):
+        for k, v in virt[r].items():
+            np.testing.assert_array_equal(ref[r][k], v, err_msg=f"rank {r} {k}")
+    res = _spawn(world, tmp_path / "pool", "fused", spread=True, n_persist=1, n_buffer=1)
+    for r in range(world):
+        np.testing.assert_array_equal(res[r]["losses"], ref[r]["losses"])
+        for k, v in ref[r].items():
+            if k.startswith("master"):
+                np.testing.assert_array_equal(res[r][k][:v.size], v, err_msg=f"rank {r} {k}")
+
+
 def test_nccl_training_across_gpus(tmp_path, cuda_device):
     world = 2
     _need_gpus(world)
