@@ -1309,7 +1309,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--train-steps", type=int, default=10,
                     help="timed iterations of the end-to-end cfg2 training step (tokens/s); 0 = skip")
-    ap.add_argument("--train-timeout", type=int, default=400,
+    ap.add_argument("--train-timeout", type=int, default=300,
                     help="N>1: seconds before a training child process is killed")
     ap.add_argument("--train-exchange", default="fused", choices=["fused", "nccl"],
                     help="N>1 training: the fused RS->Adam->AG kernel over NVLink peer memory "
@@ -1331,7 +1331,7 @@ def main():
     ap.add_argument("--nccl-symmetric", action=argparse.BooleanOptionalAction, default=True,
                     help="N>1 NCCL leg: chunk buffers in NCCL symmetric windows (ncclMemAlloc + "
                          "ncclCommWindowRegister), retried on plain buffers if that fails")
-    ap.add_argument("--leg-timeout", type=int, default=600,
+    ap.add_argument("--leg-timeout", type=int, default=420,
                     help="N>1: seconds before a fused-exchange child process is killed")
     ap.add_argument("--leg", default=None, choices=[None, "train", "exchange", "ping"],
                     help=argparse.SUPPRESS)
