@@ -1204,25 +1204,41 @@ struct PeerGrads {
   const uint16_t* g[PTK_MAX_PEERS];  // rank r's gradient chunk + this rank's shard offset
 };
 
+// U units per thread per iteration keep >= 8 independent 16-byte loads in
+// flight per thread whatever W is (W = 2: 4 units).
+template <int W>
+__host__ __device__ constexpr int peer_reduce_units() { return W >= 8 ? 1 : 8 / W; }
+
 template <int W>
 __global__ void __launch_bounds__(kThreads)
 peer_reduce_f32_kernel(PeerGrads p, int64_t n, float* __restrict__ out) {
+  constexpr int U = peer_reduce_units<W>();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t nvec = n >> 3;
-  for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < nvec;
-       u += stride) {
-    uint4 raw[W];
+  for (int64_t u0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u0 < nvec;
+       u0 += stride * U) {
+    uint4 raw[U][W];
 #pragma unroll
-    for (int r = 0; r < W; ++r) raw[r] = __ldcs(reinterpret_cast<const uint4*>(p.g[r]) + u);
-    float acc[8], f[8];
-    unpack8(raw[0], acc);
+    for (int j = 0; j < U; ++j) {
+      const int64_t u = u0 + j * stride;
 #pragma unroll
-    for (int r = 1; r < W; ++r) {
-      unpack8(raw[r], f);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+      for (int r = 0; r < W; ++r)
+        raw[j][r] = u < nvec ? __ldcs(reinterpret_cast<const uint4*>(p.g[r]) + u) : uint4{};
     }
-    st8f(out + 8 * u, acc);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int64_t u = u0 + j * stride;
+      if (u >= nvec) break;
+      float acc[8], f[8];
+      unpack8(raw[j][0], acc);
+#pragma unroll
+      for (int r = 1; r < W; ++r) {
+        unpack8(raw[j][r], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+      }
+      st8f(out + 8 * u, acc);
+    }
   }
   // n % 8 trailing elements (unpadded shards only)
   for (int64_t i = 8 * nvec + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -2008,7 +2024,8 @@ int ptk_peer_reduce_scatter_f32(const uint16_t* const* grad_peers, int32_t world
   switch (world) {
 #define PTK_RS_CASE(W)                                                             \
   case W:                                                                          \
-    grid = grid_for(peer_reduce_f32_kernel<W>, (shard + 7) / 8);                   \
+    grid = grid_for(peer_reduce_f32_kernel<W>,                                     \
+                    (shard / 8 + peer_reduce_units<W>() - 1) / peer_reduce_units<W>()); \
     peer_reduce_f32_kernel<W><<<grid, kThreads, 0, st>>>(p, shard, out);           \
     break;
     PTK_RS_CASE(1) PTK_RS_CASE(2) PTK_RS_CASE(3) PTK_RS_CASE(4)
