@@ -336,10 +336,25 @@ class ChunkSet:
         """Start a step whose chunks are updated one by one, each as soon as
         its gradients are complete (ChunkedGPT2's backward hooks), on the
         side stream `side` while the backward continues on the compute
-        stream. Same kernels and inputs as step(): bit-identical results."""
-        if self.mode != "nccl":
-            raise ValueError("overlapped step needs mode='nccl' (the fused exchange brackets "
-                             "all chunks with peer barriers)")
+        stream. Same kernels and inputs as step(): bit-identical results.
+
+        Fused mode over IPC peers (w > 1): each chunk's REDUCE runs as soon as
+        its gradients are complete (ptk_peer_reduce_scatter_f32 between peer
+        barriers on the side stream: the NVLink reads overlap the remaining
+        backward, as the reference schedules the reduce,
+        proj/src/sim.cpp:426-436); after the backward, the Adam of every
+        chunk on its fp32 reduced shard (ptk_chunk_adam_f32grad) and the
+        all-gather (ptk_peer_allgather). Same fp32 rank-order sums and the
+        same update rule as the one-kernel fused step: bit-identical."""
+        self._ov_fused = self.mode == "fused" and self.world > 1
+        if self._ov_fused and self.signal_ptrs is None:
+            raise ValueError("an overlapped fused step needs IPC peers (attach_ipc_peers); "
+                             "virtual ranks step together (fused_group_step)")
+        if self.mode == "fused" and self.world == 1 and self.fused_table is None:
+            raise RuntimeError("fused mode needs peer pointers (attach_virtual_peers)")
+        if self._ov_fused and getattr(self, "_reduced", None) is None:
+            self._reduced = [torch.empty(c.shard, dtype=F32, device=self.device)
+                             for c in self.chunks]
         self.step_count += 1
         self._ov_cfg = hyper.config(self.step_count, self.world)
         self._ov_side = side
@@ -357,6 +372,12 @@ class ChunkSet:
         side.wait_stream(torch.cuda.current_stream(self.device))
         s = stream_handle(side)
         c = self.chunks[ci]
+        if self._ov_fused:   # the reduce now; update + all-gather after the backward
+            self._peer_barrier(s)          # every rank's gradients of chunk ci are final
+            nat.lib.ptk_peer_reduce_scatter_f32(self.peer_grad_ptrs[ci], self.world, self.rank,
+                                                c.shard, vp(self._reduced[ci]), s)
+            self._peer_barrier(s)          # nobody rewrites them before all have read
+            return
         tl = self.timeline
         if tl is not None:
             tl.gpu(side, "gpu", "optim_start", f"chunk={c.chunk_id + 1}")
@@ -375,8 +396,25 @@ class ChunkSet:
         order the compute stream after the side stream."""
         for ci in range(len(self.chunks)):
             self.step_chunk_overlapped(ci)
+        if self._ov_fused:
+            s = stream_handle(self._ov_side)
+            for ci, c in enumerate(self.chunks):
+                nat.lib.ptk_chunk_adam_f32grad(ctypes.byref(self._ov_cfg), vp(c.master),
+                                               vp(c.exp_avg), vp(c.exp_avg_sq),
+                                               vp(self._reduced[ci]), vp(c.param_shard()),
+                                               c.shard, vp(self.stats), vp(self.workspace),
+                                               None, None, s)
+            self._peer_barrier(s)              # every rank's updated shards are written
+            for ci, c in enumerate(self.chunks):
+                nat.lib.ptk_peer_allgather(self.peer_param_ptrs[ci], self.world, self.rank,
+                                           2 * c.shard, s)
+            self._peer_barrier(s)              # every rank has pulled every shard
         torch.cuda.current_stream(self.device).wait_stream(self._ov_side)
         self._ov_side = None
+
+    def _peer_barrier(self, s) -> None:
+        self.epoch += 1
+        nat.lib.ptk_peer_barrier(self.signal_ptrs, self.world, self.rank, self.epoch, s)
 
     def _step_clipped(self, cfg, s, max_grad_norm: float, skip_nonfinite: bool) -> None:
         for c in self.chunks:

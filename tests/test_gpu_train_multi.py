@@ -102,7 +102,8 @@ def _state(model, numels):
     return out
 
 
-def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_buffer):
+def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_buffer,
+               overlap=False):
     import ctypes
 
     import torch.distributed as dist
@@ -139,7 +140,7 @@ def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_
             loss.backward()
             model.chunks.step(hyper, max_grad_norm=max_norm)
         else:
-            loss = train_step(model, xs, ys, hyper)
+            loss = train_step(model, xs, ys, hyper, overlap=overlap)
         losses.append(float(loss.detach()))
     torch.cuda.synchronize()
     out = _state(model, numels)
@@ -156,14 +157,15 @@ def _rank_main(rank, world, port, out_dir, mode, spread, max_norm, n_persist, n_
     dist.destroy_process_group()
 
 
-def _spawn(world, tmp_path, mode, spread=False, max_norm=0.0, n_persist=None, n_buffer=0):
+def _spawn(world, tmp_path, mode, spread=False, max_norm=0.0, n_persist=None, n_buffer=0,
+           overlap=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     port = _free_port()
-    out = tmp_path / f"{mode}_{n_persist}_{max_norm}"
+    out = tmp_path / f"{mode}_{n_persist}_{max_norm}_{overlap}"
     out.mkdir(parents=True, exist_ok=True)
     procs = [ctx.Process(target=_rank_main, args=(r, world, port, str(out), mode, spread,
-                                                  max_norm, n_persist, n_buffer))
+                                                  max_norm, n_persist, n_buffer, overlap))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -238,6 +240,21 @@ def test_fused_training_processes_equal_virtual_ranks(tmp_path, cuda_device, wor
     else:
         _follows_w1(res, _w1_losses(tmp_path, cuda_device))
         assert res[0]["losses"].size == STEPS
+
+
+def test_fused_overlapped_training_equals_fused(tmp_path, cuda_device):
+    """overlap=True with the fused exchange (two processes on this GPU): each
+    chunk's reduce runs on a side stream as soon as its gradients are complete
+    (peer reduce-scatter between barriers, overlapping the rest of the
+    backward), the Adam on the fp32 reduced shards and the all-gather follow
+    the backward -- bit-identical to the one-kernel fused step."""
+    world = 2
+    ref = _spawn(world, tmp_path, "fused")
+    res = _spawn(world, tmp_path, "fused", overlap=True)
+    for r in range(world):
+        for k, v in ref[r].items():
+            if k != "coef":
+                np.testing.assert_array_equal(res[r][k], v, err_msg=f"rank {r} {k}")
 
 
 def test_peer_pool_single_rank_equals_persistent(tmp_path, cuda_device):
