@@ -298,9 +298,9 @@ def test_peer_pool_two_processes_equals_persistent(tmp_path, cuda_device):
 
 
 def test_fused_and_peer_pool_training_across_gpus(tmp_path, cuda_device):
-    """The same two checks with one rank per GPU (NVLink peers): fused
-    training equals the virtual-rank run, and the peer pool equals the
-    all-persistent fused run, bit for bit."""
+    """The same checks with one rank per GPU (NVLink peers): fused training
+    equals the virtual-rank run, and the peer pool and the overlapped fused
+    step equal the all-persistent fused run, bit for bit."""
     world = 2
     _need_gpus(world)
     ref = _spawn(world, tmp_path, "fused", spread=True)
@@ -314,6 +314,11 @@ def test_fused_and_peer_pool_training_across_gpus(tmp_path, cuda_device):
         for k, v in ref[r].items():
             if k.startswith("master"):
                 np.testing.assert_array_equal(res[r][k][:v.size], v, err_msg=f"rank {r} {k}")
+    ov = _spawn(world, tmp_path / "overlap", "fused", spread=True, overlap=True)
+    for r in range(world):
+        for k, v in ref[r].items():
+            if k != "coef":
+                np.testing.assert_array_equal(ov[r][k], v, err_msg=f"overlap rank {r} {k}")
 
 
 def test_nccl_training_across_gpus(tmp_path, cuda_device):
