@@ -35,7 +35,6 @@ import gc
 import json
 import os
 import statistics
-import subprocess
 import sys
 import tempfile
 import time
@@ -49,14 +48,12 @@ import torch  # noqa: E402
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 OUT = os.path.join(REPO, "gpurun_out")
-MEMPLAN = os.path.join(REPO, "build", "memplan")
 
 
 def memplan(*args) -> dict:
-    r = subprocess.run([MEMPLAN, *map(str, args)], capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"memplan {' '.join(map(str, args))}: {r.stderr.strip()}")
-    return json.loads(r.stdout)
+    """One planner command, in process (libptk.so's memplan::run_cli)."""
+    from paper_2406_08334_b200 import planner
+    return json.loads(planner.run_memplan([str(a) for a in args]))
 
 
 def spec_of(shape, n_blocks: int) -> dict:
