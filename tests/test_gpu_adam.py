@@ -213,7 +213,31 @@ TABLE_CASES = {
     "ragged": [1, 7, 0, 8, 1536, 1536 * 148 + 8, 100_003, 5, 4096, 0, 1537],
     "many_small": [12_288 + 8 * i for i in range(64)],
     "one_big": [1536 * 148 * 5 + 24],
+    # more chunks than one launch's table capacity (launched in batches)
+    "over_capacity": [2048 * (1 + i % 5) + 8 * (i % 3) + (i % 7) for i in range(300)],
 }
+
+
+def _random_table(seed: int) -> list[int]:
+    """Seeded random tables: empty, sub-unit, tile-boundary (+-1) and
+    multi-tile chunks, 1..200 of them."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(int(rng.integers(1, 201))):
+        kind = rng.integers(0, 4)
+        if kind == 0:
+            out.append(int(rng.integers(0, 9)))
+        elif kind == 1:
+            out.append(int(rng.integers(9, 5000)))
+        elif kind == 2:
+            out.append(int(2048 * rng.integers(1, 40) + rng.integers(-1, 2)))
+        else:
+            out.append(int(rng.integers(5000, 400_000)))
+    return out
+
+
+for _seed in range(6):
+    TABLE_CASES[f"random{_seed}"] = _random_table(_seed)
 
 
 @pytest.mark.parametrize("case", sorted(TABLE_CASES))

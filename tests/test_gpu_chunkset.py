@@ -31,12 +31,20 @@ def _bf16_bits(t):
     return t.view(torch.int16).cpu().numpy().view(np.uint16)
 
 
+def _random_numels(seed: int) -> list[int]:
+    rng = np.random.default_rng(100 + seed)
+    return [int(x) for x in rng.integers(1, 300_000, int(rng.integers(1, 41)))]
+
+
 @pytest.mark.parametrize("world,numels", [(1, [10_007, 4096]), (2, [10_007, 4096]),
                                           (3, [10_007, 4096]), (4, [10_007, 4096]),
                                           (8, [10_007, 4096]),
                                           # several full TMA tiles per CTA + a partial tile
                                           (2, [2 * 148 * 1024 * 3 + 4104]),
-                                          (8, [8 * 148 * 1024 * 2 + 8 * 1000 + 40])])
+                                          (8, [8 * 148 * 1024 * 2 + 8 * 1000 + 40]),
+                                          # seeded random tables of 1-40 ragged chunks
+                                          (2, _random_numels(0)), (3, _random_numels(1)),
+                                          (5, _random_numels(2)), (8, _random_numels(3))])
 def test_fused_virtual_ranks_bit_exact(cuda_device, world, numels):
     """The fused RS -> Adam -> AG kernel (TMA ring by default) over W virtual
     ranks: every rank's fp32 state and every rank's gathered bf16 chunk
@@ -101,8 +109,8 @@ def test_fused_ldg_variant_bit_exact(cuda_device):
                        env=env, capture_output=True, text=True, timeout=900,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    # 12 small-size cases + the 4 full-size cfg2 cases of the fused exchange
-    assert "16 passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
+    # 16 small-size cases + the 4 full-size cfg2 cases of the fused exchange
+    assert "20 passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
 
 
 def _fused_sets(ch, numels, world, dev):
