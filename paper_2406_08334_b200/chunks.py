@@ -521,34 +521,9 @@ class ChunkSet:
         self.signal = torch.zeros(PTK_MAX, dtype=torch.int32, device=self.device)
         bufs = ([c.grad for c in self.chunks] + [c.param for c in self.chunks] +
                 [self.signal, self.mailbox])
-        mine = []
-        for t in bufs:
-            h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
-            off = ctypes.c_int64()
-            nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
-            mine.append((bytes(h), off.value))
-        torch.cuda.synchronize(self.device)
-        # the physical GPU of every rank (UUID, not an ordinal: ranks may be
-        # isolated with CUDA_VISIBLE_DEVICES) decides the fused kernel once
-        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
-        everyone = [None] * self.world
-        dist.all_gather_object(everyone, (uuid, mine), group=group)
-        same_device = all(u == uuid for u, _ in everyone)
-        everyone = [m for _, m in everyone]
-        self._opened = []
-        ptrs = []  # ptrs[r][k]: rank r's k-th buffer as mapped here
-        for r in range(self.world):
-            row = []
-            for k, (hb, off) in enumerate(everyone[r]):
-                if r == self.rank:
-                    row.append(bufs[k].data_ptr())
-                    continue
-                base = ctypes.c_void_p()
-                nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
-                                            ctypes.byref(base))
-                self._opened.append(base)
-                row.append(base.value + off)
-            ptrs.append(row)
+        # ptrs[r][k]: rank r's k-th buffer as mapped here
+        ptrs, self._opened, same_device = map_peer_buffers(bufs, self.world, self.rank,
+                                                           self.device, group)
         n = len(self.chunks)
         self.peer_grad_ptrs = [arr(*[ptrs[r][ci] for r in range(self.world)]) for ci in range(n)]
         self.peer_param_ptrs = [arr(*[ptrs[r][n + ci] for r in range(self.world)])
@@ -573,6 +548,41 @@ class ChunkSet:
 
 
 PTK_MAX = nat.PTK_MAX_PEERS
+
+
+def map_peer_buffers(bufs: list[torch.Tensor], world: int, rank: int, device, group=None):
+    """Collective: every rank's `bufs` mapped into this process through cudaIpc
+    handles (exchanged over torch.distributed -- plumbing only). Returns
+    (ptrs, opened, same_device): ptrs[r][k] = rank r's k-th buffer as seen
+    here, the opened mappings (for ptk_ipc_close_handle), and whether every
+    rank is on this physical GPU (by UUID, not ordinal: ranks may be isolated
+    with CUDA_VISIBLE_DEVICES)."""
+    import torch.distributed as dist
+    mine = []
+    for t in bufs:
+        h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
+        off = ctypes.c_int64()
+        nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
+        mine.append((bytes(h), off.value))
+    torch.cuda.synchronize(device)
+    uuid = str(torch.cuda.get_device_properties(device).uuid)
+    everyone = [None] * world
+    dist.all_gather_object(everyone, (uuid, mine), group=group)
+    same_device = all(u == uuid for u, _ in everyone)
+    opened, ptrs = [], []
+    for r, (_, handles) in enumerate(everyone):
+        row = []
+        for k, (hb, off) in enumerate(handles):
+            if r == rank:
+                row.append(bufs[k].data_ptr())
+                continue
+            base = ctypes.c_void_p()
+            nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
+                                        ctypes.byref(base))
+            opened.append(base)
+            row.append(base.value + off)
+        ptrs.append(row)
+    return ptrs, opened, same_device
 
 
 class _CudaArray:

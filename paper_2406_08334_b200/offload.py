@@ -46,7 +46,7 @@ from concurrent.futures import ThreadPoolExecutor
 import torch
 
 from . import _native as nat
-from .chunks import AdamHyper, vp
+from .chunks import AdamHyper, map_peer_buffers, vp
 
 BF16 = torch.bfloat16
 
@@ -161,29 +161,7 @@ class ChunkPool:
         self._signals = [torch.zeros(nat.PTK_MAX_PEERS, dtype=torch.int32, device=self.device)
                          for _ in range(2)]
         bufs = list(self.slots) + [self.staging] + self._signals
-        mine = []
-        for t in bufs:
-            h = (ctypes.c_uint8 * nat.PTK_IPC_HANDLE_BYTES)()
-            off = ctypes.c_int64()
-            nat.lib.ptk_ipc_get_handle(vp(t), h, ctypes.byref(off))
-            mine.append((bytes(h), off.value))
-        torch.cuda.synchronize(self.device)
-        everyone = [None] * self.world
-        dist.all_gather_object(everyone, mine, group=group)
-        self._opened = []
-        ptrs = []
-        for r in range(self.world):
-            row = []
-            for k, (hb, off) in enumerate(everyone[r]):
-                if r == self.rank:
-                    row.append(bufs[k].data_ptr())
-                    continue
-                base = ctypes.c_void_p()
-                nat.lib.ptk_ipc_open_handle((ctypes.c_uint8 * len(hb)).from_buffer_copy(hb),
-                                            ctypes.byref(base))
-                self._opened.append(base)
-                row.append(base.value + off)
-            ptrs.append(row)
+        ptrs, self._opened, _ = map_peer_buffers(bufs, self.world, self.rank, self.device, group)
         self._set_peer_tables(ptrs)
         dist.barrier(group=group)
 
