@@ -14,6 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libptk.so")
 
 PTK_OK = 0
+PTK_EINVAL, PTK_ECUDA, PTK_ENCCL, PTK_EUNSUPPORTED = -1, -2, -3, -4   # include/ptk.h
 PTK_MAX_PEERS = 8
 PTK_UNIQUE_ID_BYTES = 128
 PTK_IPC_HANDLE_BYTES = 64

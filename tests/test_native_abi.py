@@ -141,6 +141,36 @@ def test_host_adam_f32grad_bit_exact(mode, offset):
     np.testing.assert_array_equal(pa, pb)
 
 
+def test_peer_exchange_argument_errors_without_a_gpu():
+    """The peer exchange and the symmetric-window entry points validate their
+    arguments before touching the device: loud PTK_EINVAL with the entry
+    point's name (runs on the CPU box)."""
+    from paper_2406_08334_b200 import _native as nat
+    arr = (ctypes.c_void_p * nat.PTK_MAX_PEERS)()
+    out = ctypes.c_void_p(16)
+    cases = [
+        (lambda: nat.raw.ptk_peer_reduce_scatter_f32(None, 2, 0, 8, out, None),
+         "ptk_peer_reduce_scatter_f32"),
+        (lambda: nat.raw.ptk_peer_reduce_scatter_f32(arr, 9, 0, 8, out, None),
+         "ptk_peer_reduce_scatter_f32"),
+        (lambda: nat.raw.ptk_peer_reduce_scatter_f32(arr, 2, 2, 8, out, None),
+         "ptk_peer_reduce_scatter_f32"),
+        (lambda: nat.raw.ptk_peer_reduce_scatter_f32(arr, 2, 0, 8, out, None),   # null peers
+         "null peer"),
+        (lambda: nat.raw.ptk_peer_allgather(None, 2, 0, 16, None), "ptk_peer_allgather"),
+        (lambda: nat.raw.ptk_peer_allgather(arr, 2, 0, -1, None), "ptk_peer_allgather"),
+        (lambda: nat.raw.ptk_peer_allgather(arr, 2, 1, 16, None), "null local buffer"),
+        (lambda: nat.raw.ptk_comm_window_register(None, out, 16, ctypes.byref(ctypes.c_void_p())),
+         "null comm"),
+        (lambda: nat.raw.ptk_comm_mem_alloc(None, 16), "ptk_comm_mem_alloc"),
+        (lambda: nat.raw.ptk_cpu_adam_f32grad(None, None, None, None, None, None, 0, 0, None,
+                                              None), "ptk_cpu_adam_f32grad"),
+    ]
+    for call, what in cases:
+        assert call() == nat.PTK_EINVAL, what
+        assert what in nat.last_error(), (what, nat.last_error())
+
+
 def test_errors_are_reported():
     from paper_2406_08334_b200 import _native as nat
     rc = nat.raw.ptk_cpu_adam(None, None, None, None, None, None, 0, 0, None, None)
