@@ -130,3 +130,22 @@ def test_e2e_pieces_cover_the_chunk(n, piece, up, down):
         assert got[0][1] == 1 << 20
     if down and n > 4 * piece:
         assert got[-1][1] == 1 << 20
+
+
+def test_reference_arm_line_n1():
+    """--impl reference at N=1: the oracle port of the same step on the host
+    cores, same metric / unit / config keys as the GPU arm, e2e = the line's
+    own value with no host<->device bytes."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                        "--workload", "flat32", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["unit"] == "GB/s"
+    assert d["metric"] == bench.METRIC and d["higher_is_better"] is True
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["same_config"] is True
