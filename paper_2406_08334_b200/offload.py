@@ -311,8 +311,9 @@ class ChunkPool:
         if self.reduced_free[b] is not None:    # its previous D2H has read it
             cur.wait_event(self.reduced_free[b])
         out = self.reduced[b]
-        if self.world == 1:
-            nat.lib.ptk_peer_reduce_scatter_f32(self.staging_peers, 1, 0, s, vp(out), _sh(cur))
+        if self.world == 1:   # the "sum" of one rank: the gradient itself, in fp32
+            one = (ctypes.c_void_p * nat.PTK_MAX_PEERS)(grad.data_ptr())
+            nat.lib.ptk_peer_reduce_scatter_f32(one, 1, 0, s, vp(out), _sh(cur))
             return out
         if self.sig_reduce is None:
             raise RuntimeError("exchange='peer' needs attach_ipc_peers() before use")
@@ -329,8 +330,6 @@ class ChunkPool:
         staged = grad   # already padded to shard*world: reduce-scatter / D2H in place
         peer = self.exchange == "peer"
         if peer:
-            if self.world == 1:
-                self.staging_peers[0] = grad.data_ptr()
             reduced = self._reduce_peer(c, grad, cur)
         elif self.comm is not None:
             nat.lib.ptk_chunk_reduce_scatter(self.comm, vp(staged), s, 0, _sh(cur))
