@@ -16,6 +16,7 @@ Disabled (the default: `model.timeline = None`) it costs nothing.
 from __future__ import annotations
 
 import csv
+import json
 import threading
 import time
 
@@ -78,6 +79,23 @@ def write_csv(rows, path: str) -> None:
         w.writerow(["time_ns", "resource", "event", "subject"])
         for ns, resource, event, subject in rows:
             w.writerow([ns, resource, event, subject])
+
+
+def write_chrome_trace(rows, path: str) -> None:
+    """The measured timeline as Chrome-trace instant events, in the exact
+    layout `memplan simulate --timeline` writes for a simulated one
+    (proj/src/sim.cpp:765-797): one thread row per resource in order of
+    first use, ts in microseconds, name "<event> <subject>" -- so a measured
+    and a simulated iteration open side by side in chrome://tracing."""
+    rows_of: dict[str, int] = {}
+    events = []
+    for ns, resource, event, subject in rows:
+        tid = rows_of.setdefault(resource, len(rows_of) + 1)
+        events.append({"name": f"{event} {subject}", "ph": "i", "pid": 1, "s": "t",
+                       "tid": tid, "ts": ns / 1000.0})
+    with open(path, "w") as f:
+        json.dump(events, f, indent=1)
+        f.write("\n")
 
 
 def read_csv(path: str) -> list[tuple[int, str, str, str]]:

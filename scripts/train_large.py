@@ -167,7 +167,8 @@ def record_timeline(model, cs, pool, x, y, hyper, path: str, iters: int = 2) -> 
     (simulator schema, paper_2406_08334_b200.timeline; an `iter_start` event
     marks each), written as CSV; returns the summary of the LAST one (steady
     state: the previous iteration's host Adam overlaps it, as in training)."""
-    from paper_2406_08334_b200.timeline import Timeline, summarize, write_csv
+    from paper_2406_08334_b200.timeline import (Timeline, summarize, write_chrome_trace,
+                                                write_csv)
     from paper_2406_08334_b200.train import train_step
     tl = Timeline()
     model.timeline = cs.timeline = tl
@@ -188,6 +189,7 @@ def record_timeline(model, cs, pool, x, y, hyper, path: str, iters: int = 2) -> 
     if getattr(model, "_swap", None) is not None:
         model._swap.timeline = None
     write_csv(rows, path)
+    write_chrome_trace(rows, path[:-4] + ".chrome.json")   # chrome://tracing, simulator layout
     from paper_2406_08334_b200.timeline import last_iteration
     return {"iterations": iters, "last_iteration": summarize(last_iteration(rows))}
 

@@ -32,3 +32,26 @@ def test_summary_and_csv_round_trip(tmp_path):
     p = str(tmp_path / "t.csv")
     write_csv(tail, p)
     assert read_csv(p) == tail
+
+
+def test_chrome_trace_matches_the_simulators_format(tmp_path):
+    """write_chrome_trace of a timeline equals, event for event, what the
+    planner writes for the same timeline (`memplan simulate --timeline`,
+    read back through its `--timeline-csv`)."""
+    import json
+
+    from paper_2406_08334_b200 import planner
+    from paper_2406_08334_b200.timeline import write_chrome_trace
+    spec = tmp_path / "spec.json"
+    spec.write_text(json.dumps({"hidden_size": 256, "n_blocks": 4, "n_heads": 4,
+                                "vocab_size": 1000, "seq_len": 128}))
+    tpath = planner.trace_file(["--spec", str(spec), "--batch", "4"], str(tmp_path / "t.json"))
+    sim_chrome, sim_csv = tmp_path / "sim.json", tmp_path / "sim.csv"
+    planner.run_memplan(["simulate", "--trace", tpath, "--hw", "a100x1", "--s-chunk", "4194304",
+                         "--n-persist", "1", "--n-buffer", "1", "--timeline", str(sim_chrome),
+                         "--timeline-csv", str(sim_csv)])
+    rows = read_csv(str(sim_csv))
+    assert len(rows) > 10
+    ours = tmp_path / "ours.json"
+    write_chrome_trace(rows, str(ours))
+    assert json.loads(ours.read_text()) == json.loads(sim_chrome.read_text())
