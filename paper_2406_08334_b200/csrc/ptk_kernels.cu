@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cctype>
 #include <cstdint>
 #include <cstdio>
@@ -2038,6 +2039,21 @@ int ptk_peer_reduce_scatter_f32(const uint16_t* const* grad_peers, int32_t world
   return check_cuda(cudaGetLastError(), "peer_reduce_f32_kernel launch");
 }
 
+// Side streams of the peer all-gather: the W-1 pulls run as concurrent
+// copy-engine transfers (one stream per pull, forked from and joined back into
+// the caller's stream by events), created once per device.
+struct PullStreams {
+  std::mutex mu;
+  cudaStream_t s[PTK_MAX_PEERS] = {};
+  cudaEvent_t fork = nullptr, join[PTK_MAX_PEERS] = {};
+  bool ready = false;
+};
+
+PullStreams& pull_streams() {
+  static PullStreams per_dev[kMaxDevices];
+  return per_dev[current_device()];
+}
+
 int ptk_peer_allgather(void* const* buf_peers, int32_t world, int32_t rank, int64_t shard_bytes,
                        void* stream) {
   if (!buf_peers || world < 1 || world > PTK_MAX_PEERS || rank < 0 || rank >= world ||
@@ -2045,15 +2061,32 @@ int ptk_peer_allgather(void* const* buf_peers, int32_t world, int32_t rank, int6
     return fail(PTK_EINVAL, "ptk_peer_allgather: bad arguments");
   char* local = static_cast<char*>(buf_peers[rank]);
   if (!local) return fail(PTK_EINVAL, "ptk_peer_allgather: null local buffer");
+  for (int q = 0; q < world; ++q)
+    if (!buf_peers[q]) return fail(PTK_EINVAL, "ptk_peer_allgather: null peer buffer");
+  if (world == 1 || shard_bytes == 0) return PTK_OK;
   cudaStream_t st = as_stream(stream);
-  // pull: every peer's own shard, rank order from the next rank on (spreads
-  // the W-1 readers of one rank over time); copy-engine transfers, no SMs
+  PullStreams& ps = pull_streams();
+  std::lock_guard<std::mutex> lock(ps.mu);
+  if (!ps.ready) {
+    for (int k = 0; k < PTK_MAX_PEERS; ++k) {
+      PTK_TRY_CUDA(cudaStreamCreateWithFlags(&ps.s[k], cudaStreamNonBlocking));
+      PTK_TRY_CUDA(cudaEventCreateWithFlags(&ps.join[k], cudaEventDisableTiming));
+    }
+    PTK_TRY_CUDA(cudaEventCreateWithFlags(&ps.fork, cudaEventDisableTiming));
+    ps.ready = true;
+  }
+  // pull every peer's own shard, starting from the next rank (spreads the
+  // W-1 readers of one rank), each on its own copy engine stream; no SMs
+  PTK_TRY_CUDA(cudaEventRecord(ps.fork, st));
   for (int k = 1; k < world; ++k) {
     const int q = (rank + k) % world;
-    if (!buf_peers[q]) return fail(PTK_EINVAL, "ptk_peer_allgather: null peer buffer");
     const int64_t off = static_cast<int64_t>(q) * shard_bytes;
+    PTK_TRY_CUDA(cudaStreamWaitEvent(ps.s[k], ps.fork, 0));
     PTK_TRY_CUDA(cudaMemcpyAsync(local + off, static_cast<const char*>(buf_peers[q]) + off,
-                                 static_cast<size_t>(shard_bytes), cudaMemcpyDeviceToDevice, st));
+                                 static_cast<size_t>(shard_bytes), cudaMemcpyDeviceToDevice,
+                                 ps.s[k]));
+    PTK_TRY_CUDA(cudaEventRecord(ps.join[k], ps.s[k]));
+    PTK_TRY_CUDA(cudaStreamWaitEvent(st, ps.join[k], 0));
   }
   return PTK_OK;
 }
