@@ -309,7 +309,9 @@ int ptk_peer_barrier(int32_t* const* signal_peers, int32_t world, int32_t rank,
  *   in fp32 for the host Adam (ptk_cpu_adam_f32grad).
  * ptk_peer_allgather: for every q != rank, copies bytes
  *   [q * shard_bytes, (q+1) * shard_bytes) of buf_peers[q] to the same range
- *   of buf_peers[rank] (copy-engine peer transfers over NVLink on `stream`). */
+ *   of buf_peers[rank]: copy-engine peer transfers over NVLink, the W-1 pulls
+ *   concurrent on internal side streams forked from and joined back into
+ *   `stream` (stream-ordered for the caller). */
 int ptk_peer_reduce_scatter_f32(const uint16_t* const* grad_peers, int32_t world, int32_t rank,
                                 int64_t shard, float* out, void* stream);
 int ptk_peer_allgather(void* const* buf_peers, int32_t world, int32_t rank, int64_t shard_bytes,
